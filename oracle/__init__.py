@@ -1,0 +1,14 @@
+"""CPU oracle for the speculative-replanning path — TEST INFRASTRUCTURE ONLY.
+
+Nothing in ``paper_2605_13778_b200`` imports this package. Only ``tests/``,
+``__graft_entry__.smoke()`` and the ``cpu_baseline`` / ``--impl reference``
+legs of ``bench.py`` may use it, and only as the checker or the timed CPU
+baseline — never as the thing measured or shipped.
+
+* ``specflow_oracle`` — numpy float64 restatement of the reference
+  ``specflow`` hot path (verify / propose / integrate_flow / decision), each
+  function citing the reference file:line it follows. Pinned against golden
+  vectors produced by the real reference (``tests/golden/make_golden.py``).
+* ``pi0_oracle`` — numpy restatement of the pi0-scale Action Expert the
+  builder defined (no reference implementation exists; see its header).
+"""

@@ -1,0 +1,130 @@
+"""ctypes binding of the C-ABI in ``include/specflow_b200.h``.
+
+The shared library is built in-tree (``paper_2605_13778_b200/lib``) by
+``__graft_entry__.build()``. There is no CPU fallback: importing a device entry
+point without the library raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libspecflow_b200.so"
+
+SF_OK, SF_EINVAL, SF_ENONFINITE, SF_ERUNTIME, SF_ECUDA = 0, 1, 2, 3, 4
+SF_F32, SF_F64 = 0, 1
+SF_MAX_LAYERS = 8
+SF_MAX_K = 16
+SF_METRIC = {"l2": 0, "linf": 1}
+SF_RESULT_WORDS = 8
+RES_PREFIX, RES_SWITCH, RES_PATH, RES_PLANNED, RES_NONFINITE = 0, 1, 2, 3, 4
+PATH_CODES = ("flash_accepted", "flash_rejected_fallback", "flash_phase_fallback")
+
+
+class SfMlp(ctypes.Structure):
+    _fields_ = [
+        ("n_layers", ctypes.c_int),
+        ("sizes", ctypes.c_int * (SF_MAX_LAYERS + 1)),
+        ("w", ctypes.c_void_p * SF_MAX_LAYERS),
+        ("b", ctypes.c_void_p * SF_MAX_LAYERS),
+    ]
+
+
+class SfVerifyCfg(ctypes.Structure):
+    _fields_ = [
+        ("k", ctypes.c_int),
+        ("taus", ctypes.c_double * SF_MAX_K),
+        ("delta", ctypes.c_double),
+        ("metric", ctypes.c_int),
+        ("window", ctypes.c_int),
+        ("current_sign", ctypes.c_double),
+        ("phase_fallback", ctypes.c_int),
+        ("prefix_cap", ctypes.c_int),
+        ("replan_size", ctypes.c_int),
+    ]
+
+
+class SfVerifyOut(ctypes.Structure):
+    _fields_ = [
+        ("draft", ctypes.c_void_p),
+        ("reconstructed", ctypes.c_void_p),
+        ("distances", ctypes.c_void_p),
+        ("branch_prefixes", ctypes.c_void_p),
+        ("result", ctypes.c_void_p),
+    ]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_D = ctypes.c_double
+
+# name -> (restype, argtypes); every name here is declared in include/specflow_b200.h
+SIGNATURES = {
+    "sf_last_error": (ctypes.c_char_p, []),
+    "sf_version": (_I, []),
+    "sf_launch_count": (ctypes.c_int64, [_I]),
+    "sf_tiny_flash_round": (_I, [_I, ctypes.POINTER(SfMlp), _P, ctypes.POINTER(SfMlp), _P, _I, _P, _I,
+                                 _P, _I, _I, _I, ctypes.POINTER(SfVerifyCfg),
+                                 ctypes.POINTER(SfVerifyOut), _P]),
+    "sf_tiny_full_round": (_I, [_I, ctypes.POINTER(SfMlp), _P, _I, ctypes.POINTER(SfMlp), _P, _I, _P,
+                                _I, _I, _I, _P, _P, _P, _P]),
+    "sf_tiny_mlp_forward": (_I, [_I, ctypes.POINTER(SfMlp), _P, _I, _P, _P]),
+    "sf_tiny_field_eval": (_I, [_I, ctypes.POINTER(SfMlp), _P, _P, _I, _P, _I, _P, _I, _I, _I, _P,
+                                _P, _P]),
+    "sf_interpolate": (_I, [_I, _P, _P, _P, _I, _I, _P, _P]),
+    "sf_verify_epilogue": (_I, [_I, _P, _P, _P, _I, _I, _I, ctypes.POINTER(SfVerifyCfg),
+                                ctypes.POINTER(SfVerifyOut), _P]),
+    "sf_prefix_length": (_I, [_I, _P, _I, _I, _D, _P, _P]),
+    "sf_continuous_distances": (_I, [_I, _P, _P, _I, _I, _I, _I, _P, _P]),
+    "sf_gripper_switch": (_I, [_I, _P, _I, _I, _I, _D, _I, _P, _P]),
+    "sf_euler_update": (_I, [_I, _P, _P, _I, _I, _I, _P, _P]),
+}
+
+_lib = None
+
+
+class LibraryMissing(RuntimeError):
+    pass
+
+
+def lib():
+    """Load the library once; fail loudly if it is missing (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        path = os.environ.get("SPECFLOW_B200_LIB", str(_LIB_PATH))
+        if not Path(path).exists():
+            raise LibraryMissing(
+                f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        handle = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map C-ABI status codes to the reference's exception types."""
+    if rc == SF_OK:
+        return
+    msg = lib().sf_last_error().decode(errors="replace")
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == SF_EINVAL:
+        raise ValueError(msg)
+    if rc == SF_ENONFINITE:
+        raise FloatingPointError(msg)
+    raise RuntimeError(msg)
+
+
+def host_doubles(vals):
+    """HOST double array for the C-ABI's `const double*` host arguments."""
+    return (ctypes.c_double * len(vals))(*[float(v) for v in vals])
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(lib().sf_launch_count(1 if reset else 0))
