@@ -56,10 +56,13 @@ extern "C" {
 #define SF_RES_NONFINITE 4 /* first branch index with non-finite v/recon, else -1 */
 #define SF_RESULT_WORDS 8
 
-/* Tanh MLP (nets.py:16-44): weights (n_out, n_in) row-major, biases (n_out). */
+/* Tanh MLP (nets.py:16-44): weights (n_out, n_in) row-major with row stride
+ * ld[l] >= n_in elements (0 means n_in; a 16-byte multiple lets the kernels
+ * stage the layer into shared memory with TMA bulk copies), biases (n_out). */
 typedef struct {
   int n_layers;
   int sizes[SF_MAX_LAYERS + 1];
+  int ld[SF_MAX_LAYERS];
   const void* w[SF_MAX_LAYERS]; /* device */
   const void* b[SF_MAX_LAYERS]; /* device */
 } sf_mlp_t;

@@ -27,6 +27,7 @@ class SfMlp(ctypes.Structure):
     _fields_ = [
         ("n_layers", ctypes.c_int),
         ("sizes", ctypes.c_int * (SF_MAX_LAYERS + 1)),
+        ("ld", ctypes.c_int * SF_MAX_LAYERS),
         ("w", ctypes.c_void_p * SF_MAX_LAYERS),
         ("b", ctypes.c_void_p * SF_MAX_LAYERS),
     ]

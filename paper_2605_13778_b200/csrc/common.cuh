@@ -30,6 +30,11 @@ void count_launch(int n = 1);
     }                                 \
   } while (0)
 
+#define SF_DISPATCH(prec, FN, ...)                              \
+  ((prec) == SF_F32   ? FN<float>(__VA_ARGS__)                  \
+   : (prec) == SF_F64 ? FN<double>(__VA_ARGS__)                 \
+                      : (::sf::set_error("unknown precision %d", prec), SF_EINVAL))
+
 // ---- exact (non-contracted) scalar ops so element-wise steps round exactly
 // like the reference's numpy expressions -----------------------------------
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }

@@ -75,9 +75,16 @@ class DeviceMlp:
         self.desc.n_layers = len(net.weights)
         for i, s in enumerate(net.sizes):
             self.desc.sizes[i] = s
+        dt = _device.tdtype()
+        pad = 16 // torch.empty(0, dtype=dt).element_size()
         for i, (w, b) in enumerate(zip(net.weights, net.biases)):
-            tw, tb = _device.to_dev(w), _device.to_dev(b)
+            w = np.asarray(w, dtype=np.float64)
+            ld = -(-w.shape[1] // pad) * pad  # rows padded to 16 B for TMA bulk staging
+            wp = np.zeros((w.shape[0], ld))
+            wp[:, : w.shape[1]] = w
+            tw, tb = _device.to_dev(wp), _device.to_dev(b)
             self.tensors += [tw, tb]
+            self.desc.ld[i] = ld
             self.desc.w[i] = tw.data_ptr()
             self.desc.b[i] = tb.data_ptr()
 
