@@ -1,0 +1,29 @@
+/*
+ * specflow_b200 internal kernel entry points — unit-test hooks for the
+ * pi0-scale building blocks (not part of the reference-facing boundary).
+ * Same conventions as specflow_b200.h.
+ */
+#ifndef SPECFLOW_B200_INTERNAL_H
+#define SPECFLOW_B200_INTERNAL_H
+
+#include "specflow_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* D[m, n] = sum_k A[m|n, k] B[n|m, k] through the tcgen05 GEMM (bf16 in, fp32
+ * accumulate). swap_ab=0: A rows are output rows m, B rows are features n;
+ * swap_ab=1: A rows are features n, B rows are output rows m. epi_kind 0 stores
+ * fp32, 1 stores bf16; if `ssq` is non-NULL each output row m is scaled by
+ * rsqrt(sum_g ssq[g*ssq_ld + m] * inv_width + 1e-6) (RMSNorm folded into the
+ * epilogue). splits <= 0 picks split-K automatically. Synchronises `stream`. */
+int sf_dbg_gemm(const void* A, int rows_a, const void* B, int rows_b, int K, int bn, int splits,
+                int swap_ab, int epi_kind, void* out, int ld_out, int M_valid, int N_valid,
+                const float* ssq, int ssq_groups, int ssq_ld, float inv_width, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

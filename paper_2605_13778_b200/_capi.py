@@ -81,6 +81,9 @@ SIGNATURES = {
     "sf_continuous_distances": (_I, [_I, _P, _P, _I, _I, _I, _I, _P, _P]),
     "sf_gripper_switch": (_I, [_I, _P, _I, _I, _I, _D, _I, _P, _P]),
     "sf_euler_update": (_I, [_I, _P, _P, _I, _I, _I, _P, _P]),
+    # include/specflow_b200_internal.h (kernel unit-test hooks)
+    "sf_dbg_gemm": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I, _P, _I, _I,
+                         ctypes.c_float, _P]),
 }
 
 _lib = None

@@ -46,6 +46,7 @@ struct DevMlp {
   const T* w[SF_MAX_LAYERS];
   const T* b[SF_MAX_LAYERS];
   int woff[SF_MAX_LAYERS];  // element offset of this CTA's slice in the SMEM arena; -1 = global
+  int boff[SF_MAX_LAYERS];  // element offset of this CTA's bias slice (always resident)
 };
 
 template <typename T>
@@ -97,6 +98,17 @@ __device__ void init_bars(const DevMlp<T>& m, uint64_t* bars) {
   if (threadIdx.x != 0) return;
   for (int l = 0; l < m.n_layers; ++l)
     if (m.woff[l] >= 0) sm100::mbar_init(&bars[l], 1);
+}
+
+// Bias slices go to SMEM once per launch (no global load on the layer path).
+template <typename T>
+__device__ void stage_biases(const DevMlp<T>& m, T* arena, int rank, int csize) {
+  for (int l = 0; l < m.n_layers; ++l) {
+    int r0, r1;
+    slice_rows(m.sizes[l + 1], rank, csize, r0, r1);
+    for (int j = r0 + (int)threadIdx.x; j < r1; j += blockDim.x)
+      arena[m.boff[l] + (j - r0)] = __ldg(m.b[l] + j);
+  }
 }
 
 // One layer for `rows` activation rows. in: this CTA's SMEM [rows][n_in];
@@ -159,7 +171,7 @@ __device__ void cluster_layer(cg::cluster_group& cluster, const DevMlp<T>& m, in
 #pragma unroll
     for (int r = 0; r < kMaxRows; ++r)
       if (r == lane) mine = acc[r];
-    T z = add_rn(mine, __ldg(m.b[l] + j));  // z = a @ W.T + b (nets.py:103)
+    T z = add_rn(mine, arena[m.boff[l] + (j - r0)]);  // z = a @ W.T + b (nets.py:103)
     if (act) z = tanh_t(z);                  // tanh on hidden layers (nets.py:104)
     for (int r = 0; r < rows; ++r) {
       const T v = __shfl_sync(0xffffffffu, z, r);
@@ -225,6 +237,9 @@ __device__ void prologue(cg::cluster_group& cluster, const Frame<T>& f, const De
   const int rank = (int)cluster.block_rank(), csize = (int)cluster.num_blocks();
   stage_weights(n0, f.arena, f.bars0, rank, csize);
   if (n1) stage_weights(*n1, f.arena, f.bars1, rank, csize);
+  stage_biases(n0, f.arena, rank, csize);
+  if (n1) stage_biases(*n1, f.arena, rank, csize);
+  __syncthreads();
 }
 
 // ------------------------------------------------------------ flash round
@@ -335,6 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiny_full_round_kernel(const Full
   const Frame<T> f = frame<T>(smem_raw, p.buf_elems, p.extra_elems);
   T* s_emb = f.extra;
   T* s_vals = s_emb + p.emb_dim;
+  T* s_state = s_vals + p.H * p.D;
   __shared__ int s_bad, s_bad_v;
   const int HD = p.H * p.D;
   prologue<T>(cluster, f, p.field, p.has_enc ? &p.enc : nullptr);
@@ -354,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiny_full_round_kernel(const Full
     for (int i = threadIdx.x; i < p.emb_dim; i += blockDim.x) s_emb[i] = p.enc_in[i];
   }
   for (int i = threadIdx.x; i < HD; i += blockDim.x) s_vals[i] = p.start[i];
+  for (int i = threadIdx.x; i < p.state_dim; i += blockDim.x) s_state[i] = p.state[i];
   if (threadIdx.x == 0) {
     s_bad = -1;
     s_bad_v = 0;
@@ -372,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiny_full_round_kernel(const Full
       if (i < HD) v = s_vals[i];
       else if (i == HD) v = tau;
       else if (i < HD + 1 + p.emb_dim) v = s_emb[i - HD - 1];
-      else v = p.state[i - HD - 1 - p.emb_dim];
+      else v = s_state[i - HD - 1 - p.emb_dim];
       f.bufA[i] = v;
     }
     __syncthreads();
@@ -507,6 +524,13 @@ template <typename T>
 size_t plan_arena(DevMlp<T>* first, DevMlp<T>* second, size_t fixed, int csize) {
   size_t off = 0;  // elements
   DevMlp<T>* order[2] = {first, second};
+  for (DevMlp<T>* m : order) {  // biases first: always resident
+    if (!m) continue;
+    for (int l = 0; l < m->n_layers; ++l) {
+      m->boff[l] = (int)off;
+      off += ((m->sizes[l + 1] + csize - 1) / csize + 15) & ~15;
+    }
+  }
   for (DevMlp<T>* m : order) {
     if (!m) continue;
     for (int l = 0; l < m->n_layers; ++l) {
@@ -526,11 +550,28 @@ size_t plan_arena(DevMlp<T>* first, DevMlp<T>* second, size_t fixed, int csize) 
 
 int g_cluster16 = -1;  // 1 if 16-CTA clusters are schedulable, 0 if not, -1 unknown
 
+// Per-kernel attribute cache: cudaFuncSetAttribute costs microseconds of host
+// time, which would otherwise sit on the launch path of a ~10 us round.
+template <typename K>
+int ensure_attrs(K kern, size_t smem, int csize) {
+  static size_t max_smem = 0;
+  static bool nonportable = false;
+  if (smem > max_smem) {
+    SF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kSmemBudget));
+    max_smem = kSmemBudget;
+  }
+  if (csize > 8 && !nonportable) {
+    SF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    nonportable = true;
+  }
+  return SF_OK;
+}
+
 template <typename K>
 int launch_cluster(K kern, const void* params_ptr, size_t smem, cudaStream_t stream, int csize) {
-  SF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (csize > 8)
-    SF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  int rc = ensure_attrs(kern, smem, csize);
+  if (rc) return rc;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(csize);
   cfg.blockDim = dim3(kThreads);
@@ -699,7 +740,7 @@ int full_round_impl(const sf_mlp_t* enc, const void* enc_in, int emb_dim, const 
   DevMlp<T>* first = field_net ? &p.field : &p.enc;
   DevMlp<T>* second = (field_net && enc) ? &p.enc : nullptr;
   return plan_and_launch<T>(tiny_full_round_kernel<T>, p, first, second, width,
-                            emb_dim + H * D, stream);
+                            emb_dim + H * D + state_dim, stream);
 }
 
 template <typename T>
