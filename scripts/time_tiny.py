@@ -1,6 +1,13 @@
-"""Quick device timing of the tiny-path kernels (cfg1 shapes), CUDA events."""
+"""Device timing of the tiny-path kernels (cfg1 shapes), CUDA events.
 
+Reports (a) single-launch latency (event pair around one launch, includes the
+host submit), (b) back-to-back throughput (1000 launches between two events),
+(c) the python API end-to-end round, and the SM clock seen while looping.
+"""
+
+import subprocess
 import sys
+import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
@@ -13,6 +20,15 @@ from paper_2605_13778_b200.actions import ChannelLayout
 from paper_2605_13778_b200.flowpolicy import ConditioningCache, VelocityField
 from paper_2605_13778_b200.nets import init_mlp
 from paper_2605_13778_b200.verifier import VerifierConfig, make_cfg, tiny_flash_round
+
+
+def sm_clock():
+    try:
+        out = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=10).stdout.strip()
+        return out
+    except Exception:
+        return "?"
 
 
 def main():
@@ -46,13 +62,14 @@ def main():
                                                     emb.data_ptr(), 39, state.data_ptr(), 3,
                                                     eps.data_ptr(), h, d, 6, cfg, o, s))
 
-            def full():
+            def full(n=10):
                 _capi.check(lib.sf_tiny_full_round(_device.code(), ed, feats.data_ptr(), 39, fd,
-                                                   state.data_ptr(), 3, eps.data_ptr(), h, d, 10,
+                                                   state.data_ptr(), 3, eps.data_ptr(), h, d, n,
                                                    out.data_ptr(), None, words.data_ptr(), s))
 
-            for name, fn in (("spec", spec), ("full", full)):
-                for _ in range(20):
+            for name, fn in (("spec", spec), ("full", full), ("full_n1", lambda: full(1)),
+                             ("encode_only", lambda: full(0))):
+                for _ in range(50):
                     fn()
                 torch.cuda.synchronize()
                 times = []
@@ -63,17 +80,23 @@ def main():
                     b.record()
                     b.synchronize()
                     times.append(a.elapsed_time(b) * 1e3)
-                print(f"{prec} {name}: p50 {np.median(times):.1f} us  min {np.min(times):.1f} us")
-            # host API end-to-end (python, staging, sync)
-            import time
-
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                n = 2000
+                a.record()
+                for _ in range(n):
+                    fn()
+                b.record()
+                clk = sm_clock()
+                b.synchronize()
+                print(f"{prec} {name:12s}: single p50 {np.median(times):7.1f} us | back-to-back "
+                      f"{a.elapsed_time(b) * 1e3 / n:7.1f} us/launch | sm clock {clk} MHz")
             fe, em, st, ep = (np.asarray(x.cpu(), np.float64) for x in (feats, emb, state, eps))
             vcfg = VerifierConfig(timesteps=(0.25, 0.5, 0.75), delta=1.42)
             cache = ConditioningCache(em)
-            for _ in range(10):
+            for _ in range(20):
                 tiny_flash_round(field, draft_net, fe, cache, st, ep.reshape(h, d), vcfg, -1.0, lay)
             t = []
-            for _ in range(200):
+            for _ in range(300):
                 t0 = time.perf_counter()
                 tiny_flash_round(field, draft_net, fe, cache, st, ep.reshape(h, d), vcfg, -1.0, lay)
                 t.append((time.perf_counter() - t0) * 1e6)
