@@ -1,0 +1,98 @@
+/*
+ * specflow_b200 — pi0-scale Action Expert entry points (BASELINE configs 3-5).
+ *
+ * The reference has no pi0-scale model (SPEC.md:155 substitutes MLPs); these
+ * entry points implement the reference's field protocol
+ * (flowpolicy.py:249-261) and the verify / integrate_flow contracts
+ * (verifier.py:109-150, flowpolicy.py:273-292) for the builder-defined Action
+ * Expert (oracle/pi0_oracle.py). Same conventions as
+ * specflow_b200.h. All array arguments are DEVICE pointers unless noted.
+ */
+#ifndef SPECFLOW_B200_PI0_H
+#define SPECFLOW_B200_PI0_H
+
+#include <stdint.h>
+
+#include "specflow_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SF_AE_MAX_LAYERS 32
+
+#define SF_AE_GRAPH 1 /* capture/replay the round as a CUDA graph */
+#define SF_AE_PDL 2   /* programmatic dependent launch between kernels */
+
+typedef struct {
+  int width;       /* 1024 */
+  int layers;      /* 18 */
+  int q_heads;     /* 8 (one shared KV head, head_dim 256) */
+  int head_dim;    /* 256 (fixed by the kernels) */
+  int mlp;         /* 4096 (GeGLU) */
+  int action_dim;  /* D = 32; gripper = last channel */
+  int state_dim;   /* 32 */
+  int horizon;     /* H = 50 (suffix = 1 state + H action tokens) */
+  int prefix_len;  /* P = 800 prefix KV tokens */
+  float eps;       /* RMSNorm epsilon */
+  float temb_min_period, temb_max_period;
+} sf_ae_config_t;
+
+/* Device weights in DEVICE layout (see paper_2605_13778_b200/pi0.py):
+ *  a_w [W, D] f32, a_b [W] f32      action_in
+ *  s_w [W, S] f32, s_b [W] f32      state_proj
+ *  t1_w, t2_w [W, W] f32, t1_b, t2_b [W] f32   time MLP
+ *  out_w [D, W] bf16, out_b [D] f32 action head
+ *  qkv[l] [(heads+2)*256, W] bf16   q/k rows interleaved (dim i, dim i+128)
+ *  o[l] [W, heads*256] bf16
+ *  gu[l] [2*mlp, W] bf16            rows interleaved (gate_i, up_i)
+ *  down[l] [W, mlp] bf16
+ *  rope [(P + 1 + H) * 128] float2 (cos, sin) */
+typedef struct {
+  const void *a_w, *a_b, *s_w, *s_b, *t1_w, *t1_b, *t2_w, *t2_b, *out_w, *out_b;
+  const void* qkv[SF_AE_MAX_LAYERS];
+  const void* o[SF_AE_MAX_LAYERS];
+  const void* gu[SF_AE_MAX_LAYERS];
+  const void* down[SF_AE_MAX_LAYERS];
+  const void* rope;
+} sf_ae_weights_t;
+
+int sf_ae_create(const sf_ae_config_t* cfg, const sf_ae_weights_t* weights, void** handle);
+int sf_ae_destroy(void* handle);
+
+/* Bind the prefix KV pool (the VLM prefill output, flowpolicy.py:38-50 cache):
+ * k_prefix [L][n_envs][P][256] bf16, vt_prefix [L][n_envs][256][P] bf16. Env
+ * e of a batched call attends to pool entry e. */
+int sf_ae_set_prefix(void* handle, const void* k_prefix, const void* vt_prefix, int n_envs);
+
+/* Batched speculative verification (verifier.py:109-150 + runtime.py:286-320)
+ * for n_envs envs: draft, eps [n_envs][H][D] f32, state [n_envs][S] f32,
+ * signs [n_envs] f32 (NULL: cfg->current_sign). Outputs (each may be NULL
+ * except branch_prefixes/result): reconstructed [n_envs][K][H][D] f32,
+ * distances [n_envs][K][H] f32, branch_prefixes [n_envs][K], result
+ * [n_envs][SF_RESULT_WORDS]. */
+int sf_ae_verify(void* handle, int n_envs, const sf_verify_cfg_t* cfg, const float* draft,
+                 const float* eps, const float* state, const float* signs,
+                 const sf_verify_out_t* out, int flags, void* stream);
+
+/* Batched full path (flowpolicy.py:273-292): `start` = A^0 [n_envs][H][D];
+ * chunk_out [n_envs][H][D]; status [n_envs][2] = {first non-finite step or -1,
+ * 1 if a velocity was non-finite}. */
+int sf_ae_denoise(void* handle, int n_envs, int num_steps, const float* start, const float* state,
+                  float* chunk_out, int* status, int flags, void* stream);
+
+/* Field protocol: velocities for n_envs x rows states x [..][rows][H][D] at
+ * taus[rows] (HOST). */
+int sf_ae_velocity(void* handle, int n_envs, int rows, const float* x, const double* taus,
+                   const float* state, float* v_out, void* stream);
+
+/* Counter-based initialiser shared bit-for-bit with oracle/pi0_oracle.py
+ * (hash_uniform): dst[i] = U(-std*sqrt(3), std*sqrt(3)) from (seed, tid, i). */
+int sf_fill_hash_uniform(void* dst, int is_bf16, int64_t n, uint64_t seed, uint64_t tid, double std,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -81,6 +81,16 @@ SIGNATURES = {
     "sf_continuous_distances": (_I, [_I, _P, _P, _I, _I, _I, _I, _P, _P]),
     "sf_gripper_switch": (_I, [_I, _P, _I, _I, _I, _D, _I, _P, _P]),
     "sf_euler_update": (_I, [_I, _P, _P, _I, _I, _I, _P, _P]),
+    # include/specflow_b200_pi0.h
+    "sf_ae_create": (_I, [_P, _P, _P]),
+    "sf_ae_destroy": (_I, [_P]),
+    "sf_ae_set_prefix": (_I, [_P, _P, _P, _I]),
+    "sf_ae_verify": (_I, [_P, _I, ctypes.POINTER(SfVerifyCfg), _P, _P, _P, _P,
+                          ctypes.POINTER(SfVerifyOut), _I, _P]),
+    "sf_ae_denoise": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, _P]),
+    "sf_ae_velocity": (_I, [_P, _I, _I, _P, _P, _P, _P, _P]),
+    "sf_fill_hash_uniform": (_I, [_P, _I, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64,
+                                  ctypes.c_double, _P]),
     # include/specflow_b200_internal.h (kernel unit-test hooks)
     "sf_dbg_gemm": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I, _P, _I, _I,
                          ctypes.c_float, _P]),

@@ -1,0 +1,388 @@
+// MQA attention of the Action Expert's suffix tokens against the shared VLM
+// prefix KV cache + the branch's own suffix keys (sm_100a, tcgen05 + TMA).
+//
+// Query rows are (token, head) pairs: row = token * 8 + head, so the Q
+// activations [M, 8*256] are a contiguous [M*8, 256] K-major matrix and one
+// 128-row tile = 16 tokens x 8 heads. All 8 heads share the single KV head
+// (MQA), so every query tile multiplies the SAME 64-key K/V blocks:
+//   S = Q K^T   (UMMA 128 x 64 x 256, fp32 in TMEM, double-buffered)
+//   online softmax in registers (one thread per query row, exp2 with the
+//   1/sqrt(d) scale folded in, lazy rescale when the row max grows by > 2^8)
+//   O += P V    (UMMA 128 x 256 x 64; P bf16 via SMEM, V^T K-major from TMA)
+// Keys = the env's P prefix keys (13 blocks of 64) + 2 blocks covering the
+// suffix tokens of the (at most two) branch segments the tile touches, with
+// the paper's block mask: the state token sees the
+// prefix and itself, action tokens see the prefix and their branch's whole
+// suffix. Batch-1 rounds split the key blocks across CTAs (split-KV) and the
+// last CTA of each tile merges the partials in a fixed order.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "sm100.cuh"
+
+namespace sf {
+namespace attn {
+
+constexpr int kThreads = 192;
+constexpr int BQ = 128;     // query rows per tile (16 tokens x 8 heads)
+constexpr int BKEY = 64;    // keys per block
+constexpr int HD = 256;     // head dim
+constexpr int kHeads = 8;
+constexpr uint32_t kQBytes = BQ * HD * 2;         // 64 KB
+constexpr uint32_t kKBytes = BKEY * HD * 2;       // 32 KB (4 chunks of 64 x 64)
+constexpr uint32_t kVBytes = HD * BKEY * 2;       // 32 KB (V^T: 256 x 64)
+constexpr uint32_t kPBytes = BQ * BKEY * 2;       // 16 KB
+constexpr uint32_t kStageBytes = kKBytes + kVBytes;
+constexpr uint32_t kSmemBytes = kQBytes + 2 * kStageBytes + kPBytes + 1024 /*bars*/ + 1024 /*align*/;
+constexpr int kTmemCols = 512;  // S0 [0,64) S1 [64,128) O [128,384)
+
+struct Params {
+  int M;            // valid token rows
+  int env_rows;     // rows per env (multiple of 16)
+  int seg_len;      // tokens per branch segment (1 + H)
+  int segs;         // branches per env (K)
+  int prefix_len;   // P
+  int n_prefix_blocks;
+  int n_blocks;     // n_prefix_blocks + 2
+  int blocks_per_split;
+  int splits;
+  int tiles;
+  float scale_log2;  // log2(e) / sqrt(HD)
+  __nv_bfloat16* out;  // [M, 8*256]
+  float* ws;           // [tiles][splits][128][HD + 2]
+  int* counters;       // [tiles]
+};
+
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0,
+                                            int c1, int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(sm100::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(sm100::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "l"(policy)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kp,
+                const __grid_constant__ CUtensorMap tm_vp, const __grid_constant__ CUtensorMap tm_ks,
+                const __grid_constant__ CUtensorMap tm_vs, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + kQBytes;                      // 2 stages of [K 32KB | V 32KB]
+  uint8_t* sP = sKV + 2 * kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kPBytes);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* s_free = bars + 7;    // [2]
+  uint64_t* p_full = bars + 9;
+  uint64_t* pv_done = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x, split = blockIdx.y;
+  const int m0 = tile * 16;                 // first token of the tile
+  const int env = m0 / p.env_rows;
+  const int env_start = env * p.env_rows;
+  const int seg_first = (m0 - env_start) / p.seg_len;
+  const int sb = env_start + seg_first * p.seg_len;  // first suffix key token
+  const int j0 = split * p.blocks_per_split;
+  const int nb = min(p.blocks_per_split, p.n_blocks - j0);
+
+  if (warp == 0 && lane == 0) {
+    sm100::mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&kv_full[s], 1);
+      sm100::mbar_init(&kv_empty[s], 1);
+      sm100::mbar_init(&s_full[s], 1);
+      sm100::mbar_init(&s_free[s], 128);
+    }
+    sm100::mbar_init(p_full, 128);
+    sm100::mbar_init(pv_done, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<kTmemCols>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (sm100::elect_one()) {
+      sm100::tma_prefetch_desc(&tm_q);
+      sm100::tma_prefetch_desc(&tm_kp);
+      sm100::tma_prefetch_desc(&tm_vp);
+      sm100::tma_prefetch_desc(&tm_ks);
+      sm100::tma_prefetch_desc(&tm_vs);
+      const uint64_t pol_keep = sm100::policy_evict_last();
+      auto load_block = [&](int i, bool prefix_only) -> bool {
+        const int j = j0 + i;
+        const bool is_prefix = j < p.n_prefix_blocks;
+        if (prefix_only && !is_prefix) return false;
+        const int s = i & 1;
+        uint8_t* st = sKV + s * kStageBytes;
+        sm100::mbar_arrive_expect_tx(&kv_full[s], kStageBytes);
+        if (is_prefix) {
+          for (int c = 0; c < 4; ++c)
+            tma_load_3d(&tm_kp, &kv_full[s], st + c * (BKEY * 128), c * 64, j * BKEY, env, pol_keep);
+          tma_load_3d(&tm_vp, &kv_full[s], st + kKBytes, j * BKEY, 0, env, pol_keep);
+        } else {
+          const int row0 = sb + (j - p.n_prefix_blocks) * BKEY;
+          for (int c = 0; c < 4; ++c)
+            sm100::tma_load_2d(&tm_ks, &kv_full[s], st + c * (BKEY * 128), c * 64, row0, pol_keep);
+          sm100::tma_load_2d(&tm_vs, &kv_full[s], st + kKBytes, row0, 0, pol_keep);
+        }
+        return true;
+      };
+      // prefix K/V do not depend on the previous kernel: issue before the PDL wait
+      int issued = 0;
+      while (issued < min(2, nb) && load_block(issued, true)) ++issued;
+      sm100::pdl_wait();
+      sm100::mbar_arrive_expect_tx(q_full, kQBytes);
+      for (int c = 0; c < 4; ++c)
+        sm100::tma_load_2d(&tm_q, q_full, sQ + c * (BQ * 128), c * 64, m0 * kHeads, pol_keep);
+      for (int i = issued; i < nb; ++i) {
+        if (i >= 2) sm100::mbar_wait(&kv_empty[i & 1], ((i >> 1) & 1) ^ 1);
+        load_block(i, false);
+      }
+    }
+  } else if (warp == 1) {
+    if (sm100::elect_one()) {
+      const uint32_t idesc_s = sm100::make_idesc_bf16(BQ, BKEY);
+      const uint32_t idesc_o = sm100::make_idesc_bf16(BQ, HD);
+      const uint32_t q_addr = sm100::smem_u32(sQ);
+      const uint32_t p_addr = sm100::smem_u32(sP);
+      sm100::mbar_wait(q_full, 0);
+      auto issue_pv = [&](int i) {
+        sm100::mbar_wait(p_full, i & 1);
+        sm100::tc_fence_after();
+        const uint32_t v_addr = sm100::smem_u32(sKV + (i & 1) * kStageBytes + kKBytes);
+#pragma unroll
+        for (int kk = 0; kk < BKEY / 16; ++kk)
+          sm100::umma_bf16(tmem + 128, sm100::make_sw128_desc(p_addr + kk * 32),
+                           sm100::make_sw128_desc(v_addr + kk * 32), idesc_o, (i | kk) != 0);
+        sm100::umma_commit(pv_done);
+        sm100::umma_commit(&kv_empty[i & 1]);
+      };
+      for (int i = 0; i < nb; ++i) {
+        const int s = i & 1;
+        sm100::mbar_wait(&kv_full[s], (i >> 1) & 1);
+        if (i >= 2) sm100::mbar_wait(&s_free[s], ((i >> 1) & 1) ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t k_addr = sm100::smem_u32(sKV + s * kStageBytes);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const int c = kk >> 2, w = kk & 3;
+          sm100::umma_bf16(tmem + s * BKEY, sm100::make_sw128_desc(q_addr + c * (BQ * 128) + w * 32),
+                           sm100::make_sw128_desc(k_addr + c * (BKEY * 128) + w * 32), idesc_s,
+                           kk != 0);
+        }
+        sm100::umma_commit(&s_full[s]);
+        if (i >= 1) issue_pv(i - 1);
+      }
+      if (nb > 0) issue_pv(nb - 1);
+    }
+    __syncwarp();
+  } else {
+    // -------------------------------------------- softmax + correction + epilogue
+    const int q = warp & 3;
+    const int r = q * 32 + lane;  // query row in the tile == TMEM lane
+    const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
+    const int tok = m0 + (r >> 3);
+    const int head = r & 7;
+    const int local_q = tok - env_start;
+    const int seg_q = local_q / p.seg_len;
+    const int t_q = local_q - seg_q * p.seg_len;
+    const bool real_q = local_q < p.segs * p.seg_len && tok < p.M;
+    float m_used = -INFINITY, l_sum = 0.f;
+    sm100::pdl_wait();
+    if (r == 0) sm100::pdl_launch_dependents();
+    for (int i = 0; i < nb; ++i) {
+      const int j = j0 + i;
+      const int s = i & 1;
+      sm100::mbar_wait(&s_full[s], (i >> 1) & 1);
+      sm100::tc_fence_after();
+      uint32_t raw[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sm100::tmem_ld16(t_lane + s * BKEY + c * 16, raw[c]);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&s_free[s]);
+      float sv[64];
+      float mb = -INFINITY;
+      const bool is_prefix = j < p.n_prefix_blocks;
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        bool valid;
+        if (is_prefix) {
+          valid = j * BKEY + c < p.prefix_len;
+        } else {
+          const int kt = sb + (j - p.n_prefix_blocks) * BKEY + c - env_start;
+          const int seg_k = kt / p.seg_len;
+          valid = real_q && kt < p.segs * p.seg_len && seg_k == seg_q &&
+                  (t_q >= 1 || kt - seg_k * p.seg_len == 0);
+        }
+        const float x = __uint_as_float(raw[c >> 4][c & 15]) * p.scale_log2;
+        sv[c] = valid ? x : -INFINITY;
+        mb = fmaxf(mb, sv[c]);
+      }
+      const float m_new = fmaxf(m_used, mb);
+      bool rescale = false;
+      float alpha = 1.f;
+      if (m_new > -INFINITY) {
+        if (m_used == -INFINITY) {
+          m_used = m_new;  // nothing accumulated yet: O and l are still zero
+        } else if (m_new > m_used + 8.f) {
+          alpha = exp2f(m_used - m_new);
+          m_used = m_new;
+          rescale = true;
+        }
+      }
+      // P(i) overwrites P(i-1) and O may be rescaled: PV(i-1) must be done
+      if (i >= 1) {
+        sm100::mbar_wait(pv_done, (i - 1) & 1);
+        sm100::tc_fence_after();
+      }
+      if (__any_sync(0xffffffffu, rescale) && i >= 1) {
+        l_sum *= alpha;
+#pragma unroll 1
+        for (int c0 = 0; c0 < HD; c0 += 16) {
+          uint32_t o[16];
+          sm100::tmem_ld16(t_lane + 128 + c0, o);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 16; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+          sm100::tmem_st16(t_lane + 128 + c0, o);
+        }
+        sm100::tmem_st_wait();
+      } else if (rescale) {
+        l_sum *= alpha;
+      }
+      // P row (64 keys, bf16) into the SWIZZLE_128B K-major tile: 16 B chunk c
+      // of row r lives at chunk (c ^ (r & 7)).
+      uint8_t* prow = sP + r * 128;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float p0 = m_used == -INFINITY ? 0.f : exp2f(sv[c * 8 + 2 * k] - m_used);
+          const float p1 = m_used == -INFINITY ? 0.f : exp2f(sv[c * 8 + 2 * k + 1] - m_used);
+          l_sum += p0 + p1;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+          w[k] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      fence_async_smem();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(p_full);
+    }
+    // ---- epilogue: O row (256 fp32) is final once the last PV retires
+    if (nb > 0) {
+      sm100::mbar_wait(pv_done, (nb - 1) & 1);
+      sm100::tc_fence_after();
+    }
+    if (p.splits == 1) {
+      const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
+      __nv_bfloat16* dst = p.out + (size_t)tok * (kHeads * HD) + head * HD;
+      for (int c0 = 0; c0 < HD; c0 += 16) {
+        uint32_t o[16];
+        sm100::tmem_ld16(t_lane + 128 + c0, o);
+        sm100::tmem_ld_wait();
+        uint32_t w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[2 * k]) * inv,
+                                                    __uint_as_float(o[2 * k + 1]) * inv);
+          w[k] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        if (tok < p.M) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
+          d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      }
+    } else {
+      constexpr int kRow = HD + 2;
+      float* mine = p.ws + (((size_t)tile * p.splits + split) * BQ + r) * kRow;
+      for (int c0 = 0; c0 < HD; c0 += 16) {
+        uint32_t o[16];
+        sm100::tmem_ld16(t_lane + 128 + c0, o);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int k = 0; k < 16; k += 4)
+          *reinterpret_cast<float4*>(mine + c0 + k) =
+              make_float4(__uint_as_float(o[k]), __uint_as_float(o[k + 1]),
+                          __uint_as_float(o[k + 2]), __uint_as_float(o[k + 3]));
+      }
+      mine[HD] = m_used;
+      mine[HD + 1] = l_sum;
+      __threadfence();
+      softmax_bar();
+      if (r == 0) {
+        const int prev = atomicAdd(&p.counters[tile], 1);
+        const int last = prev == p.splits - 1;
+        if (last) p.counters[tile] = 0;
+        *last_flag = last;
+      }
+      softmax_bar();
+      if (*last_flag) {
+        __threadfence();
+        float mx = -INFINITY;
+        for (int s = 0; s < p.splits; ++s)
+          mx = fmaxf(mx, __ldcg(p.ws + (((size_t)tile * p.splits + s) * BQ + r) * kRow + HD));
+        float L = 0.f;
+        for (int s = 0; s < p.splits; ++s) {
+          const float* ps = p.ws + (((size_t)tile * p.splits + s) * BQ + r) * kRow;
+          const float ms = __ldcg(ps + HD);
+          if (ms > -INFINITY) L += exp2f(ms - mx) * __ldcg(ps + HD + 1);
+        }
+        const float inv = L > 0.f ? 1.f / L : 0.f;
+        __nv_bfloat16* dst = p.out + (size_t)tok * (kHeads * HD) + head * HD;
+        for (int c0 = 0; c0 < HD; c0 += 8) {
+          float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          for (int s = 0; s < p.splits; ++s) {
+            const float* ps = p.ws + (((size_t)tile * p.splits + s) * BQ + r) * kRow;
+            const float ms = __ldcg(ps + HD);
+            if (!(ms > -INFINITY)) continue;
+            const float wgt = exp2f(ms - mx);
+            const float4 a = __ldcg(reinterpret_cast<const float4*>(ps + c0));
+            const float4 b = __ldcg(reinterpret_cast<const float4*>(ps + c0 + 4));
+            acc[0] += wgt * a.x; acc[1] += wgt * a.y; acc[2] += wgt * a.z; acc[3] += wgt * a.w;
+            acc[4] += wgt * b.x; acc[5] += wgt * b.y; acc[6] += wgt * b.z; acc[7] += wgt * b.w;
+          }
+          uint32_t w[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[2 * k] * inv, acc[2 * k + 1] * inv);
+            w[k] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          if (tok < p.M) *reinterpret_cast<uint4*>(dst + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+}  // namespace attn
+}  // namespace sf

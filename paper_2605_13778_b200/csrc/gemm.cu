@@ -5,6 +5,7 @@
 #include <stdio.h>
 
 #include "common.cuh"
+#include "gemm.cuh"
 #include "gemm_host.h"
 #include "specflow_b200_internal.h"
 

@@ -5,7 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
-#include "gemm.cuh"
+#include "gemm_types.h"
 
 namespace sf {
 namespace gemm {

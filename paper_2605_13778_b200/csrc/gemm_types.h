@@ -1,0 +1,67 @@
+// Shared host/device definitions of the tcgen05 GEMM (kernel in gemm.cuh).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace sf {
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;
+constexpr uint32_t kAStageBytes = BM * BK * 2;
+constexpr int kTmemCols = 256;
+
+enum EpiKind : int {
+  EPI_F32 = 0,    // out_f32[m, n] = acc * r[m]
+  EPI_BF16 = 1,   // out_bf16[m, n] = bf16(acc * r[m])
+  EPI_QKV = 2,    // RMS scale, RoPE on q/k (paired rows), q/k row-major, v transposed
+  EPI_RESID = 3,  // x[m, n] += acc; xb = bf16(x); ssq partials per 128-feature group
+  EPI_GEGLU = 4,  // RMS scale, h[m, n/2] = gelu_tanh(gate) * up for paired rows
+};
+
+struct EpiArgs {
+  int kind;
+  int M;  // valid token rows
+  int N;  // valid output features
+  float* out_f32;
+  int ld_f32;
+  __nv_bfloat16* out_bf16;
+  int ld_bf16;
+  const float* bias;  // per output feature (EPI_F32 / EPI_BF16), may be null
+  // RMSNorm row scale r[m] = rsqrt(sum_g ssq_in[g * ssq_ld + m] * inv_width + eps)
+  const float* ssq_in;
+  int ssq_groups;
+  int ssq_ld;
+  float inv_width;
+  float eps;
+  // QKV
+  __nv_bfloat16* q;
+  __nv_bfloat16* k;
+  __nv_bfloat16* vt;
+  int vt_ld;
+  const float2* rope;  // [pos][head_dim/2] (cos, sin)
+  int q_features;      // q_heads * head_dim
+  int env_rows, seg_len, pos0;
+  // RESID
+  float* x;
+  __nv_bfloat16* xb;
+  float* ssq_out;
+  int ssq_out_ld;
+};
+
+struct Params {
+  int rows_a, rows_b, K;
+  int bn;
+  int num_kb, kb_per_split, splits;
+  int stages;
+  int swap_ab;
+  int tiles_a, tiles_b;
+  float* ws;       // [splits][tiles][bn][128] fp32 partials
+  int* counters;   // [tiles]
+  EpiArgs e;
+};
+
+}  // namespace gemm
+}  // namespace sf

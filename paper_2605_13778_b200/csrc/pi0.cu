@@ -1,0 +1,989 @@
+// pi0-scale Action Expert: verify chain and Euler full path (sm_100a).
+//
+// Per verify round (B envs x K branches, T = 1 + H suffix tokens per branch,
+// env_rows = round_up(K*T, 16) token rows per env):
+//   embed        x_t = tau a + (1-tau) eps (verifier.py:73) -> action_in + temb,
+//                state_proj; fp32 residual X, bf16 copy, RMS partial sums
+//   18 x layer   QKV GEMM (RMS scale + RoPE fused)  -> MQA attention vs the
+//                shared prefix KV -> O GEMM (+residual) -> gate/up GEMM
+//                (RMS scale + GeGLU fused) -> down GEMM (+residual)
+//   head         out_proj GEMM (RMS scale + bias) -> velocity v
+//   epilogue     recon = x + (1-tau) v, distances, warp-ballot prefix,
+//                min over K, gripper gate, decision (verify_epi.cuh)
+// The whole sequence is captured once per (B, K) shape into a CUDA graph with
+// programmatic dependent launch between kernels; the Euler full path
+// (flowpolicy.py:273-292) is N x (embed, layers, head, update) in one graph.
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "attention.cuh"
+#include "common.cuh"
+#include "gemm_host.h"
+#include "specflow_b200_pi0.h"
+#include "verify_epi.cuh"
+
+namespace sf {
+namespace pi0 {
+
+using bf16 = __nv_bfloat16;
+
+// ----------------------------------------------------------- init kernel
+
+__device__ __forceinline__ float hash_uniform(uint64_t seed, uint64_t tid, uint64_t idx, float a) {
+  uint64_t z = seed * 0x9E3779B97F4A7C15ull + tid * 0xD1B54A32D192ED03ull + idx;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z = z ^ (z >> 31);
+  const float u = __fmul_rn((float)(uint32_t)(z >> 40), 5.9604644775390625e-08f);  // 2^-24
+  return __fmul_rn(__fsub_rn(__fmul_rn(u, 2.0f), 1.0f), a);
+}
+
+__global__ void fill_hash_kernel(void* dst, int is_bf16, int64_t n, uint64_t seed, uint64_t tid,
+                                 float a) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = hash_uniform(seed, tid, (uint64_t)i, a);
+    if (is_bf16) static_cast<bf16*>(dst)[i] = __float2bfloat16_rn(v);
+    else static_cast<float*>(dst)[i] = v;
+  }
+}
+
+// --------------------------------------------------- time embedding (fp32)
+
+// h = swish(W1 f(tau) + b1) for R taus; one warp per output feature.
+__global__ void temb_hidden_kernel(const float* __restrict__ w1, const float* __restrict__ b1,
+                                   const float* __restrict__ taus, int R, int W, float min_p,
+                                   float max_p, float* __restrict__ hidden) {
+  extern __shared__ float feat[];  // [R][W]
+  const int half = W / 2;
+  for (int idx = threadIdx.x; idx < R * W; idx += blockDim.x) {
+    const int r = idx / W, i = idx - r * W;
+    const int ii = i < half ? i : i - half;
+    const double frac = half > 1 ? (double)ii / (double)(half - 1) : 0.0;
+    const double period = (double)min_p * pow((double)max_p / (double)min_p, frac);
+    const double ang = 2.0 * 3.141592653589793 * (double)taus[r] / period;
+    feat[idx] = (float)(i < half ? sin(ang) : cos(ang));
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  for (int o = blockIdx.x * nw + warp; o < W; o += gridDim.x * nw) {
+    for (int r = 0; r < R; ++r) {
+      float acc = 0.f;
+      for (int i = lane; i < W; i += 32) acc = fmaf(w1[(size_t)o * W + i], feat[r * W + i], acc);
+      for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (lane == 0) {
+        const float h = acc + b1[o];
+        hidden[r * W + o] = h / (1.f + expf(-h));
+      }
+    }
+  }
+}
+
+__global__ void temb_out_kernel(const float* __restrict__ w2, const float* __restrict__ b2,
+                                const float* __restrict__ hidden, int R, int W,
+                                float* __restrict__ temb) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  for (int o = blockIdx.x * nw + warp; o < W; o += gridDim.x * nw) {
+    for (int r = 0; r < R; ++r) {
+      float acc = 0.f;
+      for (int i = lane; i < W; i += 32) acc = fmaf(w2[(size_t)o * W + i], hidden[r * W + i], acc);
+      for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (lane == 0) temb[r * W + o] = acc + b2[o];
+    }
+  }
+}
+
+// ------------------------------------------------------------ embedding
+
+struct EmbedParams {
+  int W, D, S, H, T, K, env_rows, B;
+  int mode;             // 0: verify (interpolate draft/eps at taus[k]); 1: Euler (actions given)
+  const float* draft;   // [B][H][D]   (mode 0) | current A [B][H][D] (mode 1)
+  const float* eps;     // [B][H][D]   (mode 0)
+  float taus[SF_MAX_K];
+  const float* temb;    // [K][W] (mode 0) | [1][W] for this step (mode 1)
+  const float* state;   // [B][S]
+  const float* a_w;     // [W][D]
+  const float* a_b;
+  const float* s_w;     // [W][S]
+  const float* s_b;
+  float* x;             // [M][W]
+  bf16* xb;             // [M][W]
+  float* ssq;           // [W/128][M_ld]
+  int ssq_ld;
+};
+
+// One CTA per token row (256 threads, W/256 features each).
+__global__ void __launch_bounds__(256) embed_kernel(const EmbedParams p) {
+  sm100::pdl_wait();
+  const int m = blockIdx.x;
+  const int e = m / p.env_rows;
+  const int local = m - e * p.env_rows;
+  const int k = local / p.T;
+  const int t = local - k * p.T;
+  const bool real = local < p.K * p.T;
+  __shared__ float in[64];
+  __shared__ float red[8][8];
+  if (real && threadIdx.x < 64) {
+    float v = 0.f;
+    if (t == 0) {
+      if (threadIdx.x < p.S) v = p.state[e * p.S + threadIdx.x];
+    } else if (threadIdx.x < p.D) {
+      if (p.mode == 0) {
+        const int i = (e * p.H + (t - 1)) * p.D + threadIdx.x;
+        const float tau = p.taus[k];
+        // tau * a + (1 - tau) * eps, rounded like the verify epilogue (verifier.py:73)
+        v = __fadd_rn(__fmul_rn(tau, p.draft[i]), __fmul_rn(__fsub_rn(1.f, tau), p.eps[i]));
+      } else {
+        v = p.draft[((e * p.K + k) * p.H + (t - 1)) * p.D + threadIdx.x];
+      }
+    }
+    in[threadIdx.x] = v;
+  }
+  __syncthreads();
+  float sq[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int n = threadIdx.x; n < p.W; n += blockDim.x) {
+    float acc = 0.f;
+    if (real) {
+      if (t == 0) {
+        acc = p.s_b[n];
+        for (int i = 0; i < p.S; ++i) acc = fmaf(p.s_w[n * p.S + i], in[i], acc);
+      } else {
+        acc = p.a_b[n];
+        for (int i = 0; i < p.D; ++i) acc = fmaf(p.a_w[n * p.D + i], in[i], acc);
+        acc += p.temb[k * p.W + n];
+      }
+    }
+    p.x[(size_t)m * p.W + n] = acc;
+    p.xb[(size_t)m * p.W + n] = __float2bfloat16_rn(acc);
+    sq[n >> 7 & 7] += acc * acc;
+  }
+  // per-128-feature-group sum of squares (fixed reduction order)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int g = 0; g < 8; ++g) {
+    float s = sq[g];
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) red[warp][g] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < p.W / 128) {
+    float s = 0.f;
+    for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+    p.ssq[(size_t)threadIdx.x * p.ssq_ld + m] = s;
+  }
+  if (threadIdx.x == 0) sm100::pdl_launch_dependents();
+}
+
+// --------------------------------------------------------- verify epilogue
+
+struct VerifyEpiParams {
+  int H, D, C, K, T, env_rows;
+  float taus[SF_MAX_K];
+  float delta;
+  int metric, window;
+  float sign;
+  const float* signs;  // [B] or null
+  int phase_fallback, prefix_cap, replan_size;
+  const float* draft;  // [B][H][D]
+  const float* eps;    // [B][H][D]
+  const float* vel;    // [M][D] head output
+  float* out_recon;    // [B][K][H][D] or null
+  float* out_dist;     // [B][K][H] or null
+  int* out_branch;     // [B][K]
+  int* out_result;     // [B][8]
+};
+
+__global__ void __launch_bounds__(256) verify_epi_kernel(const VerifyEpiParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  sm100::pdl_wait();
+  const int e = blockIdx.x;
+  float* s_recon = reinterpret_cast<float*>(smem_raw);
+  float* s_dist = s_recon + p.K * p.H * p.D;
+  const int HD = p.H * p.D;
+  const float* vel = p.vel + (size_t)e * p.env_rows * p.D;
+  verify_epilogue_cta<float, false>(
+      p.draft + (size_t)e * HD, p.eps + (size_t)e * HD,
+      [&](int k, int i) { return vel[(size_t)(k * p.T + 1) * p.D + i]; }, p.H, p.D, p.C, p.K,
+      p.taus, p.delta, p.metric, p.window, p.signs ? p.signs[e] : p.sign, p.phase_fallback,
+      p.prefix_cap, p.replan_size, p.out_recon ? p.out_recon + (size_t)e * p.K * HD : nullptr,
+      p.out_dist ? p.out_dist + (size_t)e * p.K * p.H : nullptr, p.out_branch + e * p.K,
+      p.out_result + e * SF_RESULT_WORDS, s_recon, s_dist);
+}
+
+struct EulerParams {
+  float* A;
+  const float* vel;
+  int B, H, D, env_rows, n, step;
+  int* status;
+};
+
+// A <- A + v / N with the finite check (flowpolicy.py:289-291), rows of the
+// single-branch Euler layout (token 1 + h of env e).
+__global__ void euler_rows_kernel(const EulerParams p) {
+  sm100::pdl_wait();
+  const int total = p.B * p.H * p.D;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int e = i / (p.H * p.D);
+    const int rem = i - e * p.H * p.D;
+    const int h = rem / p.D, d = rem - h * p.D;
+    const float v = p.vel[((size_t)e * p.env_rows + 1 + h) * p.D + d];
+    const float nxt = __fadd_rn(p.A[i], __fdiv_rn(v, (float)p.n));
+    p.A[i] = nxt;
+    if (!isfinite(v)) atomicCAS(&p.status[2 * e + 1], 0, 1);
+    if (!isfinite(nxt)) atomicCAS(&p.status[2 * e], -1, p.step);
+  }
+  if (threadIdx.x == 0) sm100::pdl_launch_dependents();
+}
+
+struct GatherParams {
+  const float* vel;
+  float* out;  // [B][K][H][D]
+  int B, K, H, D, T, env_rows;
+};
+
+__global__ void gather_vel_kernel(const GatherParams p) {
+  const int total = p.B * p.K * p.H * p.D;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int d = i % p.D;
+    const int h = (i / p.D) % p.H;
+    const int k = (i / (p.D * p.H)) % p.K;
+    const int e = i / (p.D * p.H * p.K);
+    p.out[i] = p.vel[((size_t)e * p.env_rows + k * p.T + 1 + h) * p.D + d];
+  }
+}
+
+// ----------------------------------------------------------------- handle
+
+struct Buffers {
+  int B = 0, K = 0, env_rows = 0, M = 0, m_ld = 0;
+  float* x = nullptr;      // [M][W]
+  bf16* xb = nullptr;      // [M][W]
+  float* ssq = nullptr;    // [8][m_ld]
+  bf16* q = nullptr;       // [M][8*256]
+  bf16* ks = nullptr;      // [M][256]
+  bf16* vt = nullptr;      // [256][m_ld]
+  bf16* attn = nullptr;    // [M][8*256]
+  bf16* h = nullptr;       // [M][mlp]
+  float* vel = nullptr;    // [M][D]
+  float* draft = nullptr;  // [B][H][D] staged inputs (graph-stable)
+  float* eps = nullptr;
+  float* state = nullptr;  // [B][S]
+  float* signs = nullptr;  // [B]
+  float* recon = nullptr;  // [B][K][H][D]
+  float* dist = nullptr;   // [B][K][H]
+  int* branch = nullptr;   // [B][K]
+  int* result = nullptr;   // [B][8]
+  int* status = nullptr;   // [B][2] Euler status
+  float* ws = nullptr;
+  size_t ws_bytes = 0;
+  int* counters = nullptr;
+  int n_counters = 0;
+  std::vector<gemm::Op> ops;     // per layer: qkv, o, gu, down; then head
+  std::vector<size_t> attn_ops;  // unused placeholder
+  attn::Params ap{};
+  int attn_tiles = 0, attn_splits = 1;
+  std::vector<CUtensorMap> attn_maps;  // per layer: q, kp, vp, ks, vs
+  cudaGraphExec_t graph = nullptr;
+  int graph_key = 0;
+};
+
+struct Handle {
+  sf_ae_config_t cfg{};
+  sf_ae_weights_t w{};
+  const bf16* k_prefix = nullptr;   // [L][E][P][256]
+  const bf16* vt_prefix = nullptr;  // [L][E][256][P]
+  int n_prefix_envs = 0;
+  float* temb = nullptr;   // [SF_MAX_K][W] for the verify taus
+  float temb_taus[SF_MAX_K];
+  int temb_k = -1;
+  float* temb_euler = nullptr;  // [N][W]
+  int temb_euler_n = -1;
+  float* temb_hidden = nullptr;
+  float* temb_tau_dev = nullptr;
+  std::map<long long, std::unique_ptr<Buffers>> buffers;  // key: (B, K, mode)
+  cudaStream_t capture_stream = nullptr;
+};
+
+int T_of(const Handle& h) { return 1 + h.cfg.horizon; }
+
+template <typename P>
+int launch_pdl(void (*kern)(P), dim3 grid, dim3 block, size_t smem, cudaStream_t s, const P& p,
+               bool pdl) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+  count_launch();
+  return SF_OK;
+}
+
+int compute_temb(Handle& h, const float* taus_host, int R, float* out, cudaStream_t s) {
+  const int W = h.cfg.width;
+  SF_CHECK_CUDA(cudaMemcpyAsync(h.temb_tau_dev, taus_host, sizeof(float) * R,
+                                cudaMemcpyHostToDevice, s));
+  const size_t smem = sizeof(float) * R * W;
+  SF_REQUIRE(smem <= 200 * 1024, "too many taus for the time embedding (%d)", R);
+  SF_CHECK_CUDA(cudaFuncSetAttribute(temb_hidden_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  temb_hidden_kernel<<<64, 256, smem, s>>>((const float*)h.w.t1_w, (const float*)h.w.t1_b,
+                                           h.temb_tau_dev, R, W, h.cfg.temb_min_period,
+                                           h.cfg.temb_max_period, h.temb_hidden);
+  temb_out_kernel<<<64, 256, 0, s>>>((const float*)h.w.t2_w, (const float*)h.w.t2_b,
+                                     h.temb_hidden, R, W, out);
+  SF_CHECK_CUDA(cudaGetLastError());
+  count_launch(2);
+  return SF_OK;
+}
+
+int make_map_3d(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2,
+                uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0, uint32_t box1) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("3-D tensor map encode failed (%d)", (int)r);
+    return SF_ECUDA;
+  }
+  return SF_OK;
+}
+
+template <typename T>
+int dalloc(T** p, size_t n) {
+  SF_CHECK_CUDA(cudaMalloc(p, sizeof(T) * (n ? n : 1)));
+  SF_CHECK_CUDA(cudaMemset(*p, 0, sizeof(T) * (n ? n : 1)));
+  return SF_OK;
+}
+
+// Build buffers + GEMM / attention plans for B envs x K branches.
+int build(Handle& h, Buffers& b, int B, int K) {
+  const sf_ae_config_t& c = h.cfg;
+  const int W = c.width, T = T_of(h), L = c.layers;
+  const int nq = c.q_heads * c.head_dim;
+  b.B = B;
+  b.K = K;
+  b.env_rows = ((K * T + 15) / 16) * 16;
+  b.M = B * b.env_rows;
+  b.m_ld = ((b.M + 63) / 64) * 64;
+  int rc;
+#define ALLOC(ptr, n) \
+  if ((rc = dalloc(&(ptr), (n)))) return rc
+  ALLOC(b.x, (size_t)b.M * W);
+  ALLOC(b.xb, (size_t)b.m_ld * W);
+  ALLOC(b.ssq, (size_t)(W / 128) * b.m_ld);
+  ALLOC(b.q, (size_t)b.m_ld * nq);
+  ALLOC(b.ks, (size_t)b.m_ld * c.head_dim);
+  ALLOC(b.vt, (size_t)c.head_dim * b.m_ld);
+  ALLOC(b.attn, (size_t)b.m_ld * nq);
+  ALLOC(b.h, (size_t)b.m_ld * c.mlp);
+  ALLOC(b.vel, (size_t)b.M * c.action_dim);
+  ALLOC(b.draft, (size_t)B * c.horizon * c.action_dim);
+  ALLOC(b.eps, (size_t)B * c.horizon * c.action_dim);
+  ALLOC(b.state, (size_t)B * c.state_dim);
+  ALLOC(b.signs, (size_t)B);
+  ALLOC(b.recon, (size_t)B * K * c.horizon * c.action_dim);
+  ALLOC(b.dist, (size_t)B * K * c.horizon);
+  ALLOC(b.branch, (size_t)B * K);
+  ALLOC(b.result, (size_t)B * SF_RESULT_WORDS);
+  ALLOC(b.status, (size_t)B * 2);
+
+  // --- GEMM plans. Batch-1 shapes stream weights (swap-AB + split-K);
+  // larger batches run the normal orientation with 256-feature tiles.
+  const bool swap = b.M <= 256;
+  const int bn_swap = ((b.M + 15) / 16) * 16;
+  struct G {
+    const void* w;
+    int n_out, k_in;
+    int kind;
+  };
+  // worst-case split-K workspace across all GEMMs
+  size_t ws = 0;
+  int max_tiles = 0;
+  auto splits_for = [&](int n_out, int k_in, int bn) {
+    const int tiles = swap ? (n_out + 127) / 128 : ((b.M + 127) / 128) * ((n_out + bn - 1) / bn);
+    int s = 148 / (tiles > 0 ? tiles : 1);
+    if (s < 1) s = 1;
+    const int kb = k_in / 64;
+    if (s > kb) s = kb;
+    const int kbps = (kb + s - 1) / s;
+    s = (kb + kbps - 1) / kbps;
+    if (tiles > max_tiles) max_tiles = tiles;
+    const size_t need = swap ? gemm::ws_bytes_needed(n_out, b.M, k_in, bn, s)
+                             : gemm::ws_bytes_needed(b.M, n_out, k_in, bn, s);
+    if (need > ws) ws = need;
+    return s;
+  };
+  const int bn_norm = 256;
+  std::vector<int> splits;
+  for (int l = 0; l < L; ++l) {
+    splits.push_back(splits_for(nq + 2 * c.head_dim, W, swap ? bn_swap : bn_norm));
+    splits.push_back(splits_for(W, nq, swap ? bn_swap : bn_norm));
+    splits.push_back(splits_for(2 * c.mlp, W, swap ? bn_swap : bn_norm));
+    splits.push_back(splits_for(W, c.mlp, swap ? bn_swap : bn_norm));
+  }
+  const int bn_head = swap ? bn_swap : 32;
+  splits.push_back(splits_for(c.action_dim, W, bn_head));
+  b.ws_bytes = ws;
+  if (ws) ALLOC(b.ws, ws / sizeof(float));
+  // attention split-KV workspace
+  const int n_prefix_blocks = (c.prefix_len + attn::BKEY - 1) / attn::BKEY;
+  const int n_blocks = n_prefix_blocks + 2;
+  b.attn_tiles = b.M / 16;
+  int asplit = 148 / b.attn_tiles;
+  if (asplit < 1) asplit = 1;
+  if (asplit > n_blocks) asplit = n_blocks;
+  const int bps = (n_blocks + asplit - 1) / asplit;
+  asplit = (n_blocks + bps - 1) / bps;
+  b.attn_splits = asplit;
+  float* attn_ws = nullptr;
+  if (asplit > 1) ALLOC(attn_ws, (size_t)b.attn_tiles * asplit * attn::BQ * (attn::HD + 2));
+  b.n_counters = (max_tiles > b.attn_tiles ? max_tiles : b.attn_tiles) + 8;
+  ALLOC(b.counters, (size_t)b.n_counters);
+#undef ALLOC
+
+  auto epi_base = [&](int kind) {
+    gemm::EpiArgs e{};
+    e.kind = kind;
+    e.M = b.M;
+    e.ssq_in = b.ssq;
+    e.ssq_groups = W / 128;
+    e.ssq_ld = b.m_ld;
+    e.inv_width = 1.f / (float)W;
+    e.eps = c.eps;
+    return e;
+  };
+  b.ops.resize(4 * L + 1);
+  int si = 0;
+  auto plan_op = [&](gemm::Op* op, const void* wt, int n_out, const void* act, int k_in,
+                     const gemm::EpiArgs& e) {
+    const int bn = swap ? bn_swap : bn_norm;
+    const int sp = splits[si++];
+    if (swap)
+      return gemm::plan(op, wt, n_out, k_in, act, b.M, k_in, k_in, bn, sp, 1, e, b.ws, b.ws_bytes,
+                        b.counters, b.n_counters);
+    return gemm::plan(op, act, b.M, k_in, wt, n_out, k_in, k_in, bn, sp, 0, e, b.ws, b.ws_bytes,
+                      b.counters, b.n_counters);
+  };
+  for (int l = 0; l < L; ++l) {
+    gemm::EpiArgs e = epi_base(gemm::EPI_QKV);
+    e.N = nq + 2 * c.head_dim;
+    e.q = b.q;
+    e.k = b.ks;
+    e.vt = b.vt;
+    e.vt_ld = b.m_ld;
+    e.rope = static_cast<const float2*>(h.w.rope);
+    e.q_features = nq;
+    e.env_rows = b.env_rows;
+    e.seg_len = T;
+    e.pos0 = c.prefix_len;
+    if ((rc = plan_op(&b.ops[4 * l + 0], h.w.qkv[l], e.N, b.xb, W, e))) return rc;
+    gemm::EpiArgs eo = epi_base(gemm::EPI_RESID);
+    eo.ssq_in = nullptr;
+    eo.N = W;
+    eo.x = b.x;
+    eo.xb = b.xb;
+    eo.ssq_out = b.ssq;
+    eo.ssq_out_ld = b.m_ld;
+    if ((rc = plan_op(&b.ops[4 * l + 1], h.w.o[l], W, b.attn, nq, eo))) return rc;
+    gemm::EpiArgs eg = epi_base(gemm::EPI_GEGLU);
+    eg.N = 2 * c.mlp;
+    eg.out_bf16 = b.h;
+    eg.ld_bf16 = c.mlp;
+    if ((rc = plan_op(&b.ops[4 * l + 2], h.w.gu[l], eg.N, b.xb, W, eg))) return rc;
+    if ((rc = plan_op(&b.ops[4 * l + 3], h.w.down[l], W, b.h, c.mlp, eo))) return rc;
+  }
+  {
+    gemm::EpiArgs e = epi_base(gemm::EPI_F32);
+    e.N = c.action_dim;
+    e.out_f32 = b.vel;
+    e.ld_f32 = c.action_dim;
+    e.bias = static_cast<const float*>(h.w.out_b);
+    const int bn = bn_head;
+    const int sp = splits[si++];
+    if (swap)
+      rc = gemm::plan(&b.ops[4 * L], h.w.out_w, c.action_dim, W, b.xb, b.M, W, W, bn, sp, 1, e,
+                      b.ws, b.ws_bytes, b.counters, b.n_counters);
+    else
+      rc = gemm::plan(&b.ops[4 * L], b.xb, b.M, W, h.w.out_w, c.action_dim, W, W, bn, sp, 0, e,
+                      b.ws, b.ws_bytes, b.counters, b.n_counters);
+    if (rc) return rc;
+  }
+  // --- attention plans (per layer: 5 tensor maps)
+  attn::Params& ap = b.ap;
+  ap.M = b.M;
+  ap.env_rows = b.env_rows;
+  ap.seg_len = T;
+  ap.segs = K;
+  ap.prefix_len = c.prefix_len;
+  ap.n_prefix_blocks = n_prefix_blocks;
+  ap.n_blocks = n_blocks;
+  ap.blocks_per_split = bps;
+  ap.splits = asplit;
+  ap.tiles = b.attn_tiles;
+  ap.scale_log2 = 1.4426950408889634f / sqrtf((float)c.head_dim);
+  ap.out = b.attn;
+  ap.ws = attn_ws;
+  ap.counters = b.counters;  // shared with split-K GEMMs: kernels are stream-ordered
+  b.attn_maps.resize(5 * L);
+  const int E = h.n_prefix_envs;
+  for (int l = 0; l < L; ++l) {
+    CUtensorMap* mp = &b.attn_maps[5 * l];
+    if ((rc = gemm::make_map(&mp[0], b.q, b.M * attn::kHeads, c.head_dim, c.head_dim, attn::BQ)))
+      return rc;
+    const bf16* kp = h.k_prefix + (size_t)l * E * c.prefix_len * c.head_dim;
+    const bf16* vp = h.vt_prefix + (size_t)l * E * c.head_dim * c.prefix_len;
+    if ((rc = make_map_3d(&mp[1], kp, c.head_dim, c.prefix_len, E, (uint64_t)c.head_dim * 2,
+                          (uint64_t)c.prefix_len * c.head_dim * 2, 64, attn::BKEY)))
+      return rc;
+    if ((rc = make_map_3d(&mp[2], vp, c.prefix_len, c.head_dim, E, (uint64_t)c.prefix_len * 2,
+                          (uint64_t)c.prefix_len * c.head_dim * 2, attn::BKEY, c.head_dim)))
+      return rc;
+    if ((rc = gemm::make_map(&mp[3], b.ks, b.M, c.head_dim, c.head_dim, attn::BKEY))) return rc;
+    if ((rc = gemm::make_map(&mp[4], b.vt, c.head_dim, b.m_ld, b.m_ld, c.head_dim))) return rc;
+  }
+  return SF_OK;
+}
+
+int launch_attn(const Buffers& b, int l, cudaStream_t s, bool pdl) {
+  static bool attr = false;
+  if (!attr) {
+    SF_CHECK_CUDA(cudaFuncSetAttribute(attn::attn_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)attn::kSmemBytes));
+    attr = true;
+  }
+  const CUtensorMap* mp = &b.attn_maps[5 * l];
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(b.attn_tiles, b.attn_splits);
+  cfg.blockDim = dim3(attn::kThreads);
+  cfg.dynamicSmemBytes = attn::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, attn::attn_kernel, mp[0], mp[1], mp[2], mp[3], mp[4], b.ap));
+  count_launch();
+  return SF_OK;
+}
+
+// The layer stack + head on the current X (used by verify and Euler).
+int run_stack(Handle& h, Buffers& b, cudaStream_t s, bool pdl) {
+  int rc;
+  for (int l = 0; l < h.cfg.layers; ++l) {
+    if ((rc = gemm::launch(b.ops[4 * l + 0], s, pdl))) return rc;
+    if ((rc = launch_attn(b, l, s, pdl))) return rc;
+    if ((rc = gemm::launch(b.ops[4 * l + 1], s, pdl))) return rc;
+    if ((rc = gemm::launch(b.ops[4 * l + 2], s, pdl))) return rc;
+    if ((rc = gemm::launch(b.ops[4 * l + 3], s, pdl))) return rc;
+  }
+  return gemm::launch(b.ops[4 * h.cfg.layers], s, pdl);
+}
+
+EmbedParams embed_params(const Handle& h, const Buffers& b, int mode, const float* temb) {
+  const sf_ae_config_t& c = h.cfg;
+  EmbedParams p{};
+  p.W = c.width;
+  p.D = c.action_dim;
+  p.S = c.state_dim;
+  p.H = c.horizon;
+  p.T = T_of(h);
+  p.K = b.K;
+  p.env_rows = b.env_rows;
+  p.B = b.B;
+  p.mode = mode;
+  p.draft = b.draft;
+  p.eps = b.eps;
+  for (int k = 0; k < b.K && k < SF_MAX_K; ++k) p.taus[k] = h.temb_taus[k];
+  p.temb = temb;
+  p.state = b.state;
+  p.a_w = static_cast<const float*>(h.w.a_w);
+  p.a_b = static_cast<const float*>(h.w.a_b);
+  p.s_w = static_cast<const float*>(h.w.s_w);
+  p.s_b = static_cast<const float*>(h.w.s_b);
+  p.x = b.x;
+  p.xb = b.xb;
+  p.ssq = b.ssq;
+  p.ssq_ld = b.m_ld;
+  return p;
+}
+
+// Verify chain for the staged inputs of `b` (draft/eps/state/signs already in b).
+int enqueue_verify(Handle& h, Buffers& b, const sf_verify_cfg_t* cfg, cudaStream_t s, bool pdl) {
+  int rc;
+  EmbedParams ep = embed_params(h, b, 0, h.temb);
+  if ((rc = launch_pdl(embed_kernel, dim3(b.M), dim3(256), 0, s, ep, false))) return rc;
+  if ((rc = run_stack(h, b, s, pdl))) return rc;
+  VerifyEpiParams vp{};
+  const sf_ae_config_t& c = h.cfg;
+  vp.H = c.horizon;
+  vp.D = c.action_dim;
+  vp.C = c.action_dim - 1;
+  vp.K = b.K;
+  vp.T = T_of(h);
+  vp.env_rows = b.env_rows;
+  for (int k = 0; k < b.K; ++k) vp.taus[k] = (float)cfg->taus[k];
+  vp.delta = (float)cfg->delta;
+  vp.metric = cfg->metric;
+  vp.window = cfg->window;
+  vp.sign = (float)cfg->current_sign;
+  vp.signs = b.signs;
+  vp.phase_fallback = cfg->phase_fallback;
+  vp.prefix_cap = cfg->prefix_cap;
+  vp.replan_size = cfg->replan_size;
+  vp.draft = b.draft;
+  vp.eps = b.eps;
+  vp.vel = b.vel;
+  vp.out_recon = b.recon;
+  vp.out_dist = b.dist;
+  vp.out_branch = b.branch;
+  vp.out_result = b.result;
+  const size_t smem = sizeof(float) * ((size_t)b.K * c.horizon * c.action_dim + b.K * c.horizon);
+  static bool attr = false;
+  if (!attr) {
+    SF_CHECK_CUDA(cudaFuncSetAttribute(verify_epi_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  return launch_pdl(verify_epi_kernel, dim3(b.B), dim3(256), smem, s, vp, pdl);
+}
+
+int enqueue_denoise(Handle& h, Buffers& b, int n_steps, cudaStream_t s, bool pdl) {
+  int rc;
+  const int W = h.cfg.width;
+  for (int i = 0; i < n_steps; ++i) {
+    EmbedParams ep = embed_params(h, b, 1, h.temb_euler + (size_t)i * W);
+    if ((rc = launch_pdl(embed_kernel, dim3(b.M), dim3(256), 0, s, ep, i > 0 && pdl))) return rc;
+    if ((rc = run_stack(h, b, s, pdl))) return rc;
+    const int total = b.B * h.cfg.horizon * h.cfg.action_dim;
+    EulerParams up{b.draft, b.vel, b.B, h.cfg.horizon, h.cfg.action_dim, b.env_rows, n_steps, i,
+                   b.status};
+    if ((rc = launch_pdl(euler_rows_kernel, dim3((total + 255) / 256), dim3(256), 0, s, up, pdl)))
+      return rc;
+  }
+  return SF_OK;
+}
+
+Buffers* get_buffers(Handle& h, int B, int K, int* rc) {
+  const long long key = (long long)B * 1000 + K;
+  auto it = h.buffers.find(key);
+  if (it != h.buffers.end()) return it->second.get();
+  auto b = std::make_unique<Buffers>();
+  *rc = build(h, *b, B, K);
+  if (*rc) return nullptr;
+  Buffers* raw = b.get();
+  h.buffers[key] = std::move(b);
+  return raw;
+}
+
+// Capture `fn(stream)` into a graph on the handle's capture stream.
+template <typename F>
+int capture(Handle& h, cudaGraphExec_t* exec, F&& fn) {
+  if (!h.capture_stream)
+    SF_CHECK_CUDA(cudaStreamCreateWithFlags(&h.capture_stream, cudaStreamNonBlocking));
+  cudaGraph_t g = nullptr;
+  SF_CHECK_CUDA(cudaStreamBeginCapture(h.capture_stream, cudaStreamCaptureModeThreadLocal));
+  const int rc = fn(h.capture_stream);
+  cudaError_t e = cudaStreamEndCapture(h.capture_stream, &g);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  SF_CHECK_CUDA(e);
+  if (*exec) cudaGraphExecDestroy(*exec);
+  e = cudaGraphInstantiate(exec, g, 0);
+  cudaGraphDestroy(g);
+  SF_CHECK_CUDA(e);
+  return SF_OK;
+}
+
+int cfg_key(const sf_verify_cfg_t* c) {
+  // cheap hash of the verify knobs baked into the graph's kernel params
+  uint64_t hsh = 1469598103934665603ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) hsh = (hsh ^ b[i]) * 1099511628211ull;
+  };
+  mix(c, sizeof(*c));
+  return (int)(hsh & 0x7fffffff);
+}
+
+}  // namespace pi0
+}  // namespace sf
+
+using namespace sf::pi0;
+
+extern "C" int sf_fill_hash_uniform(void* dst, int is_bf16, int64_t n, uint64_t seed, uint64_t tid,
+                                    double std_, void* stream) {
+  SF_REQUIRE(dst && n >= 0, "bad fill arguments");
+  if (n == 0) return SF_OK;
+  const float a = (float)(std_ * 1.7320508075688772);  // np.float32(std * np.sqrt(3.0))
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  fill_hash_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(dst, is_bf16, n, seed, tid, a);
+  SF_CHECK_CUDA(cudaGetLastError());
+  sf::count_launch();
+  return SF_OK;
+}
+
+extern "C" int sf_ae_create(const sf_ae_config_t* cfg, const sf_ae_weights_t* w, void** handle) {
+  SF_REQUIRE(cfg && w && handle, "null argument");
+  SF_REQUIRE(cfg->head_dim == 256, "head_dim must be 256");
+  SF_REQUIRE(cfg->q_heads == 8, "the attention kernel is built for 8 query heads");
+  SF_REQUIRE(cfg->width % 256 == 0 && cfg->width <= 2048, "width must be a multiple of 256");
+  SF_REQUIRE(cfg->layers >= 1 && cfg->layers <= SF_AE_MAX_LAYERS, "bad layer count");
+  SF_REQUIRE(cfg->mlp % 64 == 0, "mlp must be a multiple of 64");
+  SF_REQUIRE(cfg->action_dim >= 2 && cfg->action_dim <= 64, "action_dim must be in [2, 64]");
+  SF_REQUIRE(cfg->state_dim >= 1 && cfg->state_dim <= 64, "state_dim must be in [1, 64]");
+  SF_REQUIRE(cfg->horizon >= 1 && cfg->prefix_len >= 1, "bad horizon / prefix");
+  auto* h = new Handle();
+  h->cfg = *cfg;
+  h->w = *w;
+  int rc;
+  if ((rc = dalloc(&h->temb, (size_t)SF_MAX_K * cfg->width)) ||
+      (rc = dalloc(&h->temb_hidden, (size_t)64 * cfg->width)) ||
+      (rc = dalloc(&h->temb_tau_dev, 64))) {
+    delete h;
+    return rc;
+  }
+  *handle = h;
+  return SF_OK;
+}
+
+extern "C" int sf_ae_destroy(void* handle) {
+  auto* h = static_cast<Handle*>(handle);
+  if (!h) return SF_OK;
+  for (auto& kv : h->buffers) {
+    Buffers& b = *kv.second;
+    if (b.graph) cudaGraphExecDestroy(b.graph);
+    void* ptrs[] = {b.x, b.xb, b.ssq, b.q, b.ks, b.vt, b.attn, b.h, b.vel, b.draft, b.eps,
+                    b.state, b.signs, b.recon, b.dist, b.branch, b.result, b.status, b.ws,
+                    b.counters, b.ap.ws};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+  cudaFree(h->temb);
+  cudaFree(h->temb_hidden);
+  cudaFree(h->temb_tau_dev);
+  if (h->temb_euler) cudaFree(h->temb_euler);
+  if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
+  delete h;
+  return SF_OK;
+}
+
+extern "C" int sf_ae_set_prefix(void* handle, const void* k_prefix, const void* vt_prefix,
+                                int n_envs) {
+  auto* h = static_cast<Handle*>(handle);
+  SF_REQUIRE(h && k_prefix && vt_prefix && n_envs >= 1, "bad prefix arguments");
+  h->k_prefix = static_cast<const bf16*>(k_prefix);
+  h->vt_prefix = static_cast<const bf16*>(vt_prefix);
+  h->n_prefix_envs = n_envs;
+  // plans embed the prefix tensor maps: drop them
+  for (auto& kv : h->buffers) {
+    Buffers& b = *kv.second;
+    if (b.graph) cudaGraphExecDestroy(b.graph);
+    void* ptrs[] = {b.x, b.xb, b.ssq, b.q, b.ks, b.vt, b.attn, b.h, b.vel, b.draft, b.eps,
+                    b.state, b.signs, b.recon, b.dist, b.branch, b.result, b.status, b.ws,
+                    b.counters, b.ap.ws};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+  h->buffers.clear();
+  return SF_OK;
+}
+
+static int ensure_temb(Handle& h, const sf_verify_cfg_t* cfg, cudaStream_t s) {
+  bool same = h.temb_k == cfg->k;
+  for (int k = 0; same && k < cfg->k; ++k) same = h.temb_taus[k] == (float)cfg->taus[k];
+  if (same) return SF_OK;
+  for (int k = 0; k < cfg->k; ++k) h.temb_taus[k] = (float)cfg->taus[k];
+  h.temb_k = cfg->k;
+  return compute_temb(h, h.temb_taus, cfg->k, h.temb, s);
+}
+
+extern "C" int sf_ae_verify(void* handle, int n_envs, const sf_verify_cfg_t* cfg, const float* draft,
+                            const float* eps, const float* state, const float* signs,
+                            const sf_verify_out_t* out, int flags, void* stream) {
+  auto* h = static_cast<Handle*>(handle);
+  SF_REQUIRE(h && cfg && draft && eps && state && out && out->branch_prefixes && out->result,
+             "null argument");
+  SF_REQUIRE(h->k_prefix, "no prefix KV bound (sf_ae_set_prefix)");
+  SF_REQUIRE(n_envs >= 1 && n_envs <= h->n_prefix_envs, "n_envs exceeds the prefix pool");
+  SF_REQUIRE(cfg->k >= 1 && cfg->k <= SF_MAX_K, "need 1..%d verification timesteps", SF_MAX_K);
+  for (int i = 0; i < cfg->k; ++i) {
+    SF_REQUIRE(cfg->taus[i] > 0.0 && cfg->taus[i] < 1.0,
+               "verification timesteps must lie strictly inside (0, 1)");
+    if (i) SF_REQUIRE(cfg->taus[i] > cfg->taus[i - 1], "verification timesteps must be strictly increasing");
+  }
+  SF_REQUIRE(cfg->delta >= 0.0, "delta must be non-negative");
+  SF_REQUIRE(cfg->metric == SF_METRIC_L2 || cfg->metric == SF_METRIC_LINF, "unknown metric");
+  SF_REQUIRE(signs || cfg->current_sign == 1.0 || cfg->current_sign == -1.0,
+             "current_sign must be -1.0 or +1.0");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = 0;
+  Buffers* b = get_buffers(*h, n_envs, cfg->k, &rc);
+  if (!b) return rc;
+  if ((rc = ensure_temb(*h, cfg, s))) return rc;
+  const sf_ae_config_t& c = h->cfg;
+  const size_t hd = (size_t)n_envs * c.horizon * c.action_dim;
+  SF_CHECK_CUDA(cudaMemcpyAsync(b->draft, draft, hd * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(b->eps, eps, hd * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(b->state, state, (size_t)n_envs * c.state_dim * 4,
+                                cudaMemcpyDeviceToDevice, s));
+  if (signs) {
+    SF_CHECK_CUDA(cudaMemcpyAsync(b->signs, signs, n_envs * 4, cudaMemcpyDeviceToDevice, s));
+  } else {
+    std::vector<float> hs(n_envs, (float)cfg->current_sign);
+    SF_CHECK_CUDA(cudaMemcpyAsync(b->signs, hs.data(), n_envs * 4, cudaMemcpyHostToDevice, s));
+    SF_CHECK_CUDA(cudaStreamSynchronize(s));  // hs is a host temporary
+  }
+  const bool pdl = (flags & SF_AE_PDL) != 0;
+  if (flags & SF_AE_GRAPH) {
+    const int key = cfg_key(cfg) ^ (pdl ? 0x5bd1e995 : 0);
+    if (!b->graph || b->graph_key != key) {
+      rc = capture(*h, &b->graph, [&](cudaStream_t cs) { return enqueue_verify(*h, *b, cfg, cs, pdl); });
+      if (rc) return rc;
+      b->graph_key = key;
+    }
+    SF_CHECK_CUDA(cudaGraphLaunch(b->graph, s));
+    sf::count_launch(0);
+  } else {
+    if ((rc = enqueue_verify(*h, *b, cfg, s, pdl))) return rc;
+  }
+  const size_t khd = hd * cfg->k;
+  if (out->reconstructed)
+    SF_CHECK_CUDA(cudaMemcpyAsync(out->reconstructed, b->recon, khd * 4, cudaMemcpyDeviceToDevice, s));
+  if (out->distances)
+    SF_CHECK_CUDA(cudaMemcpyAsync(out->distances, b->dist, (size_t)n_envs * cfg->k * c.horizon * 4,
+                                  cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(out->branch_prefixes, b->branch, (size_t)n_envs * cfg->k * 4,
+                                cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(out->result, b->result, (size_t)n_envs * SF_RESULT_WORDS * 4,
+                                cudaMemcpyDeviceToDevice, s));
+  return SF_OK;
+}
+
+extern "C" int sf_ae_denoise(void* handle, int n_envs, int num_steps, const float* start,
+                             const float* state, float* chunk_out, int* status, int flags,
+                             void* stream) {
+  auto* h = static_cast<Handle*>(handle);
+  SF_REQUIRE(h && start && state && chunk_out && status, "null argument");
+  SF_REQUIRE(h->k_prefix, "no prefix KV bound (sf_ae_set_prefix)");
+  SF_REQUIRE(n_envs >= 1 && n_envs <= h->n_prefix_envs, "n_envs exceeds the prefix pool");
+  SF_REQUIRE(num_steps >= 1 && num_steps <= 64, "num_steps must be in [1, 64]");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = 0;
+  Buffers* b = get_buffers(*h, n_envs, 1, &rc);
+  if (!b) return rc;
+  const sf_ae_config_t& c = h->cfg;
+  if (h->temb_euler_n != num_steps) {
+    if (h->temb_euler) cudaFree(h->temb_euler);
+    if ((rc = dalloc(&h->temb_euler, (size_t)num_steps * c.width))) return rc;
+    std::vector<float> taus(num_steps);
+    for (int i = 0; i < num_steps; ++i) taus[i] = (float)((double)i / (double)num_steps);
+    if ((rc = compute_temb(*h, taus.data(), num_steps, h->temb_euler, s))) return rc;
+    SF_CHECK_CUDA(cudaStreamSynchronize(s));
+    h->temb_euler_n = num_steps;
+    if (b->graph) {
+      cudaGraphExecDestroy(b->graph);
+      b->graph = nullptr;
+    }
+  }
+  const size_t hd = (size_t)n_envs * c.horizon * c.action_dim;
+  SF_CHECK_CUDA(cudaMemcpyAsync(b->draft, start, hd * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(b->state, state, (size_t)n_envs * c.state_dim * 4,
+                                cudaMemcpyDeviceToDevice, s));
+  std::vector<int> init(2 * n_envs);
+  for (int e = 0; e < n_envs; ++e) {
+    init[2 * e] = -1;
+    init[2 * e + 1] = 0;
+  }
+  SF_CHECK_CUDA(cudaMemcpyAsync(b->status, init.data(), init.size() * 4, cudaMemcpyHostToDevice, s));
+  SF_CHECK_CUDA(cudaStreamSynchronize(s));
+  const bool pdl = (flags & SF_AE_PDL) != 0;
+  if (flags & SF_AE_GRAPH) {
+    const int key = 0x40000000 | (num_steps << 1) | (pdl ? 1 : 0);
+    if (!b->graph || b->graph_key != key) {
+      rc = capture(*h, &b->graph, [&](cudaStream_t cs) { return enqueue_denoise(*h, *b, num_steps, cs, pdl); });
+      if (rc) return rc;
+      b->graph_key = key;
+    }
+    SF_CHECK_CUDA(cudaGraphLaunch(b->graph, s));
+  } else {
+    if ((rc = enqueue_denoise(*h, *b, num_steps, s, pdl))) return rc;
+  }
+  SF_CHECK_CUDA(cudaMemcpyAsync(chunk_out, b->draft, hd * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(status, b->status, (size_t)n_envs * 8, cudaMemcpyDeviceToDevice, s));
+  return SF_OK;
+}
+
+extern "C" int sf_ae_velocity(void* handle, int n_envs, int rows, const float* x, const double* taus,
+                              const float* state, float* v_out, void* stream) {
+  auto* h = static_cast<Handle*>(handle);
+  SF_REQUIRE(h && x && taus && state && v_out, "null argument");
+  SF_REQUIRE(h->k_prefix, "no prefix KV bound (sf_ae_set_prefix)");
+  SF_REQUIRE(n_envs >= 1 && n_envs <= h->n_prefix_envs, "n_envs exceeds the prefix pool");
+  SF_REQUIRE(rows >= 1 && rows <= SF_MAX_K, "rows must be in [1, %d]", SF_MAX_K);
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = 0;
+  Buffers* b = get_buffers(*h, n_envs, rows, &rc);
+  if (!b) return rc;
+  sf_verify_cfg_t c{};
+  c.k = rows;
+  for (int r = 0; r < rows; ++r) {
+    SF_REQUIRE(taus[r] >= 0.0 && taus[r] <= 1.0, "tau=%g outside [0, 1]", taus[r]);
+    c.taus[r] = taus[r];
+  }
+  if ((rc = ensure_temb(*h, &c, s))) return rc;
+  const sf_ae_config_t& cf = h->cfg;
+  const size_t n = (size_t)n_envs * rows * cf.horizon * cf.action_dim;
+  float* actions = nullptr;
+  if ((rc = dalloc(&actions, n))) return rc;
+  SF_CHECK_CUDA(cudaMemcpyAsync(actions, x, n * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(b->state, state, (size_t)n_envs * cf.state_dim * 4,
+                                cudaMemcpyDeviceToDevice, s));
+  EmbedParams ep = embed_params(*h, *b, 1, h->temb);
+  ep.draft = actions;
+  if ((rc = launch_pdl(embed_kernel, dim3(b->M), dim3(256), 0, s, ep, false))) return rc;
+  if ((rc = run_stack(*h, *b, s, false))) return rc;
+  GatherParams gp{b->vel, v_out, n_envs, rows, cf.horizon, cf.action_dim, T_of(*h), b->env_rows};
+  gather_vel_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(gp);
+  SF_CHECK_CUDA(cudaGetLastError());
+  sf::count_launch();
+  SF_CHECK_CUDA(cudaStreamSynchronize(s));
+  cudaFree(actions);
+  return SF_OK;
+}
+
+namespace sf {
+namespace pi0 {
+
+}  // namespace pi0
+}  // namespace sf

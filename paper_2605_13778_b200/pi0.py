@@ -1,0 +1,328 @@
+"""pi0-scale Action Expert on the device (BASELINE configs 3-5).
+
+The reference substitutes MLPs for the Action Expert; this is
+the builder-defined pi0-scale field: 18 layers, width 1024, 8
+query heads x 256 sharing one KV head (MQA), GeGLU 4096, RMSNorm, RoPE,
+attending to a per-env VLM prefix KV cache (800 tokens) with the paper's
+block mask. It honours the reference's field protocol
+(``evaluate(values, tau, cache, state)``, ``horizon``, ``dim``, ``layout``,
+``eval_count`` — flowpolicy.py:249-261), so the drop-in ``verify`` /
+``integrate_flow`` dispatch to its fused device chains:
+
+* ``device_verify``  -> ``sf_ae_verify`` (embed -> 18 x [QKV GEMM+RoPE, MQA
+  attention, O GEMM, GeGLU GEMM, down GEMM] -> head GEMM -> verify
+  epilogue), one CUDA graph with programmatic dependent launch;
+* ``device_denoise`` -> ``sf_ae_denoise`` (N Euler steps in one graph).
+
+Weights are random-init with a counter-based generator shared bit-for-bit with
+``oracle/pi0_oracle.py`` and stored in the kernels' layouts (q/k rows paired
+for RoPE, gate/up rows interleaved).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _capi, _device
+from .actions import ChannelLayout
+
+SF_AE_GRAPH, SF_AE_PDL = 1, 2
+TID_A_W, TID_S_W, TID_T1_W, TID_T2_W, TID_OUT_W = 1, 2, 3, 4, 5
+TID_LAYER_BASE = 100
+TID_KV_BASE = 10000
+
+
+@dataclass(frozen=True)
+class AEConfig:
+    width: int = 1024
+    layers: int = 18
+    q_heads: int = 8
+    head_dim: int = 256
+    mlp: int = 4096
+    action_dim: int = 32
+    state_dim: int = 32
+    horizon: int = 50
+    prefix_len: int = 800
+    rope_base: float = 10000.0
+    eps: float = 1e-6
+    temb_min_period: float = 4e-3
+    temb_max_period: float = 4.0
+
+    @property
+    def seg_len(self) -> int:
+        return 1 + self.horizon
+
+    def n_params(self) -> int:
+        W, nq = self.width, self.q_heads * self.head_dim
+        per_layer = (nq + 2 * self.head_dim) * W + W * nq + 2 * self.mlp * W + W * self.mlp
+        io = (W * self.action_dim + W) + (W * self.state_dim + W) + 2 * (W * W + W) + \
+            (self.action_dim * W + self.action_dim)
+        return self.layers * per_layer + io
+
+    def weight_bytes_streamed(self) -> int:
+        """bf16 bytes of the per-layer GEMM weights + head read per forward."""
+        W, nq = self.width, self.q_heads * self.head_dim
+        per_layer = (nq + 2 * self.head_dim) * W + W * nq + 2 * self.mlp * W + W * self.mlp
+        return 2 * (self.layers * per_layer + self.action_dim * W)
+
+    def kv_bytes(self) -> int:
+        return 2 * 2 * self.layers * self.prefix_len * self.head_dim
+
+
+PI0 = AEConfig()
+
+
+class _AeConfigC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("width", "layers", "q_heads", "head_dim", "mlp",
+                                            "action_dim", "state_dim", "horizon", "prefix_len")] + \
+               [("eps", ctypes.c_float), ("temb_min_period", ctypes.c_float),
+                ("temb_max_period", ctypes.c_float)]
+
+
+_MAXL = 32
+
+
+class _AeWeightsC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("a_w", "a_b", "s_w", "s_b", "t1_w", "t1_b", "t2_w",
+                                               "t2_b", "out_w", "out_b")] + \
+               [("qkv", ctypes.c_void_p * _MAXL), ("o", ctypes.c_void_p * _MAXL),
+                ("gu", ctypes.c_void_p * _MAXL), ("down", ctypes.c_void_p * _MAXL),
+                ("rope", ctypes.c_void_p)]
+
+
+def _fill(t: torch.Tensor, seed: int, tid: int, std: float) -> torch.Tensor:
+    _capi.check(_capi.lib().sf_fill_hash_uniform(
+        t.data_ptr(), 1 if t.dtype == torch.bfloat16 else 0, t.numel(), seed, tid, std,
+        torch.cuda.current_stream().cuda_stream), "init")
+    return t
+
+
+def rope_table(cfg: AEConfig, max_pos: int) -> np.ndarray:
+    half = cfg.head_dim // 2
+    inv = cfg.rope_base ** (-np.arange(half, dtype=np.float64) * 2.0 / cfg.head_dim)
+    ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv[None, :]
+    return np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
+
+
+def qkv_row_perm(cfg: AEConfig) -> torch.Tensor:
+    """device row -> natural row: per head, rows (2i, 2i+1) = dims (i, i+128)."""
+    hd, half = cfg.head_dim, cfg.head_dim // 2
+    perm = []
+    for head in range(cfg.q_heads + 1):  # q heads, then the k head
+        base = head * hd
+        for i in range(half):
+            perm += [base + i, base + i + half]
+    base = (cfg.q_heads + 1) * hd
+    perm += list(range(base, base + hd))  # v rows unchanged
+    return torch.tensor(perm, dtype=torch.long)
+
+
+def gu_row_perm(cfg: AEConfig) -> torch.Tensor:
+    """device row -> natural row: rows (2i, 2i+1) = (gate_i, up_i)."""
+    idx = torch.arange(cfg.mlp)
+    return torch.stack([idx, idx + cfg.mlp], dim=1).reshape(-1)
+
+
+class ActionExpert:
+    """Device-resident pi0-scale Action Expert + prefix KV pool (field protocol)."""
+
+    def __init__(self, cfg: AEConfig = PI0, seed: int = 0, n_envs: int = 1, kv_seed: int = 1,
+                 layout: ChannelLayout | None = None, std: float = 0.02,
+                 flags: int = SF_AE_GRAPH | SF_AE_PDL):
+        self.cfg = cfg
+        self.horizon = cfg.horizon
+        self.dim = cfg.action_dim
+        self.layout = layout or ChannelLayout(cfg.action_dim - 1, 0)
+        if self.layout.dim != cfg.action_dim:
+            raise ValueError("layout does not match action_dim")
+        self.eval_count = 0
+        self.flags = flags
+        self.seed = seed
+        dev = _device.device()
+        W, nq, L = cfg.width, cfg.q_heads * cfg.head_dim, cfg.layers
+        f32, b16 = torch.float32, torch.bfloat16
+        self._keep = []
+
+        def mk(shape, dtype, tid, s=std):
+            t = _fill(torch.empty(shape, dtype=dtype, device=dev), seed, tid, s)
+            self._keep.append(t)
+            return t
+
+        def zeros(n):
+            t = torch.zeros(n, dtype=f32, device=dev)
+            self._keep.append(t)
+            return t
+
+        w = _AeWeightsC()
+        w.a_w = mk((W, cfg.action_dim), f32, TID_A_W).data_ptr()
+        w.a_b = zeros(W).data_ptr()
+        w.s_w = mk((W, cfg.state_dim), f32, TID_S_W).data_ptr()
+        w.s_b = zeros(W).data_ptr()
+        w.t1_w = mk((W, W), f32, TID_T1_W).data_ptr()
+        w.t1_b = zeros(W).data_ptr()
+        w.t2_w = mk((W, W), f32, TID_T2_W).data_ptr()
+        w.t2_b = zeros(W).data_ptr()
+        w.out_w = mk((cfg.action_dim, W), b16, TID_OUT_W).data_ptr()
+        w.out_b = zeros(cfg.action_dim).data_ptr()
+        pq = qkv_row_perm(cfg).to(dev)
+        pg = gu_row_perm(cfg).to(dev)
+        for l in range(L):
+            b = TID_LAYER_BASE + 4 * l
+            qkv_nat = _fill(torch.empty((nq + 2 * cfg.head_dim, W), dtype=b16, device=dev), seed, b, std)
+            qkv = qkv_nat.index_select(0, pq).contiguous()
+            del qkv_nat
+            gu_nat = _fill(torch.empty((2 * cfg.mlp, W), dtype=b16, device=dev), seed, b + 2, std)
+            gu = gu_nat.index_select(0, pg).contiguous()
+            del gu_nat
+            o = mk((W, nq), b16, b + 1)
+            down = mk((W, cfg.mlp), b16, b + 3)
+            self._keep += [qkv, gu]
+            w.qkv[l], w.o[l], w.gu[l], w.down[l] = (qkv.data_ptr(), o.data_ptr(), gu.data_ptr(),
+                                                    down.data_ptr())
+        rope = torch.from_numpy(rope_table(cfg, cfg.prefix_len + cfg.seg_len)).to(dev)
+        self._keep.append(rope)
+        w.rope = rope.data_ptr()
+        c = _AeConfigC(cfg.width, cfg.layers, cfg.q_heads, cfg.head_dim, cfg.mlp, cfg.action_dim,
+                       cfg.state_dim, cfg.horizon, cfg.prefix_len, cfg.eps, cfg.temb_min_period,
+                       cfg.temb_max_period)
+        self._cfg_c, self._w_c = c, w
+        h = ctypes.c_void_p()
+        _capi.check(_capi.lib().sf_ae_create(ctypes.byref(c), ctypes.byref(w), ctypes.byref(h)),
+                    "ae create")
+        self._h = h
+        self.n_envs = 0
+        self.set_prefix_pool(n_envs, kv_seed)
+
+    # ---------------------------------------------------------- prefix KV
+    def set_prefix_pool(self, n_envs: int, kv_seed: int = 1):
+        """Random-init prefix KV for n_envs envs (stand-in for the VLM prefill)."""
+        cfg, dev = self.cfg, _device.device()
+        L, P, hd = cfg.layers, cfg.prefix_len, cfg.head_dim
+        self.k_prefix = torch.empty((L, n_envs, P, hd), dtype=torch.bfloat16, device=dev)
+        self.vt_prefix = torch.empty((L, n_envs, hd, P), dtype=torch.bfloat16, device=dev)
+        for e in range(n_envs):
+            for l in range(L):
+                t = TID_KV_BASE + 2 * (e * L + l)
+                _fill(self.k_prefix[l, e], kv_seed, t, 1.0)
+                _fill(self.vt_prefix[l, e], kv_seed, t + 1, 1.0)
+        _capi.check(_capi.lib().sf_ae_set_prefix(self._h, self.k_prefix.data_ptr(),
+                                                 self.vt_prefix.data_ptr(), n_envs), "prefix")
+        self.n_envs = n_envs
+        self.kv_seed = kv_seed
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                _capi.lib().sf_ae_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    # ----------------------------------------------------- device batched API
+    def verify_batch(self, cfg, draft: torch.Tensor, eps: torch.Tensor, state: torch.Tensor,
+                     signs: torch.Tensor | None = None, current_sign: float = -1.0,
+                     phase_fallback=True, prefix_cap=True, replan_size=12, outputs=None,
+                     stream=None):
+        """Device tensors in, device tensors out (no sync). draft/eps [B,H,D] f32,
+        state [B,S] f32, signs [B] f32. Returns (recon, dist, branch, result)."""
+        from .verifier import make_cfg
+
+        B = draft.shape[0]
+        K = len(cfg.timesteps)
+        dev = draft.device
+        if outputs is None:
+            outputs = (torch.empty((B, K, self.horizon, self.dim), dtype=torch.float32, device=dev),
+                       torch.empty((B, K, self.horizon), dtype=torch.float32, device=dev),
+                       torch.empty((B, K), dtype=torch.int32, device=dev),
+                       torch.empty((B, _capi.SF_RESULT_WORDS), dtype=torch.int32, device=dev))
+        recon, dist, branch, result = outputs
+        c = make_cfg(cfg, current_sign, phase_fallback, prefix_cap, replan_size)
+        out = _capi.SfVerifyOut(None, recon.data_ptr() if recon is not None else None,
+                                dist.data_ptr() if dist is not None else None, branch.data_ptr(),
+                                result.data_ptr())
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _capi.check(_capi.lib().sf_ae_verify(
+            self._h, B, ctypes.byref(c), draft.data_ptr(), eps.data_ptr(), state.data_ptr(),
+            signs.data_ptr() if signs is not None else None, ctypes.byref(out), self.flags, s),
+            "ae verify")
+        return outputs
+
+    def denoise_batch(self, start: torch.Tensor, state: torch.Tensor, n_steps: int,
+                      chunk: torch.Tensor | None = None, status: torch.Tensor | None = None,
+                      stream=None):
+        B = start.shape[0]
+        dev = start.device
+        chunk = torch.empty_like(start) if chunk is None else chunk
+        status = torch.empty((B, 2), dtype=torch.int32, device=dev) if status is None else status
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _capi.check(_capi.lib().sf_ae_denoise(self._h, B, n_steps, start.data_ptr(),
+                                              state.data_ptr(), chunk.data_ptr(), status.data_ptr(),
+                                              self.flags, s), "ae denoise")
+        return chunk, status
+
+    def velocity_batch(self, x: torch.Tensor, taus, state: torch.Tensor) -> torch.Tensor:
+        """x [B, R, H, D] f32 -> v [B, R, H, D] (field protocol, batched)."""
+        B, R = x.shape[0], x.shape[1]
+        out = torch.empty_like(x)
+        _capi.check(_capi.lib().sf_ae_velocity(
+            self._h, B, R, x.data_ptr(), _capi.host_doubles(list(taus)), state.data_ptr(),
+            out.data_ptr(), torch.cuda.current_stream().cuda_stream), "ae velocity")
+        return out
+
+    # --------------------------------------------- reference field protocol
+    def _env_of(self, cache) -> int:
+        env = int(cache.kv) if cache is not None and cache.kv is not None else 0
+        if not 0 <= env < self.n_envs:
+            raise ValueError(f"cache refers to prefix env {env}, pool has {self.n_envs}")
+        return env
+
+    def evaluate(self, values, tau, cache, state) -> np.ndarray:
+        """v(A, tau) for one chunk (flowpolicy.py:203-209 protocol)."""
+        self.eval_count += 1
+        if self._env_of(cache) != 0:
+            raise ValueError("single-chunk evaluation uses prefix env 0")
+        dev = _device.device()
+        x = torch.as_tensor(np.asarray(values, np.float32)).to(dev).reshape(1, 1, self.horizon, self.dim)
+        st = torch.as_tensor(np.asarray(state, np.float32)).to(dev).reshape(1, -1)
+        return self.velocity_batch(x, [tau], st)[0, 0].double().cpu().numpy()
+
+    def device_verify(self, draft, cache, state, cfg, eps, current_sign, noise_seed):
+        from .verifier import VerifierReport
+
+        if self._env_of(cache) != 0:
+            raise ValueError("single-env verify uses prefix env 0")
+        dev = _device.device()
+        d = torch.as_tensor(np.asarray(draft.values, np.float32)).to(dev)[None]
+        e = torch.as_tensor(np.asarray(eps, np.float32)).to(dev)[None]
+        st = torch.as_tensor(np.asarray(state, np.float32)).to(dev).reshape(1, -1)
+        recon, dist, branch, result = self.verify_batch(cfg, d, e, st, current_sign=current_sign)
+        res = result[0].cpu().numpy()
+        if int(res[_capi.RES_NONFINITE]) >= 0:
+            raise FloatingPointError(
+                f"velocity produced non-finite values at tau={cfg.timesteps[int(res[_capi.RES_NONFINITE])]}")
+        return VerifierReport(
+            reconstructed=recon[0].double().cpu().numpy(), distances=dist[0].double().cpu().numpy(),
+            branch_prefixes=tuple(int(x) for x in branch[0].cpu()),
+            prefix=int(res[_capi.RES_PREFIX]), gripper_switch_detected=bool(res[_capi.RES_SWITCH]),
+            shared_noise_seed=noise_seed, decision=_capi.PATH_CODES[int(res[_capi.RES_PATH])],
+            planned=int(res[_capi.RES_PLANNED]))
+
+    def device_denoise(self, cache, state, start, n) -> np.ndarray:
+        if self._env_of(cache) != 0:
+            raise ValueError("single-env denoise uses prefix env 0")
+        self.eval_count += n
+        dev = _device.device()
+        a0 = torch.as_tensor(np.asarray(start, np.float32)).to(dev)[None]
+        st = torch.as_tensor(np.asarray(state, np.float32)).to(dev).reshape(1, -1)
+        chunk, status = self.denoise_batch(a0, st, n)
+        sv = status[0].cpu().numpy()
+        if sv[0] >= 0:
+            step = int(sv[0])
+            if sv[1]:
+                raise FloatingPointError(f"velocity produced non-finite values at tau={step / n}")
+            raise FloatingPointError(f"denoising diverged at step {step} (tau={step / n})")
+        return chunk[0].double().cpu().numpy()
