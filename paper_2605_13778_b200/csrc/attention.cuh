@@ -38,6 +38,7 @@ constexpr uint32_t kPBytes = BQ * BKEY * 2;       // 16 KB
 constexpr uint32_t kStageBytes = kKBytes + kVBytes;
 constexpr uint32_t kSmemBytes = kQBytes + 2 * kStageBytes + kPBytes + 1024 /*bars*/ + 1024 /*align*/;
 constexpr int kTmemCols = 512;  // S0 [0,64) S1 [64,128) O [128,384)
+constexpr int kWsRow = HD + 4;  // split-KV partial row: O[256], m, l (+pad: 16 B aligned rows)
 
 struct Params {
   int M;            // valid token rows
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     } else {
-      constexpr int kRow = HD + 2;
+      constexpr int kRow = kWsRow;
       float* mine = p.ws + (((size_t)tile * p.splits + split) * BQ + r) * kRow;
       for (int c0 = 0; c0 < HD; c0 += 16) {
         uint32_t o[16];

@@ -462,7 +462,7 @@ int build(Handle& h, Buffers& b, int B, int K) {
   asplit = (n_blocks + bps - 1) / bps;
   b.attn_splits = asplit;
   float* attn_ws = nullptr;
-  if (asplit > 1) ALLOC(attn_ws, (size_t)b.attn_tiles * asplit * attn::BQ * (attn::HD + 2));
+  if (asplit > 1) ALLOC(attn_ws, (size_t)b.attn_tiles * asplit * attn::BQ * attn::kWsRow);
   b.n_counters = (max_tiles > b.attn_tiles ? max_tiles : b.attn_tiles) + 8;
   ALLOC(b.counters, (size_t)b.n_counters);
 #undef ALLOC
