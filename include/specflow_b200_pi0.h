@@ -36,6 +36,8 @@ typedef struct {
   int prefix_len;  /* P = 800 prefix KV tokens */
   float eps;       /* RMSNorm epsilon */
   float temb_min_period, temb_max_period;
+  int draft_in;     /* draft MLP input features (multiple of 64); 0 = no draft */
+  int draft_hidden; /* draft MLP hidden width (multiple of 64) */
 } sf_ae_config_t;
 
 /* Device weights in DEVICE layout (see paper_2605_13778_b200/pi0.py):
@@ -47,7 +49,9 @@ typedef struct {
  *  o[l] [W, heads*256] bf16
  *  gu[l] [2*mlp, W] bf16            rows interleaved (gate_i, up_i)
  *  down[l] [W, mlp] bf16
- *  rope [(P + 1 + H) * 128] float2 (cos, sin) */
+ *  rope [(P + 1 + H) * 128] float2 (cos, sin)
+ *  draft_w[0..2] bf16 [hid, in], [hid, hid], [H*D, hid]; draft_b[0..2] f32
+ *  (tanh MLP draft, draft.py:57-61 at pi0 scale) */
 typedef struct {
   const void *a_w, *a_b, *s_w, *s_b, *t1_w, *t1_b, *t2_w, *t2_b, *out_w, *out_b;
   const void* qkv[SF_AE_MAX_LAYERS];
@@ -55,6 +59,8 @@ typedef struct {
   const void* gu[SF_AE_MAX_LAYERS];
   const void* down[SF_AE_MAX_LAYERS];
   const void* rope;
+  const void* draft_w[3];
+  const void* draft_b[3];
 } sf_ae_weights_t;
 
 int sf_ae_create(const sf_ae_config_t* cfg, const sf_ae_weights_t* weights, void** handle);
@@ -74,6 +80,18 @@ int sf_ae_set_prefix(void* handle, const void* k_prefix, const void* vt_prefix, 
 int sf_ae_verify(void* handle, int n_envs, const sf_verify_cfg_t* cfg, const float* draft,
                  const float* eps, const float* state, const float* signs,
                  const sf_verify_out_t* out, int flags, void* stream);
+
+/* Batched speculative round = propose (draft MLP on obs [n_envs][draft_in]
+ * f32, draft.py:57-61) + sf_ae_verify in ONE graph; out->draft receives the
+ * draft [n_envs][H][D] f32 (runtime.py:173-198 flash_attempt). */
+int sf_ae_flash_round(void* handle, int n_envs, const sf_verify_cfg_t* cfg, const float* obs,
+                      const float* eps, const float* state, const float* signs,
+                      const sf_verify_out_t* out, int flags, void* stream);
+
+/* Run planned GEMM op `op` (0 .. 4*layers) of the (n_envs, k)
+ * verify plan `iters` times back to back on `stream` — bench hook for the
+ * per-kernel roofline. */
+int sf_ae_time_op(void* handle, int n_envs, int k, int op, int iters, void* stream);
 
 /* Batched full path (flowpolicy.py:273-292): `start` = A^0 [n_envs][H][D];
  * chunk_out [n_envs][H][D]; status [n_envs][2] = {first non-finite step or -1,

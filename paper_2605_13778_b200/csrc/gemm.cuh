@@ -60,13 +60,15 @@ __device__ __forceinline__ void apply_chunk(const Params& p, float (&v)[16], int
   }
   switch (e.kind) {
     case EPI_F32:
-    case EPI_BF16: {
+    case EPI_BF16:
+    case EPI_TANH_BF16: {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int m = swap ? tile_b * p.bn + c0 + j : tile_a * BM + lane_row;
         const int n = swap ? tile_a * BM + lane_row : tile_b * p.bn + c0 + j;
         if (m < e.M && n < e.N) {
-          const float o = e.bias ? v[j] + e.bias[n] : v[j];
+          float o = e.bias ? v[j] + e.bias[n] : v[j];
+          if (e.kind == EPI_TANH_BF16) o = tanhf(o);
           if (e.kind == EPI_F32) e.out_f32[(size_t)m * e.ld_f32 + n] = o;
           else e.out_bf16[(size_t)m * e.ld_bf16 + n] = __float2bfloat16_rn(o);
         }

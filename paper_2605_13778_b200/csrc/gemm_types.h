@@ -19,6 +19,7 @@ enum EpiKind : int {
   EPI_QKV = 2,    // RMS scale, RoPE on q/k (paired rows), q/k row-major, v transposed
   EPI_RESID = 3,  // x[m, n] += acc; xb = bf16(x); ssq partials per 128-feature group
   EPI_GEGLU = 4,  // RMS scale, h[m, n/2] = gelu_tanh(gate) * up for paired rows
+  EPI_TANH_BF16 = 5,  // out_bf16[m, n] = bf16(tanh(acc + bias[n]))  (draft MLP hidden)
 };
 
 struct EpiArgs {

@@ -244,6 +244,32 @@ __global__ void euler_rows_kernel(const EulerParams p) {
   if (threadIdx.x == 0) sm100::pdl_launch_dependents();
 }
 
+struct StatusParams {
+  int* status;
+  int B;
+};
+
+__global__ void status_init_kernel(const StatusParams p) {
+  for (int e = threadIdx.x; e < p.B; e += blockDim.x) {
+    p.status[2 * e] = -1;
+    p.status[2 * e + 1] = 0;
+  }
+}
+
+struct CastParams {
+  const float* src;
+  bf16* dst;
+  int n;
+};
+
+// obs f32 -> bf16 GEMM operand (draft MLP input).
+__global__ void cast_bf16_kernel(const CastParams p) {
+  sm100::pdl_wait();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += gridDim.x * blockDim.x)
+    p.dst[i] = __float2bfloat16_rn(p.src[i]);
+  if (threadIdx.x == 0) sm100::pdl_launch_dependents();
+}
+
 struct GatherParams {
   const float* vel;
   float* out;  // [B][K][H][D]
@@ -294,6 +320,14 @@ struct Buffers {
   std::vector<CUtensorMap> attn_maps;  // per layer: q, kp, vp, ks, vs
   cudaGraphExec_t graph = nullptr;
   int graph_key = 0;
+  int graph_kernels = 0;  // kernel nodes in `graph` (launch accounting)
+  // draft MLP (flash rounds)
+  float* obs = nullptr;   // [B][F]
+  bf16* obs_b = nullptr;  // [b_ld][F]
+  bf16* dh1 = nullptr;    // [b_ld][hidden]
+  bf16* dh2 = nullptr;
+  gemm::Op dops[3];
+  bool has_draft = false;
 };
 
 struct Handle {
@@ -412,6 +446,14 @@ int build(Handle& h, Buffers& b, int B, int K) {
   ALLOC(b.branch, (size_t)B * K);
   ALLOC(b.result, (size_t)B * SF_RESULT_WORDS);
   ALLOC(b.status, (size_t)B * 2);
+  const int b_ld = ((B + 63) / 64) * 64;
+  b.has_draft = c.draft_in > 0 && h.w.draft_w[0] != nullptr;
+  if (b.has_draft) {
+    ALLOC(b.obs, (size_t)B * c.draft_in);
+    ALLOC(b.obs_b, (size_t)b_ld * c.draft_in);
+    ALLOC(b.dh1, (size_t)b_ld * c.draft_hidden);
+    ALLOC(b.dh2, (size_t)b_ld * c.draft_hidden);
+  }
 
   // --- GEMM plans. Batch-1 shapes stream weights (swap-AB + split-K);
   // larger batches run the normal orientation with 256-feature tiles.
@@ -534,6 +576,43 @@ int build(Handle& h, Buffers& b, int B, int K) {
                       b.ws, b.ws_bytes, b.counters, b.n_counters);
     if (rc) return rc;
   }
+  // --- draft MLP plans: rows = envs (swap-AB while B <= 256)
+  if (b.has_draft) {
+    const bool dswap = B <= 256;
+    const int dbn = dswap ? ((B + 15) / 16) * 16 : 256;
+    const int HDc = c.horizon * c.action_dim;
+    const void* ins[3] = {b.obs_b, b.dh1, b.dh2};
+    const int kin[3] = {c.draft_in, c.draft_hidden, c.draft_hidden};
+    const int nout[3] = {c.draft_hidden, c.draft_hidden, HDc};
+    bf16* outs[2] = {b.dh1, b.dh2};
+    for (int i = 0; i < 3; ++i) {
+      gemm::EpiArgs e{};
+      e.kind = i < 2 ? gemm::EPI_TANH_BF16 : gemm::EPI_F32;
+      e.M = B;
+      e.N = nout[i];
+      e.bias = static_cast<const float*>(h.w.draft_b[i]);
+      if (i < 2) {
+        e.out_bf16 = outs[i];
+        e.ld_bf16 = c.draft_hidden;
+      } else {
+        e.out_f32 = b.draft;
+        e.ld_f32 = HDc;
+      }
+      const int tiles = dswap ? (nout[i] + 127) / 128 : ((B + 127) / 128) * ((nout[i] + 255) / 256);
+      int sp = 148 / tiles;
+      sp = sp < 1 ? 1 : (sp > kin[i] / 64 ? kin[i] / 64 : sp);
+      const size_t need = dswap ? gemm::ws_bytes_needed(nout[i], B, kin[i], dbn, sp)
+                                : gemm::ws_bytes_needed(B, nout[i], kin[i], dbn, sp);
+      if (need > b.ws_bytes || tiles > b.n_counters) sp = 1;
+      if (dswap)
+        rc = gemm::plan(&b.dops[i], h.w.draft_w[i], nout[i], kin[i], ins[i], B, kin[i], kin[i], dbn,
+                        sp, 1, e, b.ws, b.ws_bytes, b.counters, b.n_counters);
+      else
+        rc = gemm::plan(&b.dops[i], ins[i], B, kin[i], h.w.draft_w[i], nout[i], kin[i], kin[i], dbn,
+                        sp, 0, e, b.ws, b.ws_bytes, b.counters, b.n_counters);
+      if (rc) return rc;
+    }
+  }
   // --- attention plans (per layer: 5 tensor maps)
   attn::Params& ap = b.ap;
   ap.M = b.M;
@@ -636,10 +715,19 @@ EmbedParams embed_params(const Handle& h, const Buffers& b, int mode, const floa
 }
 
 // Verify chain for the staged inputs of `b` (draft/eps/state/signs already in b).
-int enqueue_verify(Handle& h, Buffers& b, const sf_verify_cfg_t* cfg, cudaStream_t s, bool pdl) {
+int enqueue_verify(Handle& h, Buffers& b, const sf_verify_cfg_t* cfg, cudaStream_t s, bool pdl,
+                   bool with_draft = false) {
   int rc;
+  if (with_draft) {
+    // propose (draft.py:57-61): obs -> tanh MLP -> draft [B][H][D] into b.draft
+    CastParams cp{b.obs, b.obs_b, b.B * h.cfg.draft_in};
+    if ((rc = launch_pdl(cast_bf16_kernel, dim3((cp.n + 255) / 256), dim3(256), 0, s, cp, false)))
+      return rc;
+    for (int i = 0; i < 3; ++i)
+      if ((rc = gemm::launch(b.dops[i], s, pdl))) return rc;
+  }
   EmbedParams ep = embed_params(h, b, 0, h.temb);
-  if ((rc = launch_pdl(embed_kernel, dim3(b.M), dim3(256), 0, s, ep, false))) return rc;
+  if ((rc = launch_pdl(embed_kernel, dim3(b.M), dim3(256), 0, s, ep, with_draft && pdl))) return rc;
   if ((rc = run_stack(h, b, s, pdl))) return rc;
   VerifyEpiParams vp{};
   const sf_ae_config_t& c = h.cfg;
@@ -678,9 +766,11 @@ int enqueue_verify(Handle& h, Buffers& b, const sf_verify_cfg_t* cfg, cudaStream
 int enqueue_denoise(Handle& h, Buffers& b, int n_steps, cudaStream_t s, bool pdl) {
   int rc;
   const int W = h.cfg.width;
+  StatusParams sp{b.status, b.B};
+  if ((rc = launch_pdl(status_init_kernel, dim3(1), dim3(256), 0, s, sp, false))) return rc;
   for (int i = 0; i < n_steps; ++i) {
     EmbedParams ep = embed_params(h, b, 1, h.temb_euler + (size_t)i * W);
-    if ((rc = launch_pdl(embed_kernel, dim3(b.M), dim3(256), 0, s, ep, i > 0 && pdl))) return rc;
+    if ((rc = launch_pdl(embed_kernel, dim3(b.M), dim3(256), 0, s, ep, pdl))) return rc;
     if ((rc = run_stack(h, b, s, pdl))) return rc;
     const int total = b.B * h.cfg.horizon * h.cfg.action_dim;
     EulerParams up{b.draft, b.vel, b.B, h.cfg.horizon, h.cfg.action_dim, b.env_rows, n_steps, i,
@@ -691,8 +781,8 @@ int enqueue_denoise(Handle& h, Buffers& b, int n_steps, cudaStream_t s, bool pdl
   return SF_OK;
 }
 
-Buffers* get_buffers(Handle& h, int B, int K, int* rc) {
-  const long long key = (long long)B * 1000 + K;
+Buffers* get_buffers(Handle& h, int B, int K, int mode, int* rc) {
+  const long long key = ((long long)mode << 40) | ((long long)B << 8) | K;
   auto it = h.buffers.find(key);
   if (it != h.buffers.end()) return it->second.get();
   auto b = std::make_unique<Buffers>();
@@ -705,12 +795,16 @@ Buffers* get_buffers(Handle& h, int B, int K, int* rc) {
 
 // Capture `fn(stream)` into a graph on the handle's capture stream.
 template <typename F>
-int capture(Handle& h, cudaGraphExec_t* exec, F&& fn) {
+int capture(Handle& h, cudaGraphExec_t* exec, int* n_kernels, F&& fn) {
   if (!h.capture_stream)
     SF_CHECK_CUDA(cudaStreamCreateWithFlags(&h.capture_stream, cudaStreamNonBlocking));
   cudaGraph_t g = nullptr;
   SF_CHECK_CUDA(cudaStreamBeginCapture(h.capture_stream, cudaStreamCaptureModeThreadLocal));
+  const int64_t before = sf_launch_count(0);
   const int rc = fn(h.capture_stream);
+  // captured kernels are recorded, not launched: they count on each replay
+  *n_kernels = (int)(sf_launch_count(0) - before);
+  count_launch(-*n_kernels);
   cudaError_t e = cudaStreamEndCapture(h.capture_stream, &g);
   if (rc) {
     if (g) cudaGraphDestroy(g);
@@ -828,14 +922,7 @@ static int ensure_temb(Handle& h, const sf_verify_cfg_t* cfg, cudaStream_t s) {
   return compute_temb(h, h.temb_taus, cfg->k, h.temb, s);
 }
 
-extern "C" int sf_ae_verify(void* handle, int n_envs, const sf_verify_cfg_t* cfg, const float* draft,
-                            const float* eps, const float* state, const float* signs,
-                            const sf_verify_out_t* out, int flags, void* stream) {
-  auto* h = static_cast<Handle*>(handle);
-  SF_REQUIRE(h && cfg && draft && eps && state && out && out->branch_prefixes && out->result,
-             "null argument");
-  SF_REQUIRE(h->k_prefix, "no prefix KV bound (sf_ae_set_prefix)");
-  SF_REQUIRE(n_envs >= 1 && n_envs <= h->n_prefix_envs, "n_envs exceeds the prefix pool");
+static int check_verify_cfg(const sf_verify_cfg_t* cfg, const float* signs) {
   SF_REQUIRE(cfg->k >= 1 && cfg->k <= SF_MAX_K, "need 1..%d verification timesteps", SF_MAX_K);
   for (int i = 0; i < cfg->k; ++i) {
     SF_REQUIRE(cfg->taus[i] > 0.0 && cfg->taus[i] < 1.0,
@@ -846,14 +933,32 @@ extern "C" int sf_ae_verify(void* handle, int n_envs, const sf_verify_cfg_t* cfg
   SF_REQUIRE(cfg->metric == SF_METRIC_L2 || cfg->metric == SF_METRIC_LINF, "unknown metric");
   SF_REQUIRE(signs || cfg->current_sign == 1.0 || cfg->current_sign == -1.0,
              "current_sign must be -1.0 or +1.0");
-  cudaStream_t s = (cudaStream_t)stream;
-  int rc = 0;
-  Buffers* b = get_buffers(*h, n_envs, cfg->k, &rc);
+  SF_REQUIRE(cfg->replan_size >= 1, "replan_size must be >= 1");
+  return SF_OK;
+}
+
+// Shared body of sf_ae_verify / sf_ae_flash_round. `in` is the draft
+// [B][H][D] (with_draft = false) or the draft features [B][F] (true).
+static int verify_common(Handle* h, int n_envs, const sf_verify_cfg_t* cfg, const float* in,
+                         bool with_draft, const float* eps, const float* state, const float* signs,
+                         const sf_verify_out_t* out, int flags, cudaStream_t s) {
+  SF_REQUIRE(h && cfg && in && eps && state && out && out->branch_prefixes && out->result,
+             "null argument");
+  SF_REQUIRE(h->k_prefix, "no prefix KV bound (sf_ae_set_prefix)");
+  SF_REQUIRE(n_envs >= 1 && n_envs <= h->n_prefix_envs, "n_envs exceeds the prefix pool");
+  int rc = check_verify_cfg(cfg, signs);
+  if (rc) return rc;
+  Buffers* b = get_buffers(*h, n_envs, cfg->k, 0, &rc);
   if (!b) return rc;
+  SF_REQUIRE(!with_draft || b->has_draft, "this expert was built without a draft model");
   if ((rc = ensure_temb(*h, cfg, s))) return rc;
   const sf_ae_config_t& c = h->cfg;
   const size_t hd = (size_t)n_envs * c.horizon * c.action_dim;
-  SF_CHECK_CUDA(cudaMemcpyAsync(b->draft, draft, hd * 4, cudaMemcpyDeviceToDevice, s));
+  if (with_draft)
+    SF_CHECK_CUDA(cudaMemcpyAsync(b->obs, in, (size_t)n_envs * c.draft_in * 4,
+                                  cudaMemcpyDeviceToDevice, s));
+  else
+    SF_CHECK_CUDA(cudaMemcpyAsync(b->draft, in, hd * 4, cudaMemcpyDeviceToDevice, s));
   SF_CHECK_CUDA(cudaMemcpyAsync(b->eps, eps, hd * 4, cudaMemcpyDeviceToDevice, s));
   SF_CHECK_CUDA(cudaMemcpyAsync(b->state, state, (size_t)n_envs * c.state_dim * 4,
                                 cudaMemcpyDeviceToDevice, s));
@@ -866,18 +971,22 @@ extern "C" int sf_ae_verify(void* handle, int n_envs, const sf_verify_cfg_t* cfg
   }
   const bool pdl = (flags & SF_AE_PDL) != 0;
   if (flags & SF_AE_GRAPH) {
-    const int key = cfg_key(cfg) ^ (pdl ? 0x5bd1e995 : 0);
+    const int key = cfg_key(cfg) ^ (pdl ? 0x5bd1e995 : 0) ^ (with_draft ? 0x2f3a7c11 : 0);
     if (!b->graph || b->graph_key != key) {
-      rc = capture(*h, &b->graph, [&](cudaStream_t cs) { return enqueue_verify(*h, *b, cfg, cs, pdl); });
+      rc = capture(*h, &b->graph, &b->graph_kernels, [&](cudaStream_t cs) {
+        return enqueue_verify(*h, *b, cfg, cs, pdl, with_draft);
+      });
       if (rc) return rc;
       b->graph_key = key;
     }
     SF_CHECK_CUDA(cudaGraphLaunch(b->graph, s));
-    sf::count_launch(0);
+    sf::count_launch(b->graph_kernels);
   } else {
-    if ((rc = enqueue_verify(*h, *b, cfg, s, pdl))) return rc;
+    if ((rc = enqueue_verify(*h, *b, cfg, s, pdl, with_draft))) return rc;
   }
   const size_t khd = hd * cfg->k;
+  if (out->draft)
+    SF_CHECK_CUDA(cudaMemcpyAsync(out->draft, b->draft, hd * 4, cudaMemcpyDeviceToDevice, s));
   if (out->reconstructed)
     SF_CHECK_CUDA(cudaMemcpyAsync(out->reconstructed, b->recon, khd * 4, cudaMemcpyDeviceToDevice, s));
   if (out->distances)
@@ -887,6 +996,33 @@ extern "C" int sf_ae_verify(void* handle, int n_envs, const sf_verify_cfg_t* cfg
                                 cudaMemcpyDeviceToDevice, s));
   SF_CHECK_CUDA(cudaMemcpyAsync(out->result, b->result, (size_t)n_envs * SF_RESULT_WORDS * 4,
                                 cudaMemcpyDeviceToDevice, s));
+  return SF_OK;
+}
+
+extern "C" int sf_ae_verify(void* handle, int n_envs, const sf_verify_cfg_t* cfg, const float* draft,
+                            const float* eps, const float* state, const float* signs,
+                            const sf_verify_out_t* out, int flags, void* stream) {
+  return verify_common(static_cast<Handle*>(handle), n_envs, cfg, draft, false, eps, state, signs,
+                       out, flags, (cudaStream_t)stream);
+}
+
+extern "C" int sf_ae_flash_round(void* handle, int n_envs, const sf_verify_cfg_t* cfg,
+                                 const float* obs, const float* eps, const float* state,
+                                 const float* signs, const sf_verify_out_t* out, int flags,
+                                 void* stream) {
+  return verify_common(static_cast<Handle*>(handle), n_envs, cfg, obs, true, eps, state, signs,
+                       out, flags, (cudaStream_t)stream);
+}
+
+extern "C" int sf_ae_time_op(void* handle, int n_envs, int k, int op, int iters, void* stream) {
+  auto* h = static_cast<Handle*>(handle);
+  SF_REQUIRE(h && h->k_prefix, "no expert / prefix");
+  int rc = 0;
+  Buffers* b = get_buffers(*h, n_envs, k, 0, &rc);
+  if (!b) return rc;
+  SF_REQUIRE(op >= 0 && op < (int)b->ops.size(), "op index out of range");
+  for (int i = 0; i < iters; ++i)
+    if ((rc = sf::gemm::launch(b->ops[op], (cudaStream_t)stream, false))) return rc;
   return SF_OK;
 }
 
@@ -900,7 +1036,7 @@ extern "C" int sf_ae_denoise(void* handle, int n_envs, int num_steps, const floa
   SF_REQUIRE(num_steps >= 1 && num_steps <= 64, "num_steps must be in [1, 64]");
   cudaStream_t s = (cudaStream_t)stream;
   int rc = 0;
-  Buffers* b = get_buffers(*h, n_envs, 1, &rc);
+  Buffers* b = get_buffers(*h, n_envs, 1, 1, &rc);
   if (!b) return rc;
   const sf_ae_config_t& c = h->cfg;
   if (h->temb_euler_n != num_steps) {
@@ -920,22 +1056,18 @@ extern "C" int sf_ae_denoise(void* handle, int n_envs, int num_steps, const floa
   SF_CHECK_CUDA(cudaMemcpyAsync(b->draft, start, hd * 4, cudaMemcpyDeviceToDevice, s));
   SF_CHECK_CUDA(cudaMemcpyAsync(b->state, state, (size_t)n_envs * c.state_dim * 4,
                                 cudaMemcpyDeviceToDevice, s));
-  std::vector<int> init(2 * n_envs);
-  for (int e = 0; e < n_envs; ++e) {
-    init[2 * e] = -1;
-    init[2 * e + 1] = 0;
-  }
-  SF_CHECK_CUDA(cudaMemcpyAsync(b->status, init.data(), init.size() * 4, cudaMemcpyHostToDevice, s));
-  SF_CHECK_CUDA(cudaStreamSynchronize(s));
   const bool pdl = (flags & SF_AE_PDL) != 0;
   if (flags & SF_AE_GRAPH) {
     const int key = 0x40000000 | (num_steps << 1) | (pdl ? 1 : 0);
     if (!b->graph || b->graph_key != key) {
-      rc = capture(*h, &b->graph, [&](cudaStream_t cs) { return enqueue_denoise(*h, *b, num_steps, cs, pdl); });
+      rc = capture(*h, &b->graph, &b->graph_kernels, [&](cudaStream_t cs) {
+        return enqueue_denoise(*h, *b, num_steps, cs, pdl);
+      });
       if (rc) return rc;
       b->graph_key = key;
     }
     SF_CHECK_CUDA(cudaGraphLaunch(b->graph, s));
+    sf::count_launch(b->graph_kernels);
   } else {
     if ((rc = enqueue_denoise(*h, *b, num_steps, s, pdl))) return rc;
   }
@@ -953,7 +1085,7 @@ extern "C" int sf_ae_velocity(void* handle, int n_envs, int rows, const float* x
   SF_REQUIRE(rows >= 1 && rows <= SF_MAX_K, "rows must be in [1, %d]", SF_MAX_K);
   cudaStream_t s = (cudaStream_t)stream;
   int rc = 0;
-  Buffers* b = get_buffers(*h, n_envs, rows, &rc);
+  Buffers* b = get_buffers(*h, n_envs, rows, 2, &rc);
   if (!b) return rc;
   sf_verify_cfg_t c{};
   c.k = rows;
