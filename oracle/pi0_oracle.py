@@ -54,6 +54,8 @@ class AEConfig:
     eps: float = 1e-6
     temb_min_period: float = 4e-3
     temb_max_period: float = 4.0
+    draft_in: int = 64
+    draft_hidden: int = 1024
 
     @property
     def seg_len(self) -> int:
@@ -183,7 +185,28 @@ def hash_uniform(seed: int, tid: int, shape, std: float) -> np.ndarray:
 
 # tensor ids for hash_uniform (device init uses the same table)
 TID_A_W, TID_S_W, TID_T1_W, TID_T2_W, TID_OUT_W = 1, 2, 3, 4, 5
+TID_DRAFT_BASE = 20   # + {0, 1, 2}: draft MLP layers
 TID_LAYER_BASE = 100  # + 4 * layer + {0: qkv, 1: o, 2: gu, 3: down}
+
+
+def make_draft_weights(cfg: AEConfig, seed: int = 0):
+    """tanh MLP draft [draft_in -> hid -> hid -> H*D], bf16 weights with std
+    sqrt(1/fan_in), zero fp32 biases (draft.py:29-61 at pi0 scale)."""
+    hid, hd = cfg.draft_hidden, cfg.horizon * cfg.action_dim
+    shapes = ((hid, cfg.draft_in), (hid, hid), (hd, hid))
+    ws = [bf16(hash_uniform(seed, TID_DRAFT_BASE + i, s, float(np.sqrt(1.0 / s[1]))))
+          for i, s in enumerate(shapes)]
+    return ws, [np.zeros(s[0], np.float32) for s in shapes]
+
+
+def draft_forward(cfg: AEConfig, dw, obs):
+    """propose(): bf16 operands, fp32 accumulation, bf16 hidden activations."""
+    ws, bs = dw
+    a = bf16(obs)
+    for i, (w, b) in enumerate(zip(ws, bs)):
+        z = _mm(a, w) + b
+        a = bf16(np.tanh(z)) if i < 2 else z.astype(np.float32)
+    return a.reshape(-1, cfg.horizon, cfg.action_dim)
 TID_KV_BASE = 10000   # + 2 * (env * layers + layer) + {0: K, 1: V^T}
 
 

@@ -857,6 +857,10 @@ extern "C" int sf_ae_create(const sf_ae_config_t* cfg, const sf_ae_weights_t* w,
   SF_REQUIRE(cfg->action_dim >= 2 && cfg->action_dim <= 64, "action_dim must be in [2, 64]");
   SF_REQUIRE(cfg->state_dim >= 1 && cfg->state_dim <= 64, "state_dim must be in [1, 64]");
   SF_REQUIRE(cfg->horizon >= 1 && cfg->prefix_len >= 1, "bad horizon / prefix");
+  SF_REQUIRE(cfg->draft_in == 0 || (cfg->draft_in % 64 == 0 && cfg->draft_hidden >= 64 &&
+                                    cfg->draft_hidden % 64 == 0 && w->draft_w[0] &&
+                                    w->draft_w[1] && w->draft_w[2]),
+             "draft dims must be multiples of 64 with all three layers given");
   auto* h = new Handle();
   h->cfg = *cfg;
   h->w = *w;

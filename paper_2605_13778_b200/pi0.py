@@ -32,6 +32,7 @@ from .actions import ChannelLayout
 
 SF_AE_GRAPH, SF_AE_PDL = 1, 2
 TID_A_W, TID_S_W, TID_T1_W, TID_T2_W, TID_OUT_W = 1, 2, 3, 4, 5
+TID_DRAFT_BASE = 20
 TID_LAYER_BASE = 100
 TID_KV_BASE = 10000
 
@@ -51,6 +52,8 @@ class AEConfig:
     eps: float = 1e-6
     temb_min_period: float = 4e-3
     temb_max_period: float = 4.0
+    draft_in: int = 64       # draft MLP observation features (0 disables the draft)
+    draft_hidden: int = 1024
 
     @property
     def seg_len(self) -> int:
@@ -80,7 +83,8 @@ class _AeConfigC(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in ("width", "layers", "q_heads", "head_dim", "mlp",
                                             "action_dim", "state_dim", "horizon", "prefix_len")] + \
                [("eps", ctypes.c_float), ("temb_min_period", ctypes.c_float),
-                ("temb_max_period", ctypes.c_float)]
+                ("temb_max_period", ctypes.c_float), ("draft_in", ctypes.c_int),
+                ("draft_hidden", ctypes.c_int)]
 
 
 _MAXL = 32
@@ -91,7 +95,8 @@ class _AeWeightsC(ctypes.Structure):
                                                "t2_b", "out_w", "out_b")] + \
                [("qkv", ctypes.c_void_p * _MAXL), ("o", ctypes.c_void_p * _MAXL),
                 ("gu", ctypes.c_void_p * _MAXL), ("down", ctypes.c_void_p * _MAXL),
-                ("rope", ctypes.c_void_p)]
+                ("rope", ctypes.c_void_p), ("draft_w", ctypes.c_void_p * 3),
+                ("draft_b", ctypes.c_void_p * 3)]
 
 
 def _fill(t: torch.Tensor, seed: int, tid: int, std: float) -> torch.Tensor:
@@ -186,9 +191,16 @@ class ActionExpert:
         rope = torch.from_numpy(rope_table(cfg, cfg.prefix_len + cfg.seg_len)).to(dev)
         self._keep.append(rope)
         w.rope = rope.data_ptr()
+        if cfg.draft_in > 0:
+            # tanh MLP draft [draft_in -> hid -> hid -> H*D] (draft.py:29-61 at pi0 scale)
+            hid, hdd = cfg.draft_hidden, cfg.horizon * cfg.action_dim
+            shapes = ((hid, cfg.draft_in), (hid, hid), (hdd, hid))
+            for i, shp in enumerate(shapes):
+                w.draft_w[i] = mk(shp, b16, TID_DRAFT_BASE + i, float(np.sqrt(1.0 / shp[1]))).data_ptr()
+                w.draft_b[i] = zeros(shp[0]).data_ptr()
         c = _AeConfigC(cfg.width, cfg.layers, cfg.q_heads, cfg.head_dim, cfg.mlp, cfg.action_dim,
                        cfg.state_dim, cfg.horizon, cfg.prefix_len, cfg.eps, cfg.temb_min_period,
-                       cfg.temb_max_period)
+                       cfg.temb_max_period, cfg.draft_in, cfg.draft_hidden)
         self._cfg_c, self._w_c = c, w
         h = ctypes.c_void_p()
         _capi.check(_capi.lib().sf_ae_create(ctypes.byref(c), ctypes.byref(w), ctypes.byref(h)),
@@ -250,6 +262,39 @@ class ActionExpert:
             signs.data_ptr() if signs is not None else None, ctypes.byref(out), self.flags, s),
             "ae verify")
         return outputs
+
+    def flash_batch(self, cfg, obs: torch.Tensor, eps: torch.Tensor, state: torch.Tensor,
+                    signs: torch.Tensor | None = None, current_sign: float = -1.0,
+                    phase_fallback=True, prefix_cap=True, replan_size=12, outputs=None,
+                    stream=None):
+        """Speculative round for B envs in one graph: draft MLP on obs [B, F]
+        -> verify -> gate/decision. Returns (draft, recon, dist, branch, result)."""
+        from .verifier import make_cfg
+
+        B = obs.shape[0]
+        K = len(cfg.timesteps)
+        dev = obs.device
+        if outputs is None:
+            outputs = (torch.empty((B, self.horizon, self.dim), dtype=torch.float32, device=dev),
+                       torch.empty((B, K, self.horizon, self.dim), dtype=torch.float32, device=dev),
+                       torch.empty((B, K, self.horizon), dtype=torch.float32, device=dev),
+                       torch.empty((B, K), dtype=torch.int32, device=dev),
+                       torch.empty((B, _capi.SF_RESULT_WORDS), dtype=torch.int32, device=dev))
+        draft, recon, dist, branch, result = outputs
+        c = make_cfg(cfg, current_sign, phase_fallback, prefix_cap, replan_size)
+        out = _capi.SfVerifyOut(draft.data_ptr(), recon.data_ptr() if recon is not None else None,
+                                dist.data_ptr() if dist is not None else None, branch.data_ptr(),
+                                result.data_ptr())
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _capi.check(_capi.lib().sf_ae_flash_round(
+            self._h, B, ctypes.byref(c), obs.data_ptr(), eps.data_ptr(), state.data_ptr(),
+            signs.data_ptr() if signs is not None else None, ctypes.byref(out), self.flags, s),
+            "ae flash round")
+        return outputs
+
+    def time_op(self, n_envs: int, k: int, op: int, iters: int, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _capi.check(_capi.lib().sf_ae_time_op(self._h, n_envs, k, op, iters, s), "time op")
 
     def denoise_batch(self, start: torch.Tensor, state: torch.Tensor, n_steps: int,
                       chunk: torch.Tensor | None = None, status: torch.Tensor | None = None,

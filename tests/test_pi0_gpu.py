@@ -113,6 +113,31 @@ def test_verify_matches_oracle_small(n_envs, k):
     assert flips <= max(1, n_envs // 3)
 
 
+@pytest.mark.parametrize("n_envs", [1, 300])
+def test_flash_round_draft_matches_oracle(n_envs):
+    """propose (draft MLP) fused into the verify graph: draft vs oracle, and the
+    round's verify outputs equal a verify of that draft."""
+    import torch
+
+    from oracle import pi0_oracle as po
+    from paper_2605_13778_b200 import pi0
+    from paper_2605_13778_b200.verifier import VerifierConfig
+
+    ocfg, dcfg = _pair(layers=1, prefix_len=64)
+    ae = pi0.ActionExpert(dcfg, seed=0, n_envs=n_envs, kv_seed=1)
+    rng = np.random.default_rng(n_envs)
+    obs = rng.standard_normal((n_envs, dcfg.draft_in)).astype(np.float32)
+    eps = rng.standard_normal((n_envs, dcfg.horizon, dcfg.action_dim)).astype(np.float32)
+    state = rng.standard_normal((n_envs, dcfg.state_dim)).astype(np.float32)
+    cfg = VerifierConfig(timesteps=(0.25, 0.5, 0.75), delta=1.0)
+    t = lambda a: torch.from_numpy(a).cuda()
+    draft, recon, dist, branch, result = [x.clone() for x in ae.flash_batch(cfg, t(obs), t(eps), t(state))]
+    want = po.draft_forward(ocfg, po.make_draft_weights(ocfg, 0), obs)
+    np.testing.assert_allclose(draft.cpu().numpy(), want, rtol=1e-2, atol=1e-2 * np.abs(want).max())
+    r2, d2, b2, res2 = ae.verify_batch(cfg, draft, t(eps), t(state))
+    assert torch.equal(r2, recon) and torch.equal(b2, branch) and torch.equal(res2, result)
+
+
 def test_denoise_matches_oracle_small():
     import torch
 
