@@ -47,7 +47,7 @@ struct Params {
   int segs;         // branches per env (K)
   int prefix_len;   // P
   int n_prefix_blocks;
-  int n_blocks;     // n_prefix_blocks + 2
+  int n_blocks;     // n_prefix_blocks + suffix blocks
   int blocks_per_split;
   int splits;
   int tiles;
@@ -99,7 +99,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int env = m0 / p.env_rows;
   const int env_start = env * p.env_rows;
   const int seg_first = (m0 - env_start) / p.seg_len;
-  const int sb = env_start + seg_first * p.seg_len;  // first suffix key token
+  // first suffix key token, rounded down to a 64-key boundary so every TMA box
+  // of the transposed V starts on an aligned inner coordinate (3 blocks then
+  // cover the <= 2 segments of 1 + H tokens the tile can touch)
+  const int sb = (env_start + seg_first * p.seg_len) & ~(BKEY - 1);
   const int j0 = split * p.blocks_per_split;
   const int nb = min(p.blocks_per_split, p.n_blocks - j0);
 
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           const int kt = sb + (j - p.n_prefix_blocks) * BKEY + c - env_start;
           const int seg_k = kt / p.seg_len;
-          valid = real_q && kt < p.segs * p.seg_len && seg_k == seg_q &&
+          valid = real_q && kt >= 0 && kt < p.segs * p.seg_len && seg_k == seg_q &&
                   (t_q >= 1 || kt - seg_k * p.seg_len == 0);
         }
         const float x = __uint_as_float(raw[c >> 4][c & 15]) * p.scale_log2;

@@ -495,7 +495,9 @@ int build(Handle& h, Buffers& b, int B, int K) {
   if (ws) ALLOC(b.ws, ws / sizeof(float));
   // attention split-KV workspace
   const int n_prefix_blocks = (c.prefix_len + attn::BKEY - 1) / attn::BKEY;
-  const int n_blocks = n_prefix_blocks + 2;
+  // suffix keys of the (<= 2) segments a 16-token tile touches, from a
+  // 64-aligned start: span <= 63 + 2 * T
+  const int n_blocks = n_prefix_blocks + (63 + 2 * T + attn::BKEY - 1) / attn::BKEY;
   b.attn_tiles = b.M / 16;
   int asplit = 148 / b.attn_tiles;
   if (asplit < 1) asplit = 1;
