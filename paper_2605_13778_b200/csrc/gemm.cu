@@ -1,5 +1,6 @@
-// Host side of the tcgen05 GEMM: tensor maps, split-K planning, PDL launch,
-// and a debug C entry point used by the GEMM unit tests.
+// Host side of the tcgen05 GEMMs: tensor maps, planning (swap-AB + cluster
+// split-K for batch-1 shapes, persistent tiles for batched shapes), PDL /
+// cluster launch, and a debug C entry point used by the GEMM unit tests.
 
 #include <cudaTypedefs.h>
 #include <stdio.h>
@@ -24,6 +25,40 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
   }
   return fn;
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+using KernelFn = void (*)(CUtensorMap, CUtensorMap, Params);
+
+template <int KIND>
+KernelFn swap_fn() {
+  return gemm_swap_kernel<KIND>;
+}
+template <int KIND>
+KernelFn persistent_fn() {
+  return gemm_persistent_kernel<KIND>;
+}
+
+KernelFn pick(int kind, bool swap) {
+  switch (kind) {
+    case EPI_F32: return swap ? swap_fn<EPI_F32>() : persistent_fn<EPI_F32>();
+    case EPI_BF16: return swap ? swap_fn<EPI_BF16>() : persistent_fn<EPI_BF16>();
+    case EPI_QKV: return swap ? swap_fn<EPI_QKV>() : persistent_fn<EPI_QKV>();
+    case EPI_RESID: return swap ? swap_fn<EPI_RESID>() : persistent_fn<EPI_RESID>();
+    case EPI_GEGLU: return swap ? swap_fn<EPI_GEGLU>() : persistent_fn<EPI_GEGLU>();
+    case EPI_TANH_BF16: return swap ? swap_fn<EPI_TANH_BF16>() : persistent_fn<EPI_TANH_BF16>();
+  }
+  return nullptr;
 }
 }  // namespace
 
@@ -50,18 +85,20 @@ int make_map(CUtensorMap* m, const void* ptr, int rows, int K, int ld, int box_r
   return SF_OK;
 }
 
-size_t ws_bytes_needed(int rows_a, int rows_b, int K, int bn, int splits) {
-  const int tiles = ((rows_a + BM - 1) / BM) * ((rows_b + bn - 1) / bn);
-  (void)K;
-  return splits > 1 ? (size_t)splits * tiles * bn * BM * sizeof(float) : 0;
+int auto_splits(int tiles, int num_kb) {
+  int s = num_sms() / (tiles > 0 ? tiles : 1);
+  if (s > kMaxSplits) s = kMaxSplits;
+  if (s > num_kb) s = num_kb;
+  return s < 1 ? 1 : s;
 }
 
 int plan(Op* op, const void* A, int rows_a, int lda, const void* B, int rows_b, int ldb, int K,
-         int bn, int splits, int swap_ab, const EpiArgs& e, float* ws, size_t ws_bytes,
-         int* counters, int n_counters, int max_stages) {
+         int bn, int splits, int swap_ab, const EpiArgs& e, int max_stages) {
   SF_REQUIRE(bn >= 16 && bn <= 256 && bn % 16 == 0, "bn must be a multiple of 16 in [16, 256]");
   SF_REQUIRE(K % BK == 0, "K (%d) must be a multiple of %d", K, BK);
+  SF_REQUIRE(e.kind >= 0 && e.kind < EPI_KINDS, "bad epilogue kind");
   SF_REQUIRE(e.kind != EPI_RESID || swap_ab || bn % 128 == 0, "residual epilogue needs bn %% 128 == 0");
+  SF_REQUIRE(swap_ab || rows_a > 0, "empty GEMM");
   Params& p = op->p;
   p = Params{};
   p.rows_a = rows_a;
@@ -72,55 +109,75 @@ int plan(Op* op, const void* A, int rows_a, int lda, const void* B, int rows_b, 
   p.swap_ab = swap_ab;
   p.tiles_a = (rows_a + BM - 1) / BM;
   p.tiles_b = (rows_b + bn - 1) / bn;
-  const int tiles = p.tiles_a * p.tiles_b;
-  if (splits <= 0) {
-    // cover the 148 SMs with weight streams: split K until tiles*splits >= ~148
-    splits = (148 + tiles - 1) / tiles;
-  }
+  p.total_tiles = p.tiles_a * p.tiles_b;
+  if (!swap_ab) splits = 1;  // the persistent kernel walks whole-K tiles
+  if (splits <= 0) splits = auto_splits(p.total_tiles, p.num_kb);
   splits = splits < 1 ? 1 : (splits > p.num_kb ? p.num_kb : splits);
+  SF_REQUIRE(splits <= kMaxSplits, "at most %d K splits", kMaxSplits);
   p.kb_per_split = (p.num_kb + splits - 1) / splits;
   p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;  // every split gets >= 1 block
-  if (p.splits > 1) {
-    SF_REQUIRE(ws && counters, "split-K needs a workspace");
-    SF_REQUIRE(ws_bytes >= ws_bytes_needed(rows_a, rows_b, K, bn, p.splits),
-               "split-K workspace too small");
-    SF_REQUIRE(n_counters >= tiles, "split-K counters too small");
-  }
-  p.ws = ws;
-  p.counters = counters;
   p.e = e;
   const uint32_t stage_bytes = kAStageBytes + ((bn * BK * 2 + 1023) & ~1023);
-  const size_t scratch = 64 + 256 * 4 + 4 * 256 * 4 + 1024 /* align slack */;
-  int stages = (int)((227 * 1024 - scratch) / stage_bytes);
+  const size_t budget = 227 * 1024 - kTailBytes - 1024;
+  int stages = (int)(budget / stage_bytes);
   if (stages > max_stages) stages = max_stages;
-  if (stages > p.kb_per_split) stages = p.kb_per_split < 2 ? 2 : p.kb_per_split;
+  if (stages > 16) stages = 16;
+  const int per_cta_kb = swap_ab ? p.kb_per_split : p.num_kb;
+  if (swap_ab && stages > per_cta_kb) stages = per_cta_kb < 2 ? 2 : per_cta_kb;
   SF_REQUIRE(stages >= 2, "GEMM tile does not fit in shared memory");
   p.stages = stages;
-  op->smem = (size_t)stages * stage_bytes + 8 * (2 * stages + 1) + 16 + 256 * 4 + 4 * 256 * 4 + 1024;
-  op->grid = dim3(p.tiles_a, p.tiles_b, p.splits);
+  size_t region = (size_t)stages * stage_bytes;
+  if (p.splits > 1) {
+    const size_t staging = (size_t)BM * bn * 4;  // fp32 partial [bn][128]
+    if (staging > region) region = staging;
+  }
+  region = (region + 1023) & ~size_t(1023);
+  SF_REQUIRE(region + kTailBytes + 1024 <= 227 * 1024, "GEMM shared memory over budget");
+  p.smem_stage_region = (uint32_t)region;
+  op->smem = region + kTailBytes + 1024;
+  if (swap_ab) {
+    op->grid = dim3(p.tiles_a, p.tiles_b, p.splits);
+    op->cluster = p.splits;
+  } else {
+    const int ctas = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
+    op->grid = dim3(ctas, 1, 1);
+    op->cluster = 1;
+  }
+  op->fn = reinterpret_cast<void*>(pick(e.kind, swap_ab));
   int rc = make_map(&op->ta, A, rows_a, K, lda, BM);
   if (rc) return rc;
   return make_map(&op->tb, B, rows_b, K, ldb, bn);
 }
 
 int launch(const Op& op, cudaStream_t stream, bool pdl) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    SF_CHECK_CUDA(cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       227 * 1024));
-    attr_set = true;
+  static bool attr_done[2 * EPI_KINDS] = {};
+  const int slot = op.p.e.kind * 2 + (op.p.swap_ab ? 1 : 0);
+  KernelFn fn = reinterpret_cast<KernelFn>(op.fn);
+  if (!attr_done[slot]) {
+    SF_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    SF_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr_done[slot] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = op.grid;
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = op.smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[na].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  ++na;
+  if (op.cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 1;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = op.cluster;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel, op.ta, op.tb, op.p));
+  cfg.numAttrs = na;
+  SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, fn, op.ta, op.tb, op.p));
   count_launch();
   return SF_OK;
 }
@@ -129,8 +186,7 @@ int launch(const Op& op, cudaStream_t stream, bool pdl) {
 }  // namespace sf
 
 // Debug entry: D = A @ B^T with an F32 / BF16 epilogue (optional RMS row
-// scale from ssq partials). Allocates its own split-K workspace; not for the
-// hot path.
+// scale from ssq partials). Synchronises `stream`; not for the hot path.
 extern "C" int sf_dbg_gemm(const void* A, int rows_a, const void* B, int rows_b, int K, int bn,
                            int splits, int swap_ab, int epi_kind, void* out, int ld_out,
                            int M_valid, int N_valid, const float* ssq, int ssq_groups, int ssq_ld,
@@ -150,20 +206,9 @@ extern "C" int sf_dbg_gemm(const void* A, int rows_a, const void* B, int rows_b,
   e.ssq_ld = ssq_ld;
   e.inv_width = inv_width;
   e.eps = 1e-6f;
-  const int tiles = ((rows_a + BM - 1) / BM) * ((rows_b + bn - 1) / bn);
-  const int max_splits = K / BK;
-  const size_t wsb = ws_bytes_needed(rows_a, rows_b, K, bn, splits > 0 ? splits : max_splits);
-  float* ws = nullptr;
-  int* counters = nullptr;
-  if (wsb) SF_CHECK_CUDA(cudaMalloc(&ws, wsb));
-  SF_CHECK_CUDA(cudaMalloc(&counters, sizeof(int) * (tiles + 1)));
-  SF_CHECK_CUDA(cudaMemsetAsync(counters, 0, sizeof(int) * (tiles + 1), (cudaStream_t)stream));
   Op op;
-  int rc = plan(&op, A, rows_a, K, B, rows_b, K, K, bn, splits, swap_ab, e, ws, wsb, counters,
-                tiles + 1);
+  int rc = plan(&op, A, rows_a, K, B, rows_b, K, K, bn, splits, swap_ab, e);
   if (!rc) rc = launch(op, (cudaStream_t)stream, false);
-  cudaStreamSynchronize((cudaStream_t)stream);
-  if (ws) cudaFree(ws);
-  cudaFree(counters);
+  SF_CHECK_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   return rc;
 }

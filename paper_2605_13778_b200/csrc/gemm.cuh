@@ -1,34 +1,43 @@
 // tcgen05 GEMM for the pi0-scale Action Expert (sm_100a).
 //
-//   D[a, b] = sum_k A[a, k] * B[b, k]      (A, B bf16 K-major; fp32 accumulation in TMEM)
+//   D[a, b] = sum_k A[a, k] * B[b, k]   (A, B bf16 K-major; fp32 accumulation in TMEM)
 //
-// One CTA computes a 128 x BN tile (UMMA M=128, N=BN<=256, K=16 per
-// instruction) over a K range; warp 0 is the TMA producer (SWIZZLE_128B tiles
-// 64 elements deep into a `stages`-deep mbarrier ring), warp 1 allocates TMEM
-// and issues tcgen05.mma from one elected lane, warps 2-5 are the epilogue
-// (tcgen05.ld 32x32b -> registers -> fused op -> global).
+// Warp roles (320 threads): warp 0 = TMA producer (SWIZZLE_128B 64-deep
+// K tiles into a `stages`-deep mbarrier ring), warp 1 = TMEM allocator + MMA
+// issuer (one elected lane, UMMA 128 x BN x 16), warps 2-9 = epilogue
+// (tcgen05.ld 32x32b; two warps per TMEM lane quarter split the columns).
+// Epilogues are compile-time specialised per fused op (RMS scale + RoPE,
+// residual + RMS partials, GeGLU, tanh, plain store) with vectorised stores.
 //
-// Two orientations share the kernel:
-//  * swap-AB (batch-1 rounds, 51..416 token rows): A = weights, so the 128
-//    TMEM lanes are output features and the BN columns are token rows. Weight
-//    tiles fill the M=128 slot; split-K spreads the weight stream over all
-//    148 SMs; partials are reduced deterministically by the last-arriving CTA
-//    of each tile (fixed split order), which then runs the fused epilogue.
-//  * normal (batched envs): A = token rows, B = weights, BN = 256 features.
+// Two kernels:
+//  * gemm_swap_kernel (batch-1 shapes, <= 256 token rows): A = weights, so the
+//    128 TMEM lanes are output features and BN columns are token rows; split-K
+//    spreads the weight stream over up to 148 SMs. The S split CTAs of a tile
+//    form a thread-block cluster: each stages its fp32 partial in SMEM, then
+//    every CTA reduces 1/S of the columns over DSMEM in a fixed split order
+//    (deterministic) and runs the fused epilogue on them. No global workspace,
+//    no serial last-CTA reduction.
+//  * gemm_persistent_kernel (batched envs): A = token rows, B = weights,
+//    BN = 256; one CTA per SM walks tiles (features fastest, so a row tile's
+//    activations are shared through L2); two TMEM accumulators (512 columns)
+//    let the epilogue of tile i overlap the MMAs of tile i+1.
 // PDL: weight tiles do not depend on the previous kernel, so the producer
-// issues them BEFORE griddepcontrol.wait; only activation tiles wait.
+// issues them BEFORE griddepcontrol.wait; activation tiles wait.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "sm100.cuh"
 #include "gemm_types.h"
+#include "sm100.cuh"
 
 namespace sf {
 namespace gemm {
+
+namespace cg = cooperative_groups;
 
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
@@ -42,273 +51,517 @@ __device__ __forceinline__ float row_scale(const EpiArgs& e, int m) {
   return rsqrtf(s * e.inv_width + e.eps);
 }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+}
 
-// Apply the fused op to one 16-column chunk held by this thread.
-// swap: lane_row = feature, columns = tokens; else lane_row = token, columns = features.
-__device__ __forceinline__ void apply_chunk(const Params& p, float (&v)[16], int lane_row, int c0,
-                                            const float* rs_cols, float rs_row, float* red_q,
-                                            float& ssq_acc) {
-  const EpiArgs& e = p.e;
-  const bool swap = p.swap_ab;
-  const int tile_a = blockIdx.x, tile_b = blockIdx.y;
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// ------------------------------------------------------------- epilogues
+//
+// SWAP: thread = feature n (fixed), columns = tokens m0 + j.
+template <int KIND>
+__device__ __forceinline__ void epi_swap(const EpiArgs& e, int n, int m0, const float (&v)[16],
+                                         const float* rs, float* red_q, int c0) {
+  const bool nvalid = n < e.N;
+  if (KIND == EPI_F32 || KIND == EPI_BF16 || KIND == EPI_TANH_BF16) {
+    const float b = (e.bias && nvalid) ? e.bias[n] : 0.f;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int m = swap ? tile_b * p.bn + c0 + j : tile_a * BM + lane_row;
-    const float r = swap ? rs_cols[c0 + j] : rs_row;
-    if (e.kind != EPI_RESID) v[j] *= r;
-  }
-  switch (e.kind) {
-    case EPI_F32:
-    case EPI_BF16:
-    case EPI_TANH_BF16: {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int m = swap ? tile_b * p.bn + c0 + j : tile_a * BM + lane_row;
-        const int n = swap ? tile_a * BM + lane_row : tile_b * p.bn + c0 + j;
-        if (m < e.M && n < e.N) {
-          float o = e.bias ? v[j] + e.bias[n] : v[j];
-          if (e.kind == EPI_TANH_BF16) o = tanhf(o);
-          if (e.kind == EPI_F32) e.out_f32[(size_t)m * e.ld_f32 + n] = o;
-          else e.out_bf16[(size_t)m * e.ld_bf16 + n] = __float2bfloat16_rn(o);
-        }
+    for (int j = 0; j < 16; ++j) {
+      const int m = m0 + j;
+      if (nvalid && m < e.M) {
+        float o = v[j] * rs[c0 + j] + b;
+        if (KIND == EPI_TANH_BF16) o = tanhf(o);
+        if (KIND == EPI_F32) e.out_f32[(size_t)m * e.ld_f32 + n] = o;
+        else e.out_bf16[(size_t)m * e.ld_bf16 + n] = __float2bfloat16_rn(o);
       }
-      break;
     }
-    case EPI_GEGLU:
-    case EPI_QKV: {
+  } else if (KIND == EPI_GEGLU) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float partner = swap ? __shfl_xor_sync(0xffffffffu, v[j], 1) : v[j ^ 1];
-        const int m = swap ? tile_b * p.bn + c0 + j : tile_a * BM + lane_row;
-        const int n = swap ? tile_a * BM + lane_row : tile_b * p.bn + c0 + j;
-        if (m >= e.M || n >= e.N) continue;
-        const int second = n & 1;
-        if (e.kind == EPI_GEGLU) {
-          // device rows interleave (gate_i, up_i) -> h_i = gelu(gate_i) * up_i
-          if (!second)
-            e.out_bf16[(size_t)m * e.ld_bf16 + (n >> 1)] =
-                __float2bfloat16_rn(gelu_tanh(v[j]) * partner);
-        } else if (n < e.q_features + 256) {
-          // rows (2i, 2i+1) = (dim i, dim i+128) of one head: rotate_half RoPE
-          const int local = m % e.env_rows;
-          const int pos = e.pos0 + (local % e.seg_len);
-          const int i = (n & 255) >> 1;
-          const float2 cs = e.rope[pos * 128 + i];
-          const float a = second ? partner : v[j];
-          const float b = second ? v[j] : partner;
-          const float y = second ? (b * cs.x + a * cs.y) : (a * cs.x - b * cs.y);
-          const int dim = i + (second << 7);
-          if (n < e.q_features)
-            e.q[(size_t)m * e.q_features + (n & ~255) + dim] = __float2bfloat16_rn(y);
-          else
-            e.k[(size_t)m * 256 + dim] = __float2bfloat16_rn(y);
-        } else {
-          const int d = n - e.q_features - 256;
-          e.vt[(size_t)d * e.vt_ld + m] = __float2bfloat16_rn(v[j]);
-        }
-      }
-      break;
+    for (int j = 0; j < 16; ++j) {
+      const float x = v[j] * rs[c0 + j];
+      const float partner = __shfl_xor_sync(0xffffffffu, x, 1);
+      const int m = m0 + j;
+      if (nvalid && m < e.M && !(n & 1))
+        e.out_bf16[(size_t)m * e.ld_bf16 + (n >> 1)] = __float2bfloat16_rn(gelu_tanh(x) * partner);
     }
-    case EPI_RESID: {
+  } else if (KIND == EPI_QKV) {
+    if (n < e.q_features + 256) {
+      const int second = n & 1;
+      const int i = (n & 255) >> 1;
+      const int dim = i + (second << 7);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const int m = swap ? tile_b * p.bn + c0 + j : tile_a * BM + lane_row;
-        const int n = swap ? tile_a * BM + lane_row : tile_b * p.bn + c0 + j;
-        float sq = 0.f;
-        if (m < e.M && n < e.N) {
-          const size_t o = (size_t)m * e.N + n;
-          const float xn = e.x[o] + v[j];
-          e.x[o] = xn;
-          e.xb[o] = __float2bfloat16_rn(xn);
-          sq = xn * xn;
-        }
-        if (swap) {
-          // sum over the 128 features (lanes of 4 warps) of this token column
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
-          if ((threadIdx.x & 31) == 0) red_q[c0 + j] = sq;
-        } else {
-          ssq_acc += sq;
-        }
+        const float x = v[j] * rs[c0 + j];
+        const float partner = __shfl_xor_sync(0xffffffffu, x, 1);
+        const int m = m0 + j;
+        if (!nvalid || m >= e.M) continue;
+        const int pos = e.pos0 + ((m % e.env_rows) % e.seg_len);
+        const float2 cs = e.rope[pos * 128 + i];
+        const float a = second ? partner : x;
+        const float b = second ? x : partner;
+        const float y = second ? (b * cs.x + a * cs.y) : (a * cs.x - b * cs.y);
+        if (n < e.q_features) e.q[(size_t)m * e.q_features + (n & ~255) + dim] = __float2bfloat16_rn(y);
+        else e.k[(size_t)m * 256 + dim] = __float2bfloat16_rn(y);
       }
-      break;
+    } else if (nvalid) {
+      // v^T: 16 consecutive tokens of one feature row -> 32 contiguous bytes
+      const int d = n - e.q_features - 256;
+      uint32_t w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) w[j] = pack_bf16(v[2 * j] * rs[c0 + 2 * j], v[2 * j + 1] * rs[c0 + 2 * j + 1]);
+      uint4* dst = reinterpret_cast<uint4*>(e.vt + (size_t)d * e.vt_ld + m0);
+      dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+  } else if (KIND == EPI_RESID) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int m = m0 + j;
+      float sq = 0.f;
+      if (nvalid && m < e.M) {
+        const size_t o = (size_t)m * e.N + n;
+        const float xn = e.x[o] + v[j];
+        e.x[o] = xn;
+        e.xb[o] = __float2bfloat16_rn(xn);
+        sq = xn * xn;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+      if ((threadIdx.x & 31) == 0) red_q[c0 + j] = sq;
     }
   }
 }
 
+// NORMAL: thread = token m (fixed), columns = features n0 + j (16-aligned).
+template <int KIND>
+__device__ __forceinline__ void epi_normal(const EpiArgs& e, int m, int n0, float (&v)[16], float rs,
+                                           float& ssq_acc) {
+  if (m >= e.M) return;
+  const bool full = n0 + 16 <= e.N;
+  if (KIND == EPI_F32 || KIND == EPI_BF16 || KIND == EPI_TANH_BF16) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float o = v[j] * rs;
+      if (e.bias && n0 + j < e.N) o += e.bias[n0 + j];
+      if (KIND == EPI_TANH_BF16) o = tanhf(o);
+      v[j] = o;
+    }
+    if (KIND == EPI_F32) {
+      float* dst = e.out_f32 + (size_t)m * e.ld_f32 + n0;
+      if (full && (e.ld_f32 % 4) == 0) {
+#pragma unroll
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      } else {
+        for (int j = 0; j < 16; ++j)
+          if (n0 + j < e.N) dst[j] = v[j];
+      }
+    } else {
+      __nv_bfloat16* dst = e.out_bf16 + (size_t)m * e.ld_bf16 + n0;
+      if (full && (e.ld_bf16 % 8) == 0) {
+        uint32_t w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      } else {
+        for (int j = 0; j < 16; ++j)
+          if (n0 + j < e.N) dst[j] = __float2bfloat16_rn(v[j]);
+      }
+    }
+  } else if (KIND == EPI_GEGLU) {
+    uint32_t w[4];
+#pragma unroll
+    for (int p = 0; p < 8; p += 2) {
+      const float h0 = gelu_tanh(v[2 * p] * rs) * (v[2 * p + 1] * rs);
+      const float h1 = gelu_tanh(v[2 * p + 2] * rs) * (v[2 * p + 3] * rs);
+      w[p >> 1] = pack_bf16(h0, h1);
+    }
+    // 8 outputs h[n0/2 .. n0/2 + 7]
+    *reinterpret_cast<uint4*>(e.out_bf16 + (size_t)m * e.ld_bf16 + (n0 >> 1)) =
+        make_uint4(w[0], w[1], w[2], w[3]);
+  } else if (KIND == EPI_QKV) {
+    if (n0 < e.q_features + 256) {
+      const int pos = e.pos0 + ((m % e.env_rows) % e.seg_len);
+      const int i0 = (n0 & 255) >> 1;
+      uint32_t wa[4], wb[4];
+#pragma unroll
+      for (int p = 0; p < 8; p += 2) {
+        float ya[2], yb[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const float a = v[2 * (p + u)] * rs, b = v[2 * (p + u) + 1] * rs;
+          const float2 cs = e.rope[pos * 128 + i0 + p + u];
+          ya[u] = a * cs.x - b * cs.y;
+          yb[u] = b * cs.x + a * cs.y;
+        }
+        wa[p >> 1] = pack_bf16(ya[0], ya[1]);
+        wb[p >> 1] = pack_bf16(yb[0], yb[1]);
+      }
+      __nv_bfloat16* base = n0 < e.q_features ? e.q + (size_t)m * e.q_features + (n0 & ~255)
+                                              : e.k + (size_t)m * 256;
+      *reinterpret_cast<uint4*>(base + i0) = make_uint4(wa[0], wa[1], wa[2], wa[3]);
+      *reinterpret_cast<uint4*>(base + 128 + i0) = make_uint4(wb[0], wb[1], wb[2], wb[3]);
+    } else {
+      const int d0 = n0 - e.q_features - 256;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) e.vt[(size_t)(d0 + j) * e.vt_ld + m] = __float2bfloat16_rn(v[j] * rs);
+    }
+  } else if (KIND == EPI_RESID) {
+    float* xr = e.x + (size_t)m * e.N + n0;
+    __nv_bfloat16* xbr = e.xb + (size_t)m * e.N + n0;
+    uint32_t w[8];
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) {
+      float4 x4 = *reinterpret_cast<float4*>(xr + j);
+      x4.x += v[j];
+      x4.y += v[j + 1];
+      x4.z += v[j + 2];
+      x4.w += v[j + 3];
+      *reinterpret_cast<float4*>(xr + j) = x4;
+      ssq_acc += x4.x * x4.x + x4.y * x4.y + x4.z * x4.z + x4.w * x4.w;
+      w[j / 2] = pack_bf16(x4.x, x4.y);
+      w[j / 2 + 1] = pack_bf16(x4.z, x4.w);
+    }
+    reinterpret_cast<uint4*>(xbr)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    reinterpret_cast<uint4*>(xbr)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+}
+
+// ------------------------------------------------------ shared mainloop parts
+
+struct Ring {
+  uint8_t* smem;
+  uint64_t* full;
+  uint64_t* empty;
+  uint32_t stage_bytes, b_bytes;
+  int stages;
+};
+
+// Producer for one tile's K range; `kiter` continues the ring across tiles.
+__device__ __forceinline__ void produce_tile(const Ring& r, const CUtensorMap* tw,
+                                             const CUtensorMap* tx, uint32_t w_off, uint32_t x_off,
+                                             int w_row, int x_row, int kb0, int nkb, int& kiter,
+                                             bool first_tile, uint64_t pol_w, uint64_t pol_x) {
+  int i = 0;
+  if (first_tile) {
+    // weights first (independent of the previous kernel), then the PDL wait
+    const int pre = min(r.stages, nkb);
+    for (; i < pre; ++i) {
+      const int s = (kiter + i) % r.stages;
+      uint8_t* st = r.smem + s * r.stage_bytes;
+      sm100::mbar_arrive_expect_tx(&r.full[s], kAStageBytes + r.b_bytes);
+      sm100::tma_load_2d(tw, &r.full[s], st + w_off, (kb0 + i) * BK, w_row, pol_w);
+    }
+    sm100::pdl_wait();
+    for (int u = 0; u < pre; ++u) {
+      const int s = (kiter + u) % r.stages;
+      sm100::tma_load_2d(tx, &r.full[s], r.smem + s * r.stage_bytes + x_off, (kb0 + u) * BK, x_row,
+                         pol_x);
+    }
+  }
+  for (; i < nkb; ++i) {
+    const int k = kiter + i;
+    const int s = k % r.stages;
+    if (k >= r.stages) sm100::mbar_wait(&r.empty[s], ((k / r.stages) & 1) ^ 1);
+    uint8_t* st = r.smem + s * r.stage_bytes;
+    sm100::mbar_arrive_expect_tx(&r.full[s], kAStageBytes + r.b_bytes);
+    sm100::tma_load_2d(tw, &r.full[s], st + w_off, (kb0 + i) * BK, w_row, pol_w);
+    sm100::tma_load_2d(tx, &r.full[s], st + x_off, (kb0 + i) * BK, x_row, pol_x);
+  }
+  kiter += nkb;
+}
+
+__device__ __forceinline__ void mma_tile(const Ring& r, uint32_t tmem_d, uint32_t idesc, int nkb,
+                                         int& kiter) {
+  for (int i = 0; i < nkb; ++i) {
+    const int k = kiter + i;
+    const int s = k % r.stages;
+    sm100::mbar_wait(&r.full[s], (k / r.stages) & 1);
+    sm100::tc_fence_after();
+    const uint32_t a_addr = sm100::smem_u32(r.smem + s * r.stage_bytes);
+    const uint32_t b_addr = a_addr + kAStageBytes;
+#pragma unroll
+    for (int kk = 0; kk < BK / 16; ++kk)
+      sm100::umma_bf16(tmem_d, sm100::make_sw128_desc(a_addr + kk * 32),
+                       sm100::make_sw128_desc(b_addr + kk * 32), idesc, (i | kk) != 0);
+    sm100::umma_commit(&r.empty[s]);
+  }
+  kiter += nkb;
+}
+
+// smem tail layout after the ring region
+struct Tail {
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* tmem_full;   // [2]
+  uint64_t* tmem_empty;  // [2]
+  uint32_t* tmem_slot;
+  float* rs;             // [256]
+  float* red;            // [4][256]
+  float* sred;           // [2][2][128] (normal-mode ssq partials per warp group)
+};
+
+__device__ __forceinline__ Tail carve_tail(uint8_t* smem, const Params& p) {
+  Tail t;
+  uint8_t* q = smem + p.smem_stage_region;
+  t.full = reinterpret_cast<uint64_t*>(q);
+  t.empty = t.full + p.stages;
+  t.tmem_full = t.empty + p.stages;
+  t.tmem_empty = t.tmem_full + 2;
+  t.tmem_slot = reinterpret_cast<uint32_t*>(t.tmem_empty + 2);
+  t.rs = reinterpret_cast<float*>(t.tmem_slot + 4);
+  t.red = t.rs + 256;
+  t.sred = t.red + 4 * 256;
+  return t;
+}
+
+constexpr size_t kTailBytes = 8 * (2 * 16 + 4) + 16 + 4 * (256 + 4 * 256 + 2 * 2 * 128);
+
+// -------------------------------------------------- batch-1: swap + cluster split-K
+
+template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                const Params p) {
+    gemm_swap_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                     const Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
+  const Tail T = carve_tail(smem, p);
   const uint32_t b_bytes = (uint32_t)p.bn * BK * 2;
-  const uint32_t stage_bytes = kAStageBytes + ((b_bytes + 1023) & ~1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
-  uint64_t* empty = full + p.stages;
-  uint64_t* tmem_full = empty + p.stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
-  float* rs_cols = reinterpret_cast<float*>(tmem_slot + 4);  // [256]
-  float* red = rs_cols + 256;                                 // [4][256]
-
+  const Ring ring{smem, T.full, T.empty, kAStageBytes + ((b_bytes + 1023) & ~1023u), b_bytes, p.stages};
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile_a = blockIdx.x, tile_b = blockIdx.y, split = blockIdx.z;
   const int kb0 = split * p.kb_per_split;
   const int nkb = min(p.kb_per_split, p.num_kb - kb0);
+  const int S = p.splits;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
-      sm100::mbar_init(&full[s], 1);
-      sm100::mbar_init(&empty[s], 1);
+      sm100::mbar_init(&T.full[s], 1);
+      sm100::mbar_init(&T.empty[s], 1);
     }
-    sm100::mbar_init(tmem_full, 1);
+    sm100::mbar_init(&T.tmem_full[0], 1);
     sm100::fence_barrier_init();
   }
-  if (warp == 1) sm100::tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 1) sm100::tmem_alloc<256>(T.tmem_slot);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = *T.tmem_slot;
 
   if (warp == 0) {
     if (sm100::elect_one()) {
       sm100::tma_prefetch_desc(&tma_a);
       sm100::tma_prefetch_desc(&tma_b);
-      const uint64_t pol_w = sm100::policy_evict_first();
-      const uint64_t pol_x = sm100::policy_evict_last();
-      const CUtensorMap* tw = p.swap_ab ? &tma_a : &tma_b;  // weights
-      const CUtensorMap* tx = p.swap_ab ? &tma_b : &tma_a;  // activations
-      const int w_row = p.swap_ab ? tile_a * BM : tile_b * p.bn;
-      const int x_row = p.swap_ab ? tile_b * p.bn : tile_a * BM;
-      const uint32_t w_off = p.swap_ab ? 0 : kAStageBytes;
-      const uint32_t x_off = p.swap_ab ? kAStageBytes : 0;
-      const int pre = min(p.stages, nkb);
-      // weights first: independent of the previous kernel (PDL overlap)
-      for (int i = 0; i < pre; ++i) {
-        uint8_t* st = smem + i * stage_bytes;
-        sm100::mbar_arrive_expect_tx(&full[i], kAStageBytes + b_bytes);
-        sm100::tma_load_2d(tw, &full[i], st + w_off, (kb0 + i) * BK, w_row, pol_w);
+      int kiter = 0;
+      produce_tile(ring, &tma_a, &tma_b, 0, kAStageBytes, tile_a * BM, tile_b * p.bn, kb0, nkb,
+                   kiter, true, sm100::policy_evict_first(), sm100::policy_evict_last());
+    }
+  } else if (warp == 1) {
+    if (sm100::elect_one()) {
+      int kiter = 0;
+      mma_tile(ring, tmem, sm100::make_idesc_bf16(BM, p.bn), nkb, kiter);
+      sm100::umma_commit(&T.tmem_full[0]);
+    }
+    __syncwarp();
+  }
+
+  // ---------------------------------------------------------------- epilogue
+  const bool epi = warp >= 2;
+  const int q = warp & 3;                 // TMEM lane quarter
+  const int g = epi ? (warp - 2) >> 2 : 0;  // column group (0/1)
+  const int lane_row = q * 32 + lane;
+  const int n = tile_a * BM + lane_row;   // feature of this thread
+  const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
+  const EpiArgs& e = p.e;
+  if (epi) {
+    sm100::pdl_wait();
+    if (threadIdx.x == 64) sm100::pdl_launch_dependents();
+    for (int c = threadIdx.x - 64; c < p.bn; c += kEpiThreads) {
+      const int m = tile_b * p.bn + c;
+      T.rs[c] = (KIND != EPI_RESID && KIND != EPI_TANH_BF16 && m < e.M) ? row_scale(e, m) : 1.f;
+    }
+    sm100::mbar_wait(&T.tmem_full[0], 0);
+    sm100::tc_fence_after();
+  }
+  const int nchunks = p.bn / 16;
+  if (S == 1) {
+    if (epi) {
+      epi_bar();
+      for (int ch = g; ch < nchunks; ch += 2) {
+        uint32_t r[16];
+        sm100::tmem_ld16(t_lane + ch * 16, r);
+        sm100::tmem_ld_wait();
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+        epi_swap<KIND>(e, n, tile_b * p.bn + ch * 16, v, T.rs, T.red + q * 256, ch * 16);
       }
-      sm100::pdl_wait();
-      for (int i = 0; i < pre; ++i)
-        sm100::tma_load_2d(tx, &full[i], smem + i * stage_bytes + x_off, (kb0 + i) * BK, x_row, pol_x);
-      for (int i = pre; i < nkb; ++i) {
-        const int s = i % p.stages;
-        sm100::mbar_wait(&empty[s], ((i / p.stages) & 1) ^ 1);
-        uint8_t* st = smem + s * stage_bytes;
-        sm100::mbar_arrive_expect_tx(&full[s], kAStageBytes + b_bytes);
-        sm100::tma_load_2d(tw, &full[s], st + w_off, (kb0 + i) * BK, w_row, pol_w);
-        sm100::tma_load_2d(tx, &full[s], st + x_off, (kb0 + i) * BK, x_row, pol_x);
+      if (KIND == EPI_RESID) {
+        epi_bar();
+        for (int c = threadIdx.x - 64; c < p.bn; c += kEpiThreads) {
+          const int m = tile_b * p.bn + c;
+          if (m < e.M)
+            e.ssq_out[(size_t)tile_a * e.ssq_out_ld + m] =
+                ((T.red[c] + T.red[256 + c]) + T.red[512 + c]) + T.red[768 + c];
+        }
+      }
+    }
+  } else {
+    // stage this split's partial in SMEM as [col][128 lanes] (reuses the ring)
+    float* part = reinterpret_cast<float*>(smem);
+    if (epi) {
+      for (int ch = g; ch < nchunks; ch += 2) {
+        uint32_t r[16];
+        sm100::tmem_ld16(t_lane + ch * 16, r);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) part[(ch * 16 + j) * BM + lane_row] = __uint_as_float(r[j]);
+      }
+    }
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();  // every split's partial is staged
+    if (epi) {
+      const float* peers[kMaxSplits];
+      for (int s = 0; s < S; ++s) peers[s] = cluster.map_shared_rank(part, s);
+      const int per = (nchunks + S - 1) / S;
+      const int ch0 = split * per, ch1 = min(nchunks, ch0 + per);
+      for (int ch = ch0 + g; ch < ch1; ch += 2) {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        for (int s = 0; s < S; ++s) {  // fixed order: deterministic
+          const float* ps = peers[s] + ch * 16 * BM + lane_row;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += ps[j * BM];
+        }
+        epi_swap<KIND>(e, n, tile_b * p.bn + ch * 16, v, T.rs, T.red + q * 256, ch * 16);
+      }
+      if (KIND == EPI_RESID) {
+        epi_bar();
+        for (int c = ch0 * 16 + threadIdx.x - 64; c < ch1 * 16; c += kEpiThreads) {
+          const int m = tile_b * p.bn + c;
+          if (m < e.M)
+            e.ssq_out[(size_t)tile_a * e.ssq_out_ld + m] =
+                ((T.red[c] + T.red[256 + c]) + T.red[512 + c]) + T.red[768 + c];
+        }
+      }
+    }
+    cluster.sync();  // peers may still read this CTA's partial
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<256>(tmem);
+  }
+}
+
+// ------------------------------------------------------ batched: persistent
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_persistent_kernel(const __grid_constant__ CUtensorMap tma_a,
+                           const __grid_constant__ CUtensorMap tma_b, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const Tail T = carve_tail(smem, p);
+  const uint32_t b_bytes = (uint32_t)p.bn * BK * 2;
+  const Ring ring{smem, T.full, T.empty, kAStageBytes + ((b_bytes + 1023) & ~1023u), b_bytes, p.stages};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      sm100::mbar_init(&T.full[s], 1);
+      sm100::mbar_init(&T.empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      sm100::mbar_init(&T.tmem_full[a], 1);
+      sm100::mbar_init(&T.tmem_empty[a], kEpiThreads);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<512>(T.tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *T.tmem_slot;
+
+  if (warp == 0) {
+    if (sm100::elect_one()) {
+      sm100::tma_prefetch_desc(&tma_a);
+      sm100::tma_prefetch_desc(&tma_b);
+      const uint64_t pol_w = sm100::policy_evict_last();   // weights: reused by every row tile
+      const uint64_t pol_x = sm100::policy_evict_first();  // activations: read by tiles_b CTAs at once
+      int kiter = 0;
+      bool first = true;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        const int ta = t / p.tiles_b, tb = t % p.tiles_b;
+        produce_tile(ring, &tma_b, &tma_a, kAStageBytes, 0, tb * p.bn, ta * BM, 0, p.num_kb, kiter,
+                     first, pol_w, pol_x);
+        first = false;
       }
     }
   } else if (warp == 1) {
     if (sm100::elect_one()) {
       const uint32_t idesc = sm100::make_idesc_bf16(BM, p.bn);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % p.stages;
-        sm100::mbar_wait(&full[s], (i / p.stages) & 1);
+      int kiter = 0, it = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
+        const int a = it & 1;
+        if (it >= 2) sm100::mbar_wait(&T.tmem_empty[a], ((it >> 1) & 1) ^ 1);
         sm100::tc_fence_after();
-        const uint32_t a_addr = sm100::smem_u32(smem + s * stage_bytes);
-        const uint32_t b_addr = a_addr + kAStageBytes;
-#pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          sm100::umma_bf16(tmem, sm100::make_sw128_desc(a_addr + k * 32),
-                           sm100::make_sw128_desc(b_addr + k * 32), idesc, (i | k) != 0);
-        }
-        sm100::umma_commit(&empty[s]);
+        mma_tile(ring, tmem + a * 256, idesc, p.num_kb, kiter);
+        sm100::umma_commit(&T.tmem_full[a]);
       }
-      sm100::umma_commit(tmem_full);
     }
     __syncwarp();
   } else {
-    // ------------------------------------------------------------ epilogue
-    const int et = threadIdx.x - 64;  // 0..127
-    const int q = warp & 3;           // TMEM lane quarter this warp may access
+    const int q = warp & 3;
+    const int g = (warp - 2) >> 2;
     const int lane_row = q * 32 + lane;
-    const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
+    const EpiArgs& e = p.e;
     sm100::pdl_wait();
-    if (et == 0) sm100::pdl_launch_dependents();
-    sm100::mbar_wait(tmem_full, 0);
-    sm100::tc_fence_after();
-    const int tiles = p.tiles_a * p.tiles_b;
-    const int tile_id = tile_a * p.tiles_b + tile_b;
-    bool proceed = true;
-    if (p.splits > 1) {
-      float* mine = p.ws + ((size_t)split * tiles + tile_id) * p.bn * BM;
-      for (int c0 = 0; c0 < p.bn; c0 += 16) {
+    if (threadIdx.x == 64) sm100::pdl_launch_dependents();
+    int it = 0;
+    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
+      const int ta = t / p.tiles_b, tb = t % p.tiles_b;
+      const int a = it & 1;
+      const int m = ta * BM + lane_row;
+      const float rs = (KIND != EPI_RESID && KIND != EPI_TANH_BF16 && m < e.M) ? row_scale(e, m) : 1.f;
+      sm100::mbar_wait(&T.tmem_full[a], (it >> 1) & 1);
+      sm100::tc_fence_after();
+      const uint32_t t_lane = tmem + a * 256 + ((uint32_t)(q * 32) << 16);
+      float ssq[2] = {0.f, 0.f};
+      for (int ch = g; ch < p.bn / 16; ch += 2) {
         uint32_t r[16];
-        sm100::tmem_ld16(t_lane + c0, r);
-        sm100::tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) mine[(size_t)(c0 + j) * BM + lane_row] = __uint_as_float(r[j]);
-      }
-      __threadfence();
-      epi_bar();
-      if (et == 0) {
-        const int prev = atomicAdd(&p.counters[tile_id], 1);
-        const int last = prev == p.splits - 1;
-        if (last) p.counters[tile_id] = 0;  // re-arm for the next launch / graph replay
-        *last_flag = last;
-      }
-      epi_bar();
-      proceed = *last_flag != 0;
-      if (proceed) __threadfence();
-    }
-    if (proceed) {
-      const EpiArgs& e = p.e;
-      float rs_row = 1.f;
-      if (p.swap_ab) {
-        for (int c = et; c < p.bn; c += 128) {
-          const int m = tile_b * p.bn + c;
-          rs_cols[c] = (e.kind != EPI_RESID && m < e.M) ? row_scale(e, m) : 1.f;
-        }
-        epi_bar();
-      } else {
-        const int m = tile_a * BM + lane_row;
-        rs_row = (e.kind != EPI_RESID && m < e.M) ? row_scale(e, m) : 1.f;
-      }
-      float ssq_acc = 0.f;
-      for (int c0 = 0; c0 < p.bn; c0 += 16) {
-        uint32_t r[16];
-        sm100::tmem_ld16(t_lane + c0, r);
+        sm100::tmem_ld16(t_lane + ch * 16, r);
         sm100::tmem_ld_wait();
         float v[16];
-        if (p.splits > 1) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = 0.f;
-          for (int s = 0; s < p.splits; ++s) {
-            if (s == split) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] += __uint_as_float(r[j]);
-            } else {
-              const float* part = p.ws + ((size_t)s * tiles + tile_id) * p.bn * BM;
-#pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] += __ldcg(part + (size_t)(c0 + j) * BM + lane_row);
-            }
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-        }
-        apply_chunk(p, v, lane_row, c0, rs_cols, rs_row, red + q * 256, ssq_acc);
-        if (e.kind == EPI_RESID && !p.swap_ab && ((c0 + 16) % 128 == 0 || c0 + 16 >= p.bn)) {
-          const int m = tile_a * BM + lane_row;
-          const int g = (tile_b * p.bn + c0) / 128;
-          if (m < e.M) e.ssq_out[(size_t)g * e.ssq_out_ld + m] = ssq_acc;
-          ssq_acc = 0.f;
-        }
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+        float acc = 0.f;
+        epi_normal<KIND>(e, m, tb * p.bn + ch * 16, v, rs, acc);
+        ssq[(ch * 16) >> 7] += acc;
       }
-      if (e.kind == EPI_RESID && p.swap_ab) {
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&T.tmem_empty[a]);
+      if (KIND == EPI_RESID) {
+        // two warp groups hold partial sums of the same 128-feature group
+        T.sred[(g * 2 + 0) * 128 + lane_row] = ssq[0];
+        T.sred[(g * 2 + 1) * 128 + lane_row] = ssq[1];
         epi_bar();
-        const int g = (tile_a * BM) / 128;
-        for (int c = et; c < p.bn; c += 128) {
-          const int m = tile_b * p.bn + c;
-          if (m < e.M)
-            e.ssq_out[(size_t)g * e.ssq_out_ld + m] =
-                ((red[c] + red[256 + c]) + red[512 + c]) + red[768 + c];
+        if (g == 0 && m < e.M) {
+          for (int fg = 0; fg < p.bn / 128; ++fg)
+            e.ssq_out[(size_t)((tb * p.bn) / 128 + fg) * e.ssq_out_ld + m] =
+                T.sred[fg * 128 + lane_row] + T.sred[(2 + fg) * 128 + lane_row];
         }
+        epi_bar();
       }
     }
   }
@@ -316,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     sm100::tc_fence_after();
-    sm100::tmem_dealloc<kTmemCols>(tmem);
+    sm100::tmem_dealloc<512>(tmem);
   }
 }
 

@@ -1,4 +1,4 @@
-// Host-side planning/launch of the tcgen05 GEMM (gemm.cuh).
+// Host-side planning/launch of the tcgen05 GEMMs (gemm.cuh).
 #pragma once
 
 #include <cuda.h>
@@ -15,24 +15,26 @@ struct Op {
   CUtensorMap tb;
   Params p;
   dim3 grid;
-  size_t smem;
+  int cluster = 1;   // split-K cluster size (swap kernel)
+  size_t smem = 0;
+  void* fn = nullptr;  // specialised kernel
 };
 
 // Encode a 2-D K-major bf16 tensor map (rows x K, row stride `ld` elements)
 // with a 64 x box_rows SWIZZLE_128B box.
 int make_map(CUtensorMap* m, const void* ptr, int rows, int K, int ld, int box_rows);
 
-// Plan one GEMM. `A` has rows_a rows, `B` rows_b rows, both K-major with K
-// columns (row strides lda/ldb elements). splits=0 picks split-K so that the
-// grid covers ~`target_ctas` CTAs. ws/counters may be null when splits == 1.
+// Number of K splits that spreads `tiles` output tiles over the SMs.
+int auto_splits(int tiles, int num_kb);
+
+// Plan one GEMM. swap_ab=1: A rows are output features (weights), B rows are
+// token rows, bn covers the tokens, split-K through a CTA cluster (splits<=0:
+// auto). swap_ab=0: A rows are token rows, B rows are features, persistent
+// whole-K tiles (splits ignored).
 int plan(Op* op, const void* A, int rows_a, int lda, const void* B, int rows_b, int ldb, int K,
-         int bn, int splits, int swap_ab, const EpiArgs& e, float* ws, size_t ws_bytes,
-         int* counters, int n_counters, int max_stages = 8);
+         int bn, int splits, int swap_ab, const EpiArgs& e, int max_stages = 8);
 
 int launch(const Op& op, cudaStream_t stream, bool pdl);
-
-// split-K workspace needed for a plan (bytes) and counters (ints)
-size_t ws_bytes_needed(int rows_a, int rows_b, int K, int bn, int splits);
 
 }  // namespace gemm
 }  // namespace sf

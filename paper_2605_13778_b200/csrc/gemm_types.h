@@ -1,4 +1,4 @@
-// Shared host/device definitions of the tcgen05 GEMM (kernel in gemm.cuh).
+// Shared host/device definitions of the tcgen05 GEMM (kernels in gemm.cuh).
 #pragma once
 
 #include <cuda_bf16.h>
@@ -9,17 +9,20 @@ namespace gemm {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;                        // 2 per TMEM lane quarter
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kThreads = 64 + kEpiThreads;          // warp 0 TMA, warp 1 MMA, 8 epilogue warps
 constexpr uint32_t kAStageBytes = BM * BK * 2;
-constexpr int kTmemCols = 256;
+constexpr int kMaxSplits = 16;                      // cluster size along the split-K axis
 
 enum EpiKind : int {
-  EPI_F32 = 0,    // out_f32[m, n] = acc * r[m]
-  EPI_BF16 = 1,   // out_bf16[m, n] = bf16(acc * r[m])
-  EPI_QKV = 2,    // RMS scale, RoPE on q/k (paired rows), q/k row-major, v transposed
-  EPI_RESID = 3,  // x[m, n] += acc; xb = bf16(x); ssq partials per 128-feature group
-  EPI_GEGLU = 4,  // RMS scale, h[m, n/2] = gelu_tanh(gate) * up for paired rows
+  EPI_F32 = 0,        // out_f32[m, n] = acc * r[m] (+ bias[n])
+  EPI_BF16 = 1,       // out_bf16[m, n] = bf16(acc * r[m] (+ bias[n]))
+  EPI_QKV = 2,        // RMS scale, RoPE on q/k (paired rows), q/k row-major, v transposed
+  EPI_RESID = 3,      // x[m, n] += acc; xb = bf16(x); ssq partials per 128-feature group
+  EPI_GEGLU = 4,      // RMS scale, h[m, n/2] = gelu_tanh(gate) * up for paired rows
   EPI_TANH_BF16 = 5,  // out_bf16[m, n] = bf16(tanh(acc + bias[n]))  (draft MLP hidden)
+  EPI_KINDS = 6
 };
 
 struct EpiArgs {
@@ -30,7 +33,7 @@ struct EpiArgs {
   int ld_f32;
   __nv_bfloat16* out_bf16;
   int ld_bf16;
-  const float* bias;  // per output feature (EPI_F32 / EPI_BF16), may be null
+  const float* bias;  // per output feature (F32 / BF16 / TANH), may be null
   // RMSNorm row scale r[m] = rsqrt(sum_g ssq_in[g * ssq_ld + m] * inv_width + eps)
   const float* ssq_in;
   int ssq_groups;
@@ -45,7 +48,7 @@ struct EpiArgs {
   const float2* rope;  // [pos][head_dim/2] (cos, sin)
   int q_features;      // q_heads * head_dim
   int env_rows, seg_len, pos0;
-  // RESID
+  // RESID (x, xb are [M, N] row-major)
   float* x;
   __nv_bfloat16* xb;
   float* ssq_out;
@@ -58,9 +61,8 @@ struct Params {
   int num_kb, kb_per_split, splits;
   int stages;
   int swap_ab;
-  int tiles_a, tiles_b;
-  float* ws;       // [splits][tiles][bn][128] fp32 partials
-  int* counters;   // [tiles]
+  int tiles_a, tiles_b, total_tiles;
+  uint32_t smem_stage_region;  // bytes reserved for the TMA ring (>= split-K staging)
   EpiArgs e;
 };
 

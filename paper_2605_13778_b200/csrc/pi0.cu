@@ -457,42 +457,13 @@ int build(Handle& h, Buffers& b, int B, int K) {
 
   // --- GEMM plans. Batch-1 shapes stream weights (swap-AB + split-K);
   // larger batches run the normal orientation with 256-feature tiles.
+  // Batch-1 shapes stream weights: swap-AB + split-K reduced over DSMEM in a
+  // CTA cluster. Larger batches: persistent 128 x 256 tiles.
   const bool swap = b.M <= 256;
   const int bn_swap = ((b.M + 15) / 16) * 16;
-  struct G {
-    const void* w;
-    int n_out, k_in;
-    int kind;
-  };
-  // worst-case split-K workspace across all GEMMs
-  size_t ws = 0;
-  int max_tiles = 0;
-  auto splits_for = [&](int n_out, int k_in, int bn) {
-    const int tiles = swap ? (n_out + 127) / 128 : ((b.M + 127) / 128) * ((n_out + bn - 1) / bn);
-    int s = 148 / (tiles > 0 ? tiles : 1);
-    if (s < 1) s = 1;
-    const int kb = k_in / 64;
-    if (s > kb) s = kb;
-    const int kbps = (kb + s - 1) / s;
-    s = (kb + kbps - 1) / kbps;
-    if (tiles > max_tiles) max_tiles = tiles;
-    const size_t need = swap ? gemm::ws_bytes_needed(n_out, b.M, k_in, bn, s)
-                             : gemm::ws_bytes_needed(b.M, n_out, k_in, bn, s);
-    if (need > ws) ws = need;
-    return s;
-  };
   const int bn_norm = 256;
-  std::vector<int> splits;
-  for (int l = 0; l < L; ++l) {
-    splits.push_back(splits_for(nq + 2 * c.head_dim, W, swap ? bn_swap : bn_norm));
-    splits.push_back(splits_for(W, nq, swap ? bn_swap : bn_norm));
-    splits.push_back(splits_for(2 * c.mlp, W, swap ? bn_swap : bn_norm));
-    splits.push_back(splits_for(W, c.mlp, swap ? bn_swap : bn_norm));
-  }
   const int bn_head = swap ? bn_swap : 32;
-  splits.push_back(splits_for(c.action_dim, W, bn_head));
-  b.ws_bytes = ws;
-  if (ws) ALLOC(b.ws, ws / sizeof(float));
+  int max_tiles = 0;
   // attention split-KV workspace
   const int n_prefix_blocks = (c.prefix_len + attn::BKEY - 1) / attn::BKEY;
   // suffix keys of the (<= 2) segments a 16-token tile touches, from a
@@ -523,16 +494,15 @@ int build(Handle& h, Buffers& b, int B, int K) {
     return e;
   };
   b.ops.resize(4 * L + 1);
-  int si = 0;
+  // token rows `rows` (activations, K-major) x weights [n_out, k_in]
+  auto plan_mm = [&](gemm::Op* op, const void* wt, int n_out, const void* act, int rows, int k_in,
+                     int bn, bool sw, const gemm::EpiArgs& e) {
+    if (sw) return gemm::plan(op, wt, n_out, k_in, act, rows, k_in, k_in, bn, 0, 1, e);
+    return gemm::plan(op, act, rows, k_in, wt, n_out, k_in, k_in, bn, 1, 0, e);
+  };
   auto plan_op = [&](gemm::Op* op, const void* wt, int n_out, const void* act, int k_in,
                      const gemm::EpiArgs& e) {
-    const int bn = swap ? bn_swap : bn_norm;
-    const int sp = splits[si++];
-    if (swap)
-      return gemm::plan(op, wt, n_out, k_in, act, b.M, k_in, k_in, bn, sp, 1, e, b.ws, b.ws_bytes,
-                        b.counters, b.n_counters);
-    return gemm::plan(op, act, b.M, k_in, wt, n_out, k_in, k_in, bn, sp, 0, e, b.ws, b.ws_bytes,
-                      b.counters, b.n_counters);
+    return plan_mm(op, wt, n_out, act, b.M, k_in, swap ? bn_swap : bn_norm, swap, e);
   };
   for (int l = 0; l < L; ++l) {
     gemm::EpiArgs e = epi_base(gemm::EPI_QKV);
@@ -568,15 +538,8 @@ int build(Handle& h, Buffers& b, int B, int K) {
     e.out_f32 = b.vel;
     e.ld_f32 = c.action_dim;
     e.bias = static_cast<const float*>(h.w.out_b);
-    const int bn = bn_head;
-    const int sp = splits[si++];
-    if (swap)
-      rc = gemm::plan(&b.ops[4 * L], h.w.out_w, c.action_dim, W, b.xb, b.M, W, W, bn, sp, 1, e,
-                      b.ws, b.ws_bytes, b.counters, b.n_counters);
-    else
-      rc = gemm::plan(&b.ops[4 * L], b.xb, b.M, W, h.w.out_w, c.action_dim, W, W, bn, sp, 0, e,
-                      b.ws, b.ws_bytes, b.counters, b.n_counters);
-    if (rc) return rc;
+    if ((rc = plan_mm(&b.ops[4 * L], h.w.out_w, c.action_dim, b.xb, b.M, W, bn_head, swap, e)))
+      return rc;
   }
   // --- draft MLP plans: rows = envs (swap-AB while B <= 256)
   if (b.has_draft) {
@@ -600,19 +563,8 @@ int build(Handle& h, Buffers& b, int B, int K) {
         e.out_f32 = b.draft;
         e.ld_f32 = HDc;
       }
-      const int tiles = dswap ? (nout[i] + 127) / 128 : ((B + 127) / 128) * ((nout[i] + 255) / 256);
-      int sp = 148 / tiles;
-      sp = sp < 1 ? 1 : (sp > kin[i] / 64 ? kin[i] / 64 : sp);
-      const size_t need = dswap ? gemm::ws_bytes_needed(nout[i], B, kin[i], dbn, sp)
-                                : gemm::ws_bytes_needed(B, nout[i], kin[i], dbn, sp);
-      if (need > b.ws_bytes || tiles > b.n_counters) sp = 1;
-      if (dswap)
-        rc = gemm::plan(&b.dops[i], h.w.draft_w[i], nout[i], kin[i], ins[i], B, kin[i], kin[i], dbn,
-                        sp, 1, e, b.ws, b.ws_bytes, b.counters, b.n_counters);
-      else
-        rc = gemm::plan(&b.dops[i], ins[i], B, kin[i], h.w.draft_w[i], nout[i], kin[i], kin[i], dbn,
-                        sp, 0, e, b.ws, b.ws_bytes, b.counters, b.n_counters);
-      if (rc) return rc;
+      if ((rc = plan_mm(&b.dops[i], h.w.draft_w[i], nout[i], ins[i], B, kin[i], dbn, dswap, e)))
+        return rc;
     }
   }
   // --- attention plans (per layer: 5 tensor maps)
