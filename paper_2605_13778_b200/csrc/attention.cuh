@@ -17,6 +17,7 @@
 // last CTA of each tile merges the partials in a fixed order.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -25,6 +26,8 @@
 
 namespace sf {
 namespace attn {
+
+namespace cg = cooperative_groups;
 
 constexpr int kThreads = 192;
 constexpr int BQ = 128;     // query rows per tile (16 tokens x 8 heads)
@@ -38,7 +41,8 @@ constexpr uint32_t kPBytes = BQ * BKEY * 2;       // 16 KB
 constexpr uint32_t kStageBytes = kKBytes + kVBytes;
 constexpr uint32_t kSmemBytes = kQBytes + 2 * kStageBytes + kPBytes + 1024 /*bars*/ + 1024 /*align*/;
 constexpr int kTmemCols = 512;  // S0 [0,64) S1 [64,128) O [128,384)
-constexpr int kWsRow = HD + 4;  // split-KV partial row: O[256], m, l (+pad: 16 B aligned rows)
+constexpr int kPartStride = HD + 2;  // split-KV partial O row stride in SMEM (floats)
+constexpr int kMaxSplitsKV = 16;     // split-KV cluster size limit
 
 struct Params {
   int M;            // valid token rows
@@ -211,6 +215,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int seg_q = local_q / p.seg_len;
     const int t_q = local_q - seg_q * p.seg_len;
     const bool real_q = local_q < p.segs * p.seg_len && tok < p.M;
+    const int seg_lo = seg_q * p.seg_len;                         // local token range of the
+    const int seg_hi = seg_lo + (t_q >= 1 ? p.seg_len : 1);       // row's visible suffix keys
     float m_used = -INFINITY, l_sum = 0.f;
     sm100::pdl_wait();
     if (r == 0) sm100::pdl_launch_dependents();
@@ -225,22 +231,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::tmem_ld_wait();
       sm100::tc_fence_before();
       sm100::mbar_arrive(&s_free[s]);
+      // The valid keys of a row inside one block are a contiguous column range
+      // [lo, hi): prefix keys < P; suffix keys = the row's own segment, only
+      // its state token for the state row (block mask).
+      int lo = 0, hi;
+      if (j < p.n_prefix_blocks) {
+        hi = p.prefix_len - j * BKEY;
+      } else if (real_q) {
+        const int base = sb + (j - p.n_prefix_blocks) * BKEY - env_start;  // local token of col 0
+        lo = seg_lo - base;
+        hi = seg_hi - base;
+      } else {
+        hi = 0;
+      }
       float sv[64];
       float mb = -INFINITY;
-      const bool is_prefix = j < p.n_prefix_blocks;
 #pragma unroll
       for (int c = 0; c < 64; ++c) {
-        bool valid;
-        if (is_prefix) {
-          valid = j * BKEY + c < p.prefix_len;
-        } else {
-          const int kt = sb + (j - p.n_prefix_blocks) * BKEY + c - env_start;
-          const int seg_k = kt / p.seg_len;
-          valid = real_q && kt >= 0 && kt < p.segs * p.seg_len && seg_k == seg_q &&
-                  (t_q >= 1 || kt - seg_k * p.seg_len == 0);
-        }
         const float x = __uint_as_float(raw[c >> 4][c & 15]) * p.scale_log2;
-        sv[c] = valid ? x : -INFINITY;
+        sv[c] = (c >= lo && c < hi) ? x : -INFINITY;
         mb = fmaxf(mb, sv[c]);
       }
       const float m_new = fmaxf(m_used, mb);
@@ -278,13 +287,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       // P row (64 keys, bf16) into the SWIZZLE_128B K-major tile: 16 B chunk c
       // of row r lives at chunk (c ^ (r & 7)).
       uint8_t* prow = sP + r * 128;
+      // masked scores are -inf -> exp2 gives 0; rows with nothing valid yet use 0
+      const float mu = m_used == -INFINITY ? 0.f : m_used;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         uint32_t w[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const float p0 = m_used == -INFINITY ? 0.f : exp2f(sv[c * 8 + 2 * k] - m_used);
-          const float p1 = m_used == -INFINITY ? 0.f : exp2f(sv[c * 8 + 2 * k + 1] - m_used);
+          const float p0 = exp2f(sv[c * 8 + 2 * k] - mu);
+          const float p1 = exp2f(sv[c * 8 + 2 * k + 1] - mu);
           l_sum += p0 + p1;
           __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
           w[k] = *reinterpret_cast<uint32_t*>(&b2);
@@ -321,64 +332,57 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     } else {
-      constexpr int kRow = kWsRow;
-      float* mine = p.ws + (((size_t)tile * p.splits + split) * BQ + r) * kRow;
+      // stage the unnormalised partial O (row-major, padded stride: conflict
+      // free) + (m, l) in this CTA's SMEM; the Q/KV region is free now
+      float* part = reinterpret_cast<float*>(sQ);
       for (int c0 = 0; c0 < HD; c0 += 16) {
         uint32_t o[16];
         sm100::tmem_ld16(t_lane + 128 + c0, o);
         sm100::tmem_ld_wait();
 #pragma unroll
-        for (int k = 0; k < 16; k += 4)
-          *reinterpret_cast<float4*>(mine + c0 + k) =
-              make_float4(__uint_as_float(o[k]), __uint_as_float(o[k + 1]),
-                          __uint_as_float(o[k + 2]), __uint_as_float(o[k + 3]));
+        for (int k = 0; k < 16; ++k) part[r * kPartStride + c0 + k] = __uint_as_float(o[k]);
       }
-      mine[HD] = m_used;
-      mine[HD + 1] = l_sum;
-      __threadfence();
-      softmax_bar();
-      if (r == 0) {
-        const int prev = atomicAdd(&p.counters[tile], 1);
-        const int last = prev == p.splits - 1;
-        if (last) p.counters[tile] = 0;
-        *last_flag = last;
+      float* ml = reinterpret_cast<float*>(sP);
+      ml[r] = m_used;
+      ml[BQ + r] = l_sum;
+    }
+  }
+  if (p.splits > 1) {
+    // split-KV merge over DSMEM: the splits of a tile form one cluster; CTA
+    // `split` merges rows [split*rows, (split+1)*rows) in a fixed split order
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    if (warp >= 2) {
+      const int t = threadIdx.x - 64;  // 0..127: owns columns 2t, 2t+1
+      const int rows = (BQ + p.splits - 1) / p.splits;
+      const int r0 = split * rows, r1 = min(BQ, r0 + rows);
+      const float* parts[kMaxSplitsKV];
+      const float* mls[kMaxSplitsKV];
+      for (int s = 0; s < p.splits; ++s) {
+        parts[s] = cluster.map_shared_rank(reinterpret_cast<float*>(sQ), s);
+        mls[s] = cluster.map_shared_rank(reinterpret_cast<float*>(sP), s);
       }
-      softmax_bar();
-      if (*last_flag) {
-        __threadfence();
+      for (int row = r0; row < r1; ++row) {
+        const int tok = m0 + (row >> 3), head = row & 7;
         float mx = -INFINITY;
-        for (int s = 0; s < p.splits; ++s)
-          mx = fmaxf(mx, __ldcg(p.ws + (((size_t)tile * p.splits + s) * BQ + r) * kRow + HD));
-        float L = 0.f;
+        for (int s = 0; s < p.splits; ++s) mx = fmaxf(mx, mls[s][row]);
+        float L = 0.f, a0 = 0.f, a1 = 0.f;
         for (int s = 0; s < p.splits; ++s) {
-          const float* ps = p.ws + (((size_t)tile * p.splits + s) * BQ + r) * kRow;
-          const float ms = __ldcg(ps + HD);
-          if (ms > -INFINITY) L += exp2f(ms - mx) * __ldcg(ps + HD + 1);
+          const float ms = mls[s][row];
+          const float wgt = ms > -INFINITY ? exp2f(ms - mx) : 0.f;
+          L += wgt * mls[s][BQ + row];
+          const float2 o = *reinterpret_cast<const float2*>(parts[s] + row * kPartStride + 2 * t);
+          a0 += wgt * o.x;
+          a1 += wgt * o.y;
         }
         const float inv = L > 0.f ? 1.f / L : 0.f;
-        __nv_bfloat16* dst = p.out + (size_t)tok * (kHeads * HD) + head * HD;
-        for (int c0 = 0; c0 < HD; c0 += 8) {
-          float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          for (int s = 0; s < p.splits; ++s) {
-            const float* ps = p.ws + (((size_t)tile * p.splits + s) * BQ + r) * kRow;
-            const float ms = __ldcg(ps + HD);
-            if (!(ms > -INFINITY)) continue;
-            const float wgt = exp2f(ms - mx);
-            const float4 a = __ldcg(reinterpret_cast<const float4*>(ps + c0));
-            const float4 b = __ldcg(reinterpret_cast<const float4*>(ps + c0 + 4));
-            acc[0] += wgt * a.x; acc[1] += wgt * a.y; acc[2] += wgt * a.z; acc[3] += wgt * a.w;
-            acc[4] += wgt * b.x; acc[5] += wgt * b.y; acc[6] += wgt * b.z; acc[7] += wgt * b.w;
-          }
-          uint32_t w[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[2 * k] * inv, acc[2 * k + 1] * inv);
-            w[k] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-          if (tok < p.M) *reinterpret_cast<uint4*>(dst + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+        if (tok < p.M) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(a0 * inv, a1 * inv);
+          *reinterpret_cast<__nv_bfloat162*>(p.out + (size_t)tok * (kHeads * HD) + head * HD + 2 * t) = b2;
         }
       }
     }
+    cluster.sync();  // peers may still read this CTA's partial
   }
   sm100::tc_fence_before();
   __syncthreads();

@@ -122,63 +122,100 @@ struct EmbedParams {
   int ssq_ld;
 };
 
-// One CTA per token row (256 threads, W/256 features each).
+// One CTA per 16 token rows (256 threads; thread t owns features t + 256 i).
+// Each weight row is read once per CTA and reused for all 16 tokens.
+constexpr int kEmbedTok = 16;
+
 __global__ void __launch_bounds__(256) embed_kernel(const EmbedParams p) {
   sm100::pdl_wait();
-  const int m = blockIdx.x;
-  const int e = m / p.env_rows;
-  const int local = m - e * p.env_rows;
-  const int k = local / p.T;
-  const int t = local - k * p.T;
-  const bool real = local < p.K * p.T;
-  __shared__ float in[64];
-  __shared__ float red[8][8];
-  if (real && threadIdx.x < 64) {
-    float v = 0.f;
-    if (t == 0) {
-      if (threadIdx.x < p.S) v = p.state[e * p.S + threadIdx.x];
-    } else if (threadIdx.x < p.D) {
-      if (p.mode == 0) {
-        const int i = (e * p.H + (t - 1)) * p.D + threadIdx.x;
-        const float tau = p.taus[k];
-        // tau * a + (1 - tau) * eps, rounded like the verify epilogue (verifier.py:73)
-        v = __fadd_rn(__fmul_rn(tau, p.draft[i]), __fmul_rn(__fsub_rn(1.f, tau), p.eps[i]));
-      } else {
-        v = p.draft[((e * p.K + k) * p.H + (t - 1)) * p.D + threadIdx.x];
-      }
-    }
-    in[threadIdx.x] = v;
-  }
+  const int m0 = blockIdx.x * kEmbedTok;
+  __shared__ float in[kEmbedTok][65];
+  __shared__ int kind[kEmbedTok];  // 0 padding, 1 state token, 2 action token
+  __shared__ int kbr[kEmbedTok];   // branch of the token
+  __shared__ float red[8][8][kEmbedTok];
+  __shared__ int has_state;
+  if (threadIdx.x == 0) has_state = 0;
   __syncthreads();
-  float sq[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int n = threadIdx.x; n < p.W; n += blockDim.x) {
-    float acc = 0.f;
+  for (int idx = threadIdx.x; idx < kEmbedTok * 64; idx += blockDim.x) {
+    const int tk = idx >> 6, c = idx & 63;
+    const int m = m0 + tk;
+    const int e = m / p.env_rows;
+    const int local = m - e * p.env_rows;
+    const int k = local / p.T;
+    const int t = local - k * p.T;
+    const bool real = local < p.K * p.T && e < p.B;
+    float v = 0.f;
     if (real) {
       if (t == 0) {
-        acc = p.s_b[n];
-        for (int i = 0; i < p.S; ++i) acc = fmaf(p.s_w[n * p.S + i], in[i], acc);
-      } else {
-        acc = p.a_b[n];
-        for (int i = 0; i < p.D; ++i) acc = fmaf(p.a_w[n * p.D + i], in[i], acc);
-        acc += p.temb[k * p.W + n];
+        if (c < p.S) v = p.state[e * p.S + c];
+      } else if (c < p.D) {
+        if (p.mode == 0) {
+          const int i = (e * p.H + (t - 1)) * p.D + c;
+          const float tau = p.taus[k];
+          // tau * a + (1 - tau) * eps, rounded like the verify epilogue (verifier.py:73)
+          v = __fadd_rn(__fmul_rn(tau, p.draft[i]), __fmul_rn(__fsub_rn(1.f, tau), p.eps[i]));
+        } else {
+          v = p.draft[((e * p.K + k) * p.H + (t - 1)) * p.D + c];
+        }
       }
     }
-    p.x[(size_t)m * p.W + n] = acc;
-    p.xb[(size_t)m * p.W + n] = __float2bfloat16_rn(acc);
-    sq[n >> 7 & 7] += acc * acc;
-  }
-  // per-128-feature-group sum of squares (fixed reduction order)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int g = 0; g < 8; ++g) {
-    float s = sq[g];
-    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) red[warp][g] = s;
+    in[tk][c] = v;
+    if (c == 0) {
+      kind[tk] = real ? (t == 0 ? 1 : 2) : 0;
+      kbr[tk] = k;
+      if (real && t == 0) has_state = 1;
+    }
   }
   __syncthreads();
-  if (threadIdx.x < p.W / 128) {
-    float s = 0.f;
-    for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
-    p.ssq[(size_t)threadIdx.x * p.ssq_ld + m] = s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_iter = p.W / 256;
+  for (int it = 0; it < n_iter; ++it) {
+    const int n = threadIdx.x + 256 * it;
+    float acc[kEmbedTok];
+    const float ab = p.a_b[n];
+#pragma unroll
+    for (int tk = 0; tk < kEmbedTok; ++tk) acc[tk] = ab;
+    for (int c = 0; c < p.D; ++c) {
+      const float w = p.a_w[n * p.D + c];
+#pragma unroll
+      for (int tk = 0; tk < kEmbedTok; ++tk) acc[tk] = fmaf(w, in[tk][c], acc[tk]);
+    }
+    if (has_state) {
+      float sacc[kEmbedTok];
+      const float sb = p.s_b[n];
+#pragma unroll
+      for (int tk = 0; tk < kEmbedTok; ++tk) sacc[tk] = sb;
+      for (int c = 0; c < p.S; ++c) {
+        const float w = p.s_w[n * p.S + c];
+#pragma unroll
+        for (int tk = 0; tk < kEmbedTok; ++tk) sacc[tk] = fmaf(w, in[tk][c], sacc[tk]);
+      }
+#pragma unroll
+      for (int tk = 0; tk < kEmbedTok; ++tk)
+        if (kind[tk] == 1) acc[tk] = sacc[tk];
+    }
+#pragma unroll
+    for (int tk = 0; tk < kEmbedTok; ++tk) {
+      const int m = m0 + tk;
+      float v = 0.f;
+      if (kind[tk] == 2) v = acc[tk] + p.temb[kbr[tk] * p.W + n];
+      else if (kind[tk] == 1) v = acc[tk];
+      p.x[(size_t)m * p.W + n] = v;
+      p.xb[(size_t)m * p.W + n] = __float2bfloat16_rn(v);
+      float sq = v * v;
+      for (int off = 16; off; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+      if (lane == 0) red[warp][it][tk] = sq;
+    }
+  }
+  __syncthreads();
+  // per-128-feature-group sum of squares: group 2*it + half, half = warp >> 2
+  const int groups = p.W / 128;
+  for (int idx = threadIdx.x; idx < groups * kEmbedTok; idx += blockDim.x) {
+    const int g = idx / kEmbedTok, tk = idx - g * kEmbedTok;
+    const int it = g >> 1, half = g & 1;
+    const float s = ((red[4 * half][it][tk] + red[4 * half + 1][it][tk]) + red[4 * half + 2][it][tk]) +
+                    red[4 * half + 3][it][tk];
+    p.ssq[(size_t)g * p.ssq_ld + m0 + tk] = s;
   }
   if (threadIdx.x == 0) sm100::pdl_launch_dependents();
 }
@@ -473,11 +510,11 @@ int build(Handle& h, Buffers& b, int B, int K) {
   int asplit = 148 / b.attn_tiles;
   if (asplit < 1) asplit = 1;
   if (asplit > n_blocks) asplit = n_blocks;
+  if (asplit > attn::kMaxSplitsKV) asplit = attn::kMaxSplitsKV;
   const int bps = (n_blocks + asplit - 1) / asplit;
   asplit = (n_blocks + bps - 1) / bps;
-  b.attn_splits = asplit;
+  b.attn_splits = asplit;  // split-KV CTAs of a tile form one cluster (DSMEM merge)
   float* attn_ws = nullptr;
-  if (asplit > 1) ALLOC(attn_ws, (size_t)b.attn_tiles * asplit * attn::BQ * attn::kWsRow);
   b.n_counters = (max_tiles > b.attn_tiles ? max_tiles : b.attn_tiles) + 8;
   ALLOC(b.counters, (size_t)b.n_counters);
 #undef ALLOC
@@ -609,6 +646,8 @@ int launch_attn(const Buffers& b, int l, cudaStream_t s, bool pdl) {
     SF_CHECK_CUDA(cudaFuncSetAttribute(attn::attn_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)attn::kSmemBytes));
+    SF_CHECK_CUDA(cudaFuncSetAttribute(attn::attn_kernel,
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
   const CUtensorMap* mp = &b.attn_maps[5 * l];
@@ -617,11 +656,19 @@ int launch_attn(const Buffers& b, int l, cudaStream_t s, bool pdl) {
   cfg.blockDim = dim3(attn::kThreads);
   cfg.dynamicSmemBytes = attn::kSmemBytes;
   cfg.stream = s;
-  cudaLaunchAttribute a[1];
+  cudaLaunchAttribute a[2];
   a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   a[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  int na = 1;
+  if (b.attn_splits > 1) {
+    a[1].id = cudaLaunchAttributeClusterDimension;
+    a[1].val.clusterDim.x = 1;
+    a[1].val.clusterDim.y = b.attn_splits;
+    a[1].val.clusterDim.z = 1;
+    na = 2;
+  }
   cfg.attrs = a;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, attn::attn_kernel, mp[0], mp[1], mp[2], mp[3], mp[4], b.ap));
   count_launch();
   return SF_OK;
@@ -681,7 +728,7 @@ int enqueue_verify(Handle& h, Buffers& b, const sf_verify_cfg_t* cfg, cudaStream
       if ((rc = gemm::launch(b.dops[i], s, pdl))) return rc;
   }
   EmbedParams ep = embed_params(h, b, 0, h.temb);
-  if ((rc = launch_pdl(embed_kernel, dim3(b.M), dim3(256), 0, s, ep, with_draft && pdl))) return rc;
+  if ((rc = launch_pdl(embed_kernel, dim3(b.M / kEmbedTok), dim3(256), 0, s, ep, with_draft && pdl))) return rc;
   if ((rc = run_stack(h, b, s, pdl))) return rc;
   VerifyEpiParams vp{};
   const sf_ae_config_t& c = h.cfg;
@@ -724,7 +771,7 @@ int enqueue_denoise(Handle& h, Buffers& b, int n_steps, cudaStream_t s, bool pdl
   if ((rc = launch_pdl(status_init_kernel, dim3(1), dim3(256), 0, s, sp, false))) return rc;
   for (int i = 0; i < n_steps; ++i) {
     EmbedParams ep = embed_params(h, b, 1, h.temb_euler + (size_t)i * W);
-    if ((rc = launch_pdl(embed_kernel, dim3(b.M), dim3(256), 0, s, ep, pdl))) return rc;
+    if ((rc = launch_pdl(embed_kernel, dim3(b.M / kEmbedTok), dim3(256), 0, s, ep, pdl))) return rc;
     if ((rc = run_stack(h, b, s, pdl))) return rc;
     const int total = b.B * h.cfg.horizon * h.cfg.action_dim;
     EulerParams up{b.draft, b.vel, b.B, h.cfg.horizon, h.cfg.action_dim, b.env_rows, n_steps, i,
@@ -1061,7 +1108,7 @@ extern "C" int sf_ae_velocity(void* handle, int n_envs, int rows, const float* x
                                 cudaMemcpyDeviceToDevice, s));
   EmbedParams ep = embed_params(*h, *b, 1, h->temb);
   ep.draft = actions;
-  if ((rc = launch_pdl(embed_kernel, dim3(b->M), dim3(256), 0, s, ep, false))) return rc;
+  if ((rc = launch_pdl(embed_kernel, dim3(b->M / kEmbedTok), dim3(256), 0, s, ep, false))) return rc;
   if ((rc = run_stack(*h, *b, s, false))) return rc;
   GatherParams gp{b->vel, v_out, n_envs, rows, cf.horizon, cf.action_dim, T_of(*h), b->env_rows};
   gather_vel_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(gp);
