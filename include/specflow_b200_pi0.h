@@ -93,6 +93,12 @@ int sf_ae_flash_round(void* handle, int n_envs, const sf_verify_cfg_t* cfg, cons
  * per-kernel roofline. */
 int sf_ae_time_op(void* handle, int n_envs, int k, int op, int iters, void* stream);
 
+/* Per-kernel warm device times (us) of one eager verify round, launch order:
+ * embed, layers x [qkv, attention, o, gate/up, down], head, epilogue. */
+int sf_ae_profile_verify(void* handle, int n_envs, const sf_verify_cfg_t* cfg, const float* draft,
+                         const float* eps, const float* state, float* times_us, int max_times,
+                         int* n_times, void* stream);
+
 /* Batched full path (flowpolicy.py:273-292): `start` = A^0 [n_envs][H][D];
  * chunk_out [n_envs][H][D]; status [n_envs][2] = {first non-finite step or -1,
  * 1 if a velocity was non-finite}. */

@@ -91,6 +91,7 @@ SIGNATURES = {
     "sf_ae_flash_round": (_I, [_P, _I, ctypes.POINTER(SfVerifyCfg), _P, _P, _P, _P,
                                ctypes.POINTER(SfVerifyOut), _I, _P]),
     "sf_ae_time_op": (_I, [_P, _I, _I, _I, _I, _P]),
+    "sf_ae_profile_verify": (_I, [_P, _I, ctypes.POINTER(SfVerifyCfg), _P, _P, _P, _P, _I, _P, _P]),
     "sf_ae_velocity": (_I, [_P, _I, _I, _P, _P, _P, _P, _P]),
     "sf_fill_hash_uniform": (_I, [_P, _I, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64,
                                   ctypes.c_double, _P]),

@@ -281,6 +281,15 @@ __global__ void euler_rows_kernel(const EulerParams p) {
   if (threadIdx.x == 0) sm100::pdl_launch_dependents();
 }
 
+struct SleepParams {
+  long long ns;
+};
+
+__global__ void sleep_kernel(const SleepParams p) {
+  const long long t0 = clock64();
+  while (clock64() - t0 < p.ns * 2) __nanosleep(1000);
+}
+
 struct StatusParams {
   int* status;
   int B;
@@ -674,17 +683,35 @@ int launch_attn(const Buffers& b, int l, cudaStream_t s, bool pdl) {
   return SF_OK;
 }
 
+// Optional per-kernel event trace (sf_ae_profile_verify): an event is
+// recorded after every launch of an eager (non-graph) round.
+std::vector<cudaEvent_t>* g_trace = nullptr;
+void trace_mark(cudaStream_t s) {
+  if (!g_trace) return;
+  cudaEvent_t ev;
+  cudaEventCreate(&ev);
+  cudaEventRecord(ev, s);
+  g_trace->push_back(ev);
+}
+
 // The layer stack + head on the current X (used by verify and Euler).
 int run_stack(Handle& h, Buffers& b, cudaStream_t s, bool pdl) {
   int rc;
   for (int l = 0; l < h.cfg.layers; ++l) {
     if ((rc = gemm::launch(b.ops[4 * l + 0], s, pdl))) return rc;
+    trace_mark(s);
     if ((rc = launch_attn(b, l, s, pdl))) return rc;
+    trace_mark(s);
     if ((rc = gemm::launch(b.ops[4 * l + 1], s, pdl))) return rc;
+    trace_mark(s);
     if ((rc = gemm::launch(b.ops[4 * l + 2], s, pdl))) return rc;
+    trace_mark(s);
     if ((rc = gemm::launch(b.ops[4 * l + 3], s, pdl))) return rc;
+    trace_mark(s);
   }
-  return gemm::launch(b.ops[4 * h.cfg.layers], s, pdl);
+  rc = gemm::launch(b.ops[4 * h.cfg.layers], s, pdl);
+  trace_mark(s);
+  return rc;
 }
 
 EmbedParams embed_params(const Handle& h, const Buffers& b, int mode, const float* temb) {
@@ -729,6 +756,7 @@ int enqueue_verify(Handle& h, Buffers& b, const sf_verify_cfg_t* cfg, cudaStream
   }
   EmbedParams ep = embed_params(h, b, 0, h.temb);
   if ((rc = launch_pdl(embed_kernel, dim3(b.M / kEmbedTok), dim3(256), 0, s, ep, with_draft && pdl))) return rc;
+  trace_mark(s);
   if ((rc = run_stack(h, b, s, pdl))) return rc;
   VerifyEpiParams vp{};
   const sf_ae_config_t& c = h.cfg;
@@ -761,7 +789,9 @@ int enqueue_verify(Handle& h, Buffers& b, const sf_verify_cfg_t* cfg, cudaStream
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  return launch_pdl(verify_epi_kernel, dim3(b.B), dim3(256), smem, s, vp, pdl);
+  rc = launch_pdl(verify_epi_kernel, dim3(b.B), dim3(256), smem, s, vp, pdl);
+  trace_mark(s);
+  return rc;
 }
 
 int enqueue_denoise(Handle& h, Buffers& b, int n_steps, cudaStream_t s, bool pdl) {
@@ -1029,6 +1059,46 @@ extern "C" int sf_ae_time_op(void* handle, int n_envs, int k, int op, int iters,
   for (int i = 0; i < iters; ++i)
     if ((rc = sf::gemm::launch(b->ops[op], (cudaStream_t)stream, false))) return rc;
   return SF_OK;
+}
+
+// Per-kernel warm timings of one eager verify round (no graph, no PDL):
+// times_us[i] = device time between consecutive launches, in launch order
+// (embed, 18 x [qkv, attn, o, gate/up, down], head, epilogue).
+extern "C" int sf_ae_profile_verify(void* handle, int n_envs, const sf_verify_cfg_t* cfg,
+                                    const float* draft, const float* eps, const float* state,
+                                    float* times_us, int max_times, int* n_times, void* stream) {
+  auto* h = static_cast<Handle*>(handle);
+  SF_REQUIRE(h && cfg && draft && eps && state && times_us && n_times, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = check_verify_cfg(cfg, nullptr);
+  if (rc) return rc;
+  Buffers* b = get_buffers(*h, n_envs, cfg->k, 0, &rc);
+  if (!b) return rc;
+  if ((rc = ensure_temb(*h, cfg, s))) return rc;
+  const sf_ae_config_t& c = h->cfg;
+  const size_t hd = (size_t)n_envs * c.horizon * c.action_dim;
+  SF_CHECK_CUDA(cudaMemcpyAsync(b->draft, draft, hd * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(b->eps, eps, hd * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(b->state, state, (size_t)n_envs * c.state_dim * 4,
+                                cudaMemcpyDeviceToDevice, s));
+  std::vector<cudaEvent_t> evs;
+  // hold the stream while the host enqueues, so the trace measures the GPU
+  SleepParams sp{3000000};
+  if ((rc = launch_pdl(sleep_kernel, dim3(1), dim3(32), 0, s, sp, false))) return rc;
+  g_trace = &evs;
+  trace_mark(s);
+  rc = enqueue_verify(*h, *b, cfg, s, false, false);
+  g_trace = nullptr;
+  SF_CHECK_CUDA(cudaStreamSynchronize(s));
+  int n = 0;
+  for (size_t i = 1; i < evs.size() && n < max_times; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, evs[i - 1], evs[i]);
+    times_us[n++] = ms * 1e3f;
+  }
+  for (auto ev : evs) cudaEventDestroy(ev);
+  *n_times = n;
+  return rc;
 }
 
 extern "C" int sf_ae_denoise(void* handle, int n_envs, int num_steps, const float* start,
