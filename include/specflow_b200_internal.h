@@ -22,6 +22,12 @@ int sf_dbg_gemm(const void* A, int rows_a, const void* B, int rows_b, int K, int
                 int swap_ab, int epi_kind, void* out, int ld_out, int M_valid, int N_valid,
                 const float* ssq, int ssq_groups, int ssq_ld, float inv_width, void* stream);
 
+/* Average device time (us) of `iters` back-to-back launches of one planned
+ * GEMM (fp32 store epilogue), optionally with programmatic dependent launch. */
+int sf_dbg_gemm_time(const void* A, int rows_a, const void* B, int rows_b, int K, int bn,
+                     int splits, int swap_ab, void* out, int iters, int pdl, float* us,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -98,6 +98,7 @@ SIGNATURES = {
     # include/specflow_b200_internal.h (kernel unit-test hooks)
     "sf_dbg_gemm": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I, _P, _I, _I,
                          ctypes.c_float, _P]),
+    "sf_dbg_gemm_time": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P, _P]),
 }
 
 _lib = None

@@ -212,3 +212,39 @@ extern "C" int sf_dbg_gemm(const void* A, int rows_a, const void* B, int rows_b,
   SF_CHECK_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   return rc;
 }
+
+// Debug timing: plan once, launch `iters` times back to back between two
+// events (F32 epilogue); *us = average device time per launch.
+extern "C" int sf_dbg_gemm_time(const void* A, int rows_a, const void* B, int rows_b, int K, int bn,
+                                int splits, int swap_ab, void* out, int iters, int pdl, float* us,
+                                void* stream) {
+  using namespace sf::gemm;
+  EpiArgs e{};
+  e.kind = EPI_F32;
+  e.M = swap_ab ? rows_b : rows_a;
+  e.N = swap_ab ? rows_a : rows_b;
+  e.out_f32 = static_cast<float*>(out);
+  e.ld_f32 = e.N;
+  e.inv_width = 1.f;
+  e.eps = 1e-6f;
+  Op op;
+  int rc = plan(&op, A, rows_a, K, B, rows_b, K, K, bn, splits, swap_ab, e);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int i = 0; i < 3; ++i)
+    if ((rc = launch(op, s, pdl != 0))) return rc;
+  cudaEvent_t a, b;
+  SF_CHECK_CUDA(cudaEventCreate(&a));
+  SF_CHECK_CUDA(cudaEventCreate(&b));
+  SF_CHECK_CUDA(cudaEventRecord(a, s));
+  for (int i = 0; i < iters; ++i)
+    if ((rc = launch(op, s, pdl != 0))) return rc;
+  SF_CHECK_CUDA(cudaEventRecord(b, s));
+  SF_CHECK_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  *us = ms * 1e3f / (float)iters;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return SF_OK;
+}

@@ -1,0 +1,46 @@
+"""Sweep GEMM configurations with sf_dbg_gemm_time (device time per launch)."""
+
+import ctypes
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import torch
+
+from paper_2605_13778_b200 import _capi
+
+
+def t(M, N, K, bn, splits, swap, pdl=0, iters=50):
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    w = (torch.randn(N, K, device="cuda") * 0.05).bfloat16()
+    out = torch.empty(M, N, device="cuda")
+    a, ra, b, rb = (w, N, x, M) if swap else (x, M, w, N)
+    us = ctypes.c_float()
+    _capi.check(_capi.lib().sf_dbg_gemm_time(a.data_ptr(), ra, b.data_ptr(), rb, K, bn, splits,
+                                             int(swap), out.data_ptr(), iters, pdl, ctypes.byref(us),
+                                             torch.cuda.current_stream().cuda_stream), "time")
+    wbytes = N * K * 2
+    flops = 2.0 * M * N * K
+    print(f"M={M:6d} N={N:5d} K={K:5d} bn={bn:3d} S={splits:2d} swap={int(swap)} pdl={pdl}: "
+          f"{us.value:8.2f} us  {wbytes / us.value / 1e3:7.1f} GB/s(w)  {flops / us.value / 1e6:7.1f} TF/s")
+
+
+def main():
+    t(16, 128, 64, 16, 1, True)
+    t(208, 128, 64, 208, 1, True)
+    for s in (1, 2, 4, 8, 16):
+        t(208, 1024, 4096, 208, s, True)
+    for s in (1, 2, 4, 8):
+        t(208, 1024, 4096, 208, s, True, pdl=1)
+    for s in (1, 2, 4):
+        t(208, 8192, 1024, 208, s, True)
+    t(208, 2560, 1024, 208, 6, True)
+    t(13312, 8192, 1024, 256, 1, False)
+    t(13312, 2560, 1024, 256, 1, False)
+    t(13312, 1024, 4096, 256, 1, False)
+    t(106496, 8192, 1024, 256, 1, False, iters=5)
+
+
+if __name__ == "__main__":
+    main()
