@@ -87,7 +87,9 @@ int make_map(CUtensorMap* m, const void* ptr, int rows, int K, int ld, int box_r
 
 int auto_splits(int tiles, int num_kb) {
   int s = num_sms() / (tiles > 0 ? tiles : 1);
-  if (s > kMaxSplits) s = kMaxSplits;
+  // portable cluster sizes: 16-CTA clusters cannot all be co-resident (only
+  // ~7 fit on the GPCs at once, measured), which doubles the wave count
+  if (s > 8) s = 8;
   if (s > num_kb) s = num_kb;
   return s < 1 ? 1 : s;
 }

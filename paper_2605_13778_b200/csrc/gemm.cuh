@@ -393,14 +393,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (S == 1) {
     if (epi) {
       epi_bar();
-      for (int ch = g; ch < nchunks; ch += 2) {
-        uint32_t r[16];
-        sm100::tmem_ld16(t_lane + ch * 16, r);
+      for (int ch = g; ch < nchunks; ch += 4) {  // two TMEM loads in flight per wait
+        const bool two = ch + 2 < nchunks;
+        uint32_t r[2][16];
+        sm100::tmem_ld16(t_lane + ch * 16, r[0]);
+        if (two) sm100::tmem_ld16(t_lane + (ch + 2) * 16, r[1]);
         sm100::tmem_ld_wait();
-        float v[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-        epi_swap<KIND>(e, n, tile_b * p.bn + ch * 16, v, T.rs, T.red + q * 256, ch * 16);
+        for (int u = 0; u < 2; ++u) {
+          if (u == 1 && !two) break;
+          const int c = ch + 2 * u;
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[u][j]);
+          epi_swap<KIND>(e, n, tile_b * p.bn + c * 16, v, T.rs, T.red + q * 256, c * 16);
+        }
       }
       if (KIND == EPI_RESID) {
         epi_bar();
@@ -416,12 +423,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     // stage this split's partial in SMEM as [col][128 lanes] (reuses the ring)
     float* part = reinterpret_cast<float*>(smem);
     if (epi) {
-      for (int ch = g; ch < nchunks; ch += 2) {
-        uint32_t r[16];
-        sm100::tmem_ld16(t_lane + ch * 16, r);
+      for (int ch = g; ch < nchunks; ch += 4) {
+        const bool two = ch + 2 < nchunks;
+        uint32_t r[2][16];
+        sm100::tmem_ld16(t_lane + ch * 16, r[0]);
+        if (two) sm100::tmem_ld16(t_lane + (ch + 2) * 16, r[1]);
         sm100::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) part[(ch * 16 + j) * BM + lane_row] = __uint_as_float(r[j]);
+        for (int j = 0; j < 16; ++j) part[(ch * 16 + j) * BM + lane_row] = __uint_as_float(r[0][j]);
+        if (two) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            part[((ch + 2) * 16 + j) * BM + lane_row] = __uint_as_float(r[1][j]);
+        }
       }
     }
     cg::cluster_group cluster = cg::this_cluster();
@@ -537,18 +551,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::mbar_wait(&T.tmem_full[a], (it >> 1) & 1);
       sm100::tc_fence_after();
       const uint32_t t_lane = tmem + a * 256 + ((uint32_t)(q * 32) << 16);
-      float ssq[2] = {0.f, 0.f};
-      for (int ch = g; ch < p.bn / 16; ch += 2) {
-        uint32_t r[16];
-        sm100::tmem_ld16(t_lane + ch * 16, r);
+      float ssq0 = 0.f, ssq1 = 0.f;
+      const int nch = p.bn / 16;
+      for (int ch = g; ch < nch; ch += 4) {  // two TMEM loads in flight per wait
+        const bool two = ch + 2 < nch;
+        uint32_t r[2][16];
+        sm100::tmem_ld16(t_lane + ch * 16, r[0]);
+        if (two) sm100::tmem_ld16(t_lane + (ch + 2) * 16, r[1]);
         sm100::tmem_ld_wait();
-        float v[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-        float acc = 0.f;
-        epi_normal<KIND>(e, m, tb * p.bn + ch * 16, v, rs, acc);
-        ssq[(ch * 16) >> 7] += acc;
+        for (int u = 0; u < 2; ++u) {
+          if (u == 1 && !two) break;
+          const int c = ch + 2 * u;
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[u][j]);
+          float acc = 0.f;
+          epi_normal<KIND>(e, m, tb * p.bn + c * 16, v, rs, acc);
+          if (c * 16 < 128) ssq0 += acc;
+          else ssq1 += acc;
+        }
       }
+      float ssq[2] = {ssq0, ssq1};
       sm100::tc_fence_before();
       sm100::mbar_arrive(&T.tmem_empty[a]);
       if (KIND == EPI_RESID) {
