@@ -124,16 +124,15 @@ int plan(Op* op, const void* A, int rows_a, int lda, const void* B, int rows_b, 
   int stages = (int)(budget / stage_bytes);
   if (stages > max_stages) stages = max_stages;
   if (stages > 16) stages = 16;
-  const int per_cta_kb = swap_ab ? p.kb_per_split : p.num_kb;
-  if (swap_ab && stages > per_cta_kb) stages = per_cta_kb < 2 ? 2 : per_cta_kb;
+  // batch-1 (swap) CTAs keep a 2-stage ring (< 113 KB of SMEM) so two CTAs
+  // fit per SM: with PDL the next GEMM's CTAs become resident, initialise
+  // and prefetch their weights while this one is still running
+  if (swap_ab && stages > 2) stages = 2;
   SF_REQUIRE(stages >= 2, "GEMM tile does not fit in shared memory");
   p.stages = stages;
   size_t region = (size_t)stages * stage_bytes;
-  if (p.splits > 1) {
-    const size_t staging = (size_t)BM * bn * 4;  // fp32 partial [bn][128]
-    if (staging > region) region = staging;
-  }
   region = (region + 1023) & ~size_t(1023);
+  SF_REQUIRE(region >= 16 * BM * 4, "split-K staging needs at least one chunk");
   SF_REQUIRE(region + kTailBytes + 1024 <= 227 * 1024, "GEMM shared memory over budget");
   p.smem_stage_region = (uint32_t)region;
   op->smem = region + kTailBytes + 1024;

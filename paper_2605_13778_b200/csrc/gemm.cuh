@@ -39,9 +39,17 @@ namespace gemm {
 
 namespace cg = cooperative_groups;
 
+// MUFU tanh (max rel. error ~2^-11): its result feeds a bf16 rounding, so the
+// approximation is invisible at the stored precision.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
+  return 0.5f * x * (1.0f + tanh_fast(k0 * (x + k1 * x * x * x)));
 }
 
 __device__ __forceinline__ float row_scale(const EpiArgs& e, int m) {
@@ -74,7 +82,7 @@ __device__ __forceinline__ void epi_swap(const EpiArgs& e, int n, int m0, const 
       const int m = m0 + j;
       if (nvalid && m < e.M) {
         float o = v[j] * rs[c0 + j] + b;
-        if (KIND == EPI_TANH_BF16) o = tanhf(o);
+        if (KIND == EPI_TANH_BF16) o = tanh_fast(o);
         if (KIND == EPI_F32) e.out_f32[(size_t)m * e.ld_f32 + n] = o;
         else e.out_bf16[(size_t)m * e.ld_bf16 + n] = __float2bfloat16_rn(o);
       }
@@ -93,14 +101,26 @@ __device__ __forceinline__ void epi_swap(const EpiArgs& e, int n, int m0, const 
       const int second = n & 1;
       const int i = (n & 255) >> 1;
       const int dim = i + (second << 7);
+      // all 16 (cos, sin) loads in flight before any store (stores could
+      // alias the table in the compiler's view and would serialise them)
+      float2 csv[16];
+      {
+        int local = m0 % e.env_rows;
+        int t = local % e.seg_len;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          csv[j] = __ldg(e.rope + (e.pos0 + t) * 128 + i);
+          if (++local == e.env_rows) local = 0, t = -1;
+          if (++t == e.seg_len) t = 0;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const float x = v[j] * rs[c0 + j];
         const float partner = __shfl_xor_sync(0xffffffffu, x, 1);
         const int m = m0 + j;
         if (!nvalid || m >= e.M) continue;
-        const int pos = e.pos0 + ((m % e.env_rows) % e.seg_len);
-        const float2 cs = e.rope[pos * 128 + i];
+        const float2 cs = csv[j];
         const float a = second ? partner : x;
         const float b = second ? x : partner;
         const float y = second ? (b * cs.x + a * cs.y) : (a * cs.x - b * cs.y);
@@ -118,13 +138,17 @@ __device__ __forceinline__ void epi_swap(const EpiArgs& e, int n, int m0, const 
       dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
     }
   } else if (KIND == EPI_RESID) {
+    float xo[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)  // all loads before the read-modify-write stores
+      xo[j] = (nvalid && m0 + j < e.M) ? e.x[(size_t)(m0 + j) * e.N + n] : 0.f;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int m = m0 + j;
       float sq = 0.f;
       if (nvalid && m < e.M) {
         const size_t o = (size_t)m * e.N + n;
-        const float xn = e.x[o] + v[j];
+        const float xn = xo[j] + v[j];
         e.x[o] = xn;
         e.xb[o] = __float2bfloat16_rn(xn);
         sq = xn * xn;
@@ -147,7 +171,7 @@ __device__ __forceinline__ void epi_normal(const EpiArgs& e, int m, int n0, floa
     for (int j = 0; j < 16; ++j) {
       float o = v[j] * rs;
       if (e.bias && n0 + j < e.N) o += e.bias[n0 + j];
-      if (KIND == EPI_TANH_BF16) o = tanhf(o);
+      if (KIND == EPI_TANH_BF16) o = tanh_fast(o);
       v[j] = o;
     }
     if (KIND == EPI_F32) {
@@ -215,9 +239,12 @@ __device__ __forceinline__ void epi_normal(const EpiArgs& e, int m, int n0, floa
     float* xr = e.x + (size_t)m * e.N + n0;
     __nv_bfloat16* xbr = e.xb + (size_t)m * e.N + n0;
     uint32_t w[8];
+    float4 xin[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xin[j] = reinterpret_cast<const float4*>(xr)[j];
 #pragma unroll
     for (int j = 0; j < 16; j += 4) {
-      float4 x4 = *reinterpret_cast<float4*>(xr + j);
+      float4 x4 = xin[j / 4];
       x4.x += v[j];
       x4.y += v[j + 1];
       x4.z += v[j + 2];
@@ -420,53 +447,62 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // stage this split's partial in SMEM as [col][128 lanes] (reuses the ring)
+    // Split-K reduction over DSMEM. Partials are staged in SMEM as
+    // [col][128 lanes] through the (now idle) TMA ring, `cap` 16-column chunks
+    // per pass; chunk ch is reduced and finished by cluster rank ch % S.
     float* part = reinterpret_cast<float*>(smem);
-    if (epi) {
-      for (int ch = g; ch < nchunks; ch += 4) {
-        const bool two = ch + 2 < nchunks;
-        uint32_t r[2][16];
-        sm100::tmem_ld16(t_lane + ch * 16, r[0]);
-        if (two) sm100::tmem_ld16(t_lane + (ch + 2) * 16, r[1]);
-        sm100::tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) part[(ch * 16 + j) * BM + lane_row] = __uint_as_float(r[0][j]);
-        if (two) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            part[((ch + 2) * 16 + j) * BM + lane_row] = __uint_as_float(r[1][j]);
-        }
-      }
-    }
+    const int cap = (int)(p.smem_stage_region / (16 * BM * 4));
     cg::cluster_group cluster = cg::this_cluster();
-    cluster.sync();  // every split's partial is staged
-    if (epi) {
-      const float* peers[kMaxSplits];
-      for (int s = 0; s < S; ++s) peers[s] = cluster.map_shared_rank(part, s);
-      const int per = (nchunks + S - 1) / S;
-      const int ch0 = split * per, ch1 = min(nchunks, ch0 + per);
-      for (int ch = ch0 + g; ch < ch1; ch += 2) {
-        float v[16];
+    const float* peers[kMaxSplits];
+    for (int s = 0; s < S; ++s) peers[s] = cluster.map_shared_rank(part, s);
+    for (int base = 0; base < nchunks; base += cap) {
+      const int nb_ch = min(cap, nchunks - base);
+      if (epi) {
+        for (int lc = g; lc < nb_ch; lc += 4) {
+          const bool two = lc + 2 < nb_ch;
+          uint32_t r[2][16];
+          sm100::tmem_ld16(t_lane + (base + lc) * 16, r[0]);
+          if (two) sm100::tmem_ld16(t_lane + (base + lc + 2) * 16, r[1]);
+          sm100::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.f;
-        for (int s = 0; s < S; ++s) {  // fixed order: deterministic
-          const float* ps = peers[s] + ch * 16 * BM + lane_row;
+          for (int j = 0; j < 16; ++j) part[(lc * 16 + j) * BM + lane_row] = __uint_as_float(r[0][j]);
+          if (two) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] += ps[j * BM];
+            for (int j = 0; j < 16; ++j)
+              part[((lc + 2) * 16 + j) * BM + lane_row] = __uint_as_float(r[1][j]);
+          }
         }
-        epi_swap<KIND>(e, n, tile_b * p.bn + ch * 16, v, T.rs, T.red + q * 256, ch * 16);
       }
-      if (KIND == EPI_RESID) {
-        epi_bar();
-        for (int c = ch0 * 16 + threadIdx.x - 64; c < ch1 * 16; c += kEpiThreads) {
-          const int m = tile_b * p.bn + c;
-          if (m < e.M)
-            e.ssq_out[(size_t)tile_a * e.ssq_out_ld + m] =
-                ((T.red[c] + T.red[256 + c]) + T.red[512 + c]) + T.red[768 + c];
+      cluster.sync();  // every split's partial of this pass is staged
+      if (epi) {
+        // my chunks in this pass, split between the two warp groups
+        int k = 0;
+        for (int lc = 0; lc < nb_ch; ++lc) {
+          if ((base + lc) % S != split) continue;
+          if ((k++ & 1) != g) continue;
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = 0.f;
+          for (int s = 0; s < S; ++s) {  // fixed order: deterministic
+            const float* ps = peers[s] + lc * 16 * BM + lane_row;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] += ps[j * BM];
+          }
+          const int ch = base + lc;
+          epi_swap<KIND>(e, n, tile_b * p.bn + ch * 16, v, T.rs, T.red + q * 256, ch * 16);
         }
+      }
+      cluster.sync();  // peers may still read this pass's partial
+    }
+    if (KIND == EPI_RESID && epi) {
+      epi_bar();
+      for (int c = threadIdx.x - 64; c < p.bn; c += kEpiThreads) {
+        const int m = tile_b * p.bn + c;
+        if ((c >> 4) % S == split && m < e.M)
+          e.ssq_out[(size_t)tile_a * e.ssq_out_ld + m] =
+              ((T.red[c] + T.red[256 + c]) + T.red[512 + c]) + T.red[768 + c];
       }
     }
-    cluster.sync();  // peers may still read this CTA's partial
   }
   sm100::tc_fence_before();
   __syncthreads();
