@@ -209,6 +209,8 @@ def run_ours(args, rank, world, local):
 
     from paper_2605_13778_b200 import _capi
     from paper_2605_13778_b200.pi0 import PI0, ActionExpert
+    from paper_2605_13778_b200.sharding import (decision_counts, gather_counts, max_over_ranks,
+                                                shard_range)
     from paper_2605_13778_b200.verifier import VerifierConfig
 
     torch.cuda.set_device(local)
@@ -216,9 +218,11 @@ def run_ours(args, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     hbm_peak, tc_peak, tc_sust, peak_kind = peaks()
     cfg = PI0
-    E = args.envs // world
+    lo, hi = shard_range(args.envs, rank, world)
+    E = hi - lo
     assert E >= 1, "more GPUs than environments"
-    ae = ActionExpert(cfg, seed=0, n_envs=E, kv_seed=1 + rank)
+    # weights replicated per GPU; each rank holds only its envs' prefix KV
+    ae = ActionExpert(cfg, seed=0, n_envs=E, kv_seed=1, env_offset=lo)
     vcfg = VerifierConfig(timesteps=TAUS, delta=DELTA, gripper_window=WINDOW)
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
     dev = torch.device("cuda", local)
@@ -252,13 +256,12 @@ def run_ours(args, rank, world, local):
         b.record()
         b.synchronize()
     launches = _capi.launch_count() - launches0
-    ms = a.elapsed_time(b) / args.steps
+    ms = max_over_ranks(a.elapsed_time(b) / args.steps, dev)
+    # metrics gather after the timed region (the only data collective)
+    counts = gather_counts(decision_counts(outs[4])).tolist()
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
         dist.barrier()
-    value = args.envs / (ms / 1e3) if world > 1 else E / (ms / 1e3)
+    value = args.envs / (ms / 1e3)
 
     # ---------------- e2e through the public API with host buffers
     h_obs, h_eps = obs.cpu().pin_memory(), eps.cpu().pin_memory()
@@ -281,11 +284,7 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    e2e_ms = event_ms(e2e_step, args.steps)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(event_ms(e2e_step, args.steps), dev)
     h2d = sum(x.numel() * x.element_size() for x in (h_obs, h_eps, h_state, h_signs))
     d2h = h_branch.numel() * 4 + h_res.numel() * 4
 
@@ -319,7 +318,9 @@ def run_ours(args, rank, world, local):
                    "l2": "inputs larger than L2 (627 MB weights + 14.7 MB KV per env per step)",
                    "parallelism": f"envs sharded dp{world}, no hot-path collective"},
         "roofline": roofline,
-        "e2e": {"value": args.envs / (e2e_ms / 1e3) if world > 1 else E / (e2e_ms / 1e3),
+        "decisions": {"flash_accepted": counts[0], "flash_rejected_fallback": counts[1],
+                      "flash_phase_fallback": counts[2]},
+        "e2e": {"value": args.envs / (e2e_ms / 1e3),
                 "unit": "rounds/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": "ActionExpert.flash_batch"},
         "gpu_launches": int(launches),

@@ -137,7 +137,7 @@ class ActionExpert:
 
     def __init__(self, cfg: AEConfig = PI0, seed: int = 0, n_envs: int = 1, kv_seed: int = 1,
                  layout: ChannelLayout | None = None, std: float = 0.02,
-                 flags: int = SF_AE_GRAPH | SF_AE_PDL):
+                 flags: int = SF_AE_GRAPH | SF_AE_PDL, env_offset: int = 0):
         self.cfg = cfg
         self.horizon = cfg.horizon
         self.dim = cfg.action_dim
@@ -207,18 +207,19 @@ class ActionExpert:
                     "ae create")
         self._h = h
         self.n_envs = 0
-        self.set_prefix_pool(n_envs, kv_seed)
+        self.set_prefix_pool(n_envs, kv_seed, env_offset)
 
     # ---------------------------------------------------------- prefix KV
-    def set_prefix_pool(self, n_envs: int, kv_seed: int = 1):
-        """Random-init prefix KV for n_envs envs (stand-in for the VLM prefill)."""
+    def set_prefix_pool(self, n_envs: int, kv_seed: int = 1, env_offset: int = 0):
+        """Random-init prefix KV for envs [env_offset, env_offset + n_envs)
+        (stand-in for the VLM prefill; same values as oracle make_prefix_kv)."""
         cfg, dev = self.cfg, _device.device()
         L, P, hd = cfg.layers, cfg.prefix_len, cfg.head_dim
         self.k_prefix = torch.empty((L, n_envs, P, hd), dtype=torch.bfloat16, device=dev)
         self.vt_prefix = torch.empty((L, n_envs, hd, P), dtype=torch.bfloat16, device=dev)
         for e in range(n_envs):
             for l in range(L):
-                t = TID_KV_BASE + 2 * (e * L + l)
+                t = TID_KV_BASE + 2 * ((env_offset + e) * L + l)
                 _fill(self.k_prefix[l, e], kv_seed, t, 1.0)
                 _fill(self.vt_prefix[l, e], kv_seed, t + 1, 1.0)
         _capi.check(_capi.lib().sf_ae_set_prefix(self._h, self.k_prefix.data_ptr(),
