@@ -22,6 +22,11 @@ int sf_dbg_gemm(const void* A, int rows_a, const void* B, int rows_b, int K, int
                 int swap_ab, int epi_kind, void* out, int ld_out, int M_valid, int N_valid,
                 const float* ssq, int ssq_groups, int ssq_ld, float inv_width, void* stream);
 
+/* %globaltimer stamps (ns, 12 entries) of block (0,0,0) of one warm launch of
+ * a swap-AB split-K GEMM (see gemm.cu for the stamp points). */
+int sf_dbg_gemm_trace(const void* A, int rows_a, const void* B, int rows_b, int K, int bn,
+                      int splits, void* out, unsigned long long* stamps, void* stream);
+
 /* Average device time (us) of `iters` back-to-back launches of one planned
  * GEMM (fp32 store epilogue), optionally with programmatic dependent launch. */
 int sf_dbg_gemm_time(const void* A, int rows_a, const void* B, int rows_b, int K, int bn,

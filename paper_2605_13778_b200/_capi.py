@@ -99,6 +99,7 @@ SIGNATURES = {
     "sf_dbg_gemm": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I, _P, _I, _I,
                          ctypes.c_float, _P]),
     "sf_dbg_gemm_time": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P, _P]),
+    "sf_dbg_gemm_trace": (_I, [_P, _I, _P, _I, _I, _I, _I, _P, _P, _P]),
 }
 
 _lib = None

@@ -214,6 +214,40 @@ extern "C" int sf_dbg_gemm(const void* A, int rows_a, const void* B, int rows_b,
   return rc;
 }
 
+// Debug timeline: %globaltimer stamps (ns) of CTA (0,0,0) of one warm launch
+// of a swap GEMM: 0 entry, 1 prologue done, 2 producer issued all, 3 MMA
+// committed, 4 epilogue row scales ready, 5 accumulator ready, 6 partial
+// staged, 7 cluster sync, 8 reduce+epilogue done, 9 cluster sync, 10 epilogue
+// end, 11 TMEM freed. stamps[12] = host-visible copy (0 = not reached).
+extern "C" int sf_dbg_gemm_trace(const void* A, int rows_a, const void* B, int rows_b, int K,
+                                 int bn, int splits, void* out, unsigned long long* stamps,
+                                 void* stream) {
+  using namespace sf::gemm;
+  EpiArgs e{};
+  e.kind = EPI_F32;
+  e.M = rows_b;
+  e.N = rows_a;
+  e.out_f32 = static_cast<float*>(out);
+  e.ld_f32 = e.N;
+  e.inv_width = 1.f;
+  e.eps = 1e-6f;
+  Op op;
+  int rc = plan(&op, A, rows_a, K, B, rows_b, K, K, bn, splits, 1, e);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int i = 0; i < 3; ++i)
+    if ((rc = launch(op, s, false))) return rc;
+  unsigned long long* d = nullptr;
+  SF_CHECK_CUDA(cudaMalloc(&d, 16 * sizeof(unsigned long long)));
+  SF_CHECK_CUDA(cudaMemsetAsync(d, 0, 16 * sizeof(unsigned long long), s));
+  op.p.dbg = d;
+  rc = launch(op, s, false);
+  SF_CHECK_CUDA(cudaMemcpyAsync(stamps, d, 12 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  SF_CHECK_CUDA(cudaStreamSynchronize(s));
+  cudaFree(d);
+  return rc;
+}
+
 // Debug timing: plan once, launch `iters` times back to back between two
 // events (F32 epilogue); *us = average device time per launch.
 extern "C" int sf_dbg_gemm_time(const void* A, int rows_a, const void* B, int rows_b, int K, int bn,

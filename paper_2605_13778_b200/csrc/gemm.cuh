@@ -351,6 +351,14 @@ constexpr size_t kTailBytes = 8 * (2 * 16 + 4) + 16 + 4 * (256 + 4 * 256 + 2 * 2
 
 // -------------------------------------------------- batch-1: swap + cluster split-K
 
+__device__ __forceinline__ void stamp(const Params& p, int i) {
+  if (p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.dbg[i] = t;
+  }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_swap_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
@@ -366,6 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kb0 = split * p.kb_per_split;
   const int nkb = min(p.kb_per_split, p.num_kb - kb0);
   const int S = p.splits;
+  if (threadIdx.x == 0) stamp(p, 0);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -380,6 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *T.tmem_slot;
+  if (threadIdx.x == 0) stamp(p, 1);
 
   if (warp == 0) {
     if (sm100::elect_one()) {
@@ -388,12 +398,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       int kiter = 0;
       produce_tile(ring, &tma_a, &tma_b, 0, kAStageBytes, tile_a * BM, tile_b * p.bn, kb0, nkb,
                    kiter, true, sm100::policy_evict_first(), sm100::policy_evict_last());
+      stamp(p, 2);
     }
   } else if (warp == 1) {
     if (sm100::elect_one()) {
       int kiter = 0;
       mma_tile(ring, tmem, sm100::make_idesc_bf16(BM, p.bn), nkb, kiter);
       sm100::umma_commit(&T.tmem_full[0]);
+      stamp(p, 3);
     }
     __syncwarp();
   }
@@ -413,8 +425,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m = tile_b * p.bn + c;
       T.rs[c] = (KIND != EPI_RESID && KIND != EPI_TANH_BF16 && m < e.M) ? row_scale(e, m) : 1.f;
     }
+    if (threadIdx.x == 64) stamp(p, 4);
     sm100::mbar_wait(&T.tmem_full[0], 0);
     sm100::tc_fence_after();
+    if (threadIdx.x == 64) stamp(p, 5);
   }
   const int nchunks = p.bn / 16;
   if (S == 1) {
@@ -473,7 +487,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (threadIdx.x == 64 && base == 0) stamp(p, 6);
       cluster.sync();  // every split's partial of this pass is staged
+      if (threadIdx.x == 64 && base == 0) stamp(p, 7);
       if (epi) {
         // my chunks in this pass, split between the two warp groups
         int k = 0;
@@ -492,7 +508,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           epi_swap<KIND>(e, n, tile_b * p.bn + ch * 16, v, T.rs, T.red + q * 256, ch * 16);
         }
       }
+      if (threadIdx.x == 64 && base == 0) stamp(p, 8);
       cluster.sync();  // peers may still read this pass's partial
+      if (threadIdx.x == 64 && base == 0) stamp(p, 9);
     }
     if (KIND == EPI_RESID && epi) {
       epi_bar();
@@ -504,12 +522,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if (threadIdx.x == 64) stamp(p, 10);
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     sm100::tc_fence_after();
     sm100::tmem_dealloc<256>(tmem);
   }
+  if (threadIdx.x == 32) stamp(p, 11);
 }
 
 // ------------------------------------------------------ batched: persistent

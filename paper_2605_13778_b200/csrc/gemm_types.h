@@ -63,6 +63,7 @@ struct Params {
   int swap_ab;
   int tiles_a, tiles_b, total_tiles;
   uint32_t smem_stage_region;  // bytes reserved for the TMA ring (>= split-K staging)
+  unsigned long long* dbg;     // optional %globaltimer stamps of CTA (0,0,0) (null: off)
   EpiArgs e;
 };
 

@@ -44,3 +44,25 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def trace(M, N, K, bn, splits):
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    w = (torch.randn(N, K, device="cuda") * 0.05).bfloat16()
+    out = torch.empty(M, N, device="cuda")
+    st = (ctypes.c_ulonglong * 12)()
+    _capi.check(_capi.lib().sf_dbg_gemm_trace(w.data_ptr(), N, x.data_ptr(), M, K, bn, splits,
+                                              out.data_ptr(), st,
+                                              torch.cuda.current_stream().cuda_stream), "trace")
+    t0 = st[0]
+    names = ["entry", "prologue", "producer_done", "mma_committed", "rs_ready", "acc_ready",
+             "staged", "csync1", "reduced", "csync2", "epi_end", "tmem_freed"]
+    print(f"trace M={M} N={N} K={K} S={splits}: " +
+          " ".join(f"{n}={(v - t0) / 1e3:.2f}" if v else f"{n}=-" for n, v in zip(names, st)))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace":
+    trace(208, 1024, 4096, 208, 8)
+    trace(208, 8192, 1024, 208, 2)
+    trace(208, 2560, 1024, 208, 6)
+    trace(16, 128, 64, 16, 1)
