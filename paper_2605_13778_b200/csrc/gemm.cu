@@ -124,15 +124,13 @@ int plan(Op* op, const void* A, int rows_a, int lda, const void* B, int rows_b, 
   int stages = (int)(budget / stage_bytes);
   if (stages > max_stages) stages = max_stages;
   if (stages > 16) stages = 16;
-  // batch-1 (swap) CTAs keep a 2-stage ring (< 113 KB of SMEM) so two CTAs
-  // fit per SM: with PDL the next GEMM's CTAs become resident, initialise
-  // and prefetch their weights while this one is still running
-  if (swap_ab && stages > 2) stages = 2;
+  if (swap_ab && stages > p.kb_per_split) stages = p.kb_per_split < 2 ? 2 : p.kb_per_split;
   SF_REQUIRE(stages >= 2, "GEMM tile does not fit in shared memory");
   p.stages = stages;
   size_t region = (size_t)stages * stage_bytes;
   region = (region + 1023) & ~size_t(1023);
-  SF_REQUIRE(region >= 16 * BM * 4, "split-K staging needs at least one chunk");
+  // split-K partial workspace (caller provides op->p.ws of op->ws_bytes)
+  op->ws_bytes = p.splits > 1 ? (size_t)p.splits * p.total_tiles * (bn / 16) * BM * 16 * 4 : 0;
   SF_REQUIRE(region + kTailBytes + 1024 <= 227 * 1024, "GEMM shared memory over budget");
   p.smem_stage_region = (uint32_t)region;
   op->smem = region + kTailBytes + 1024;
@@ -151,6 +149,7 @@ int plan(Op* op, const void* A, int rows_a, int lda, const void* B, int rows_b, 
 }
 
 int launch(const Op& op, cudaStream_t stream, bool pdl) {
+  SF_REQUIRE(op.ws_bytes == 0 || op.p.ws, "split-K GEMM launched without a workspace");
   static bool attr_done[2 * EPI_KINDS] = {};
   const int slot = op.p.e.kind * 2 + (op.p.swap_ab ? 1 : 0);
   KernelFn fn = reinterpret_cast<KernelFn>(op.fn);
@@ -186,6 +185,23 @@ int launch(const Op& op, cudaStream_t stream, bool pdl) {
 }  // namespace gemm
 }  // namespace sf
 
+namespace {
+// Debug entry points own a temporary split-K workspace.
+struct DbgWs {
+  float* p = nullptr;
+  ~DbgWs() {
+    if (p) cudaFree(p);
+  }
+};
+int attach_ws(sf::gemm::Op& op, DbgWs& w) {
+  if (op.ws_bytes) {
+    SF_CHECK_CUDA(cudaMalloc(&w.p, op.ws_bytes));
+    op.p.ws = w.p;
+  }
+  return SF_OK;
+}
+}  // namespace
+
 // Debug entry: D = A @ B^T with an F32 / BF16 epilogue (optional RMS row
 // scale from ssq partials). Synchronises `stream`; not for the hot path.
 extern "C" int sf_dbg_gemm(const void* A, int rows_a, const void* B, int rows_b, int K, int bn,
@@ -209,6 +225,8 @@ extern "C" int sf_dbg_gemm(const void* A, int rows_a, const void* B, int rows_b,
   e.eps = 1e-6f;
   Op op;
   int rc = plan(&op, A, rows_a, K, B, rows_b, K, K, bn, splits, swap_ab, e);
+  DbgWs dws;
+  if (!rc) rc = attach_ws(op, dws);
   if (!rc) rc = launch(op, (cudaStream_t)stream, false);
   SF_CHECK_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   return rc;
@@ -233,6 +251,8 @@ extern "C" int sf_dbg_gemm_trace(const void* A, int rows_a, const void* B, int r
   e.eps = 1e-6f;
   Op op;
   int rc = plan(&op, A, rows_a, K, B, rows_b, K, K, bn, splits, 1, e);
+  DbgWs dws;
+  if (!rc) rc = attach_ws(op, dws);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   for (int i = 0; i < 3; ++i)
@@ -264,6 +284,8 @@ extern "C" int sf_dbg_gemm_time(const void* A, int rows_a, const void* B, int ro
   e.eps = 1e-6f;
   Op op;
   int rc = plan(&op, A, rows_a, K, B, rows_b, K, K, bn, splits, swap_ab, e);
+  DbgWs dws;
+  if (!rc) rc = attach_ws(op, dws);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   for (int i = 0; i < 3; ++i)

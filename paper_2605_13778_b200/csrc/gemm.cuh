@@ -461,57 +461,63 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // Split-K reduction over DSMEM. Partials are staged in SMEM as
-    // [col][128 lanes] through the (now idle) TMA ring, `cap` 16-column chunks
-    // per pass; chunk ch is reduced and finished by cluster rank ch % S.
-    float* part = reinterpret_cast<float*>(smem);
-    const int cap = (int)(p.smem_stage_region / (16 * BM * 4));
-    cg::cluster_group cluster = cg::this_cluster();
-    const float* peers[kMaxSplits];
-    for (int s = 0; s < S; ++s) peers[s] = cluster.map_shared_rank(part, s);
-    for (int base = 0; base < nchunks; base += cap) {
-      const int nb_ch = min(cap, nchunks - base);
-      if (epi) {
-        for (int lc = g; lc < nb_ch; lc += 4) {
-          const bool two = lc + 2 < nb_ch;
-          uint32_t r[2][16];
-          sm100::tmem_ld16(t_lane + (base + lc) * 16, r[0]);
-          if (two) sm100::tmem_ld16(t_lane + (base + lc + 2) * 16, r[1]);
-          sm100::tmem_ld_wait();
+    // Split-K reduction through L2: every split writes its partial as
+    // [chunk][128 lanes][16 cols] (each thread 64 contiguous bytes), one
+    // cluster barrier, then chunk ch is reduced (fixed split order, so the
+    // result is deterministic) and finished by cluster rank ch % S, reading
+    // the S partials with 16-byte L2 loads. All S CTAs reduce in parallel.
+    const int tile_id = tile_a * p.tiles_b + tile_b;
+    const size_t slab = (size_t)nchunks * BM * 16;  // floats per (split, tile)
+    float* mine = p.ws + ((size_t)split * p.total_tiles + tile_id) * slab;
+    if (epi) {
+      for (int ch = g; ch < nchunks; ch += 4) {
+        const bool two = ch + 2 < nchunks;
+        uint32_t r[2][16];
+        sm100::tmem_ld16(t_lane + ch * 16, r[0]);
+        if (two) sm100::tmem_ld16(t_lane + (ch + 2) * 16, r[1]);
+        sm100::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) part[(lc * 16 + j) * BM + lane_row] = __uint_as_float(r[0][j]);
-          if (two) {
+        for (int u = 0; u < 2; ++u) {
+          if (u == 1 && !two) break;
+          float4* dst = reinterpret_cast<float4*>(mine + ((size_t)(ch + 2 * u) * BM + lane_row) * 16);
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              part[((lc + 2) * 16 + j) * BM + lane_row] = __uint_as_float(r[1][j]);
-          }
+          for (int j = 0; j < 4; ++j)
+            dst[j] = make_float4(__uint_as_float(r[u][4 * j]), __uint_as_float(r[u][4 * j + 1]),
+                                 __uint_as_float(r[u][4 * j + 2]), __uint_as_float(r[u][4 * j + 3]));
         }
       }
-      if (threadIdx.x == 64 && base == 0) stamp(p, 6);
-      cluster.sync();  // every split's partial of this pass is staged
-      if (threadIdx.x == 64 && base == 0) stamp(p, 7);
-      if (epi) {
-        // my chunks in this pass, split between the two warp groups
-        int k = 0;
-        for (int lc = 0; lc < nb_ch; ++lc) {
-          if ((base + lc) % S != split) continue;
-          if ((k++ & 1) != g) continue;
-          float v[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = 0.f;
-          for (int s = 0; s < S; ++s) {  // fixed order: deterministic
-            const float* ps = peers[s] + lc * 16 * BM + lane_row;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] += ps[j * BM];
-          }
-          const int ch = base + lc;
-          epi_swap<KIND>(e, n, tile_b * p.bn + ch * 16, v, T.rs, T.red + q * 256, ch * 16);
-        }
-      }
-      if (threadIdx.x == 64 && base == 0) stamp(p, 8);
-      cluster.sync();  // peers may still read this pass's partial
-      if (threadIdx.x == 64 && base == 0) stamp(p, 9);
+      __threadfence();
     }
+    if (threadIdx.x == 64) stamp(p, 6);
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();  // every split's partial is in L2
+    if (threadIdx.x == 64) stamp(p, 7);
+    if (epi) {
+      int k = 0;
+      for (int ch = 0; ch < nchunks; ++ch) {
+        if (ch % S != split) continue;
+        if ((k++ & 1) != g) continue;
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        for (int s = 0; s < S; ++s) {  // fixed order: deterministic
+          const float4* ps = reinterpret_cast<const float4*>(
+              p.ws + ((size_t)s * p.total_tiles + tile_id) * slab + ((size_t)ch * BM + lane_row) * 16);
+          float4 a[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) a[j] = __ldcg(ps + j);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            v[4 * j] += a[j].x;
+            v[4 * j + 1] += a[j].y;
+            v[4 * j + 2] += a[j].z;
+            v[4 * j + 3] += a[j].w;
+          }
+        }
+        epi_swap<KIND>(e, n, tile_b * p.bn + ch * 16, v, T.rs, T.red + q * 256, ch * 16);
+      }
+    }
+    if (threadIdx.x == 64) stamp(p, 8);
     if (KIND == EPI_RESID && epi) {
       epi_bar();
       for (int c = threadIdx.x - 64; c < p.bn; c += kEpiThreads) {

@@ -17,6 +17,7 @@ struct Op {
   dim3 grid;
   int cluster = 1;   // split-K cluster size (swap kernel)
   size_t smem = 0;
+  size_t ws_bytes = 0;  // split-K workspace the caller must attach as p.ws
   void* fn = nullptr;  // specialised kernel
 };
 

@@ -613,6 +613,21 @@ int build(Handle& h, Buffers& b, int B, int K) {
         return rc;
     }
   }
+  // --- one split-K workspace shared by every GEMM (kernels are stream-ordered;
+  // with PDL a GEMM only touches it after griddepcontrol.wait)
+  {
+    size_t need = 0;
+    for (auto& op : b.ops) need = op.ws_bytes > need ? op.ws_bytes : need;
+    if (b.has_draft)
+      for (auto& op : b.dops) need = op.ws_bytes > need ? op.ws_bytes : need;
+    b.ws_bytes = need;
+    if (need) {
+      if ((rc = dalloc(&b.ws, need / sizeof(float)))) return rc;
+      for (auto& op : b.ops) op.p.ws = b.ws;
+      if (b.has_draft)
+        for (auto& op : b.dops) op.p.ws = b.ws;
+    }
+  }
   // --- attention plans (per layer: 5 tensor maps)
   attn::Params& ap = b.ap;
   ap.M = b.M;
