@@ -486,9 +486,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  __uint_as_float(r[u][4 * j + 2]), __uint_as_float(r[u][4 * j + 3]));
         }
       }
-      __threadfence();
     }
     if (threadIdx.x == 64) stamp(p, 6);
+    // barrier.cluster arrive.release / wait.acquire orders the partial stores
+    // before the peers' loads (cluster scope covers global memory)
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();  // every split's partial is in L2
     if (threadIdx.x == 64) stamp(p, 7);
@@ -500,18 +501,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = 0.f;
-        for (int s = 0; s < S; ++s) {  // fixed order: deterministic
-          const float4* ps = reinterpret_cast<const float4*>(
-              p.ws + ((size_t)s * p.total_tiles + tile_id) * slab + ((size_t)ch * BM + lane_row) * 16);
-          float4 a[4];
+        const float* base = p.ws + (size_t)tile_id * slab + ((size_t)ch * BM + lane_row) * 16;
+        const size_t sstride = (size_t)p.total_tiles * slab;
+        for (int s0 = 0; s0 < S; s0 += 4) {  // 4 splits' loads in flight, then fixed-order adds
+          float4 a[4][4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) a[j] = __ldcg(ps + j);
+          for (int u = 0; u < 4; ++u) {
+            if (s0 + u < S) {
+              const float4* ps = reinterpret_cast<const float4*>(base + (size_t)(s0 + u) * sstride);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            v[4 * j] += a[j].x;
-            v[4 * j + 1] += a[j].y;
-            v[4 * j + 2] += a[j].z;
-            v[4 * j + 3] += a[j].w;
+              for (int j = 0; j < 4; ++j) a[u][j] = __ldcg(ps + j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (s0 + u < S) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                v[4 * j] += a[u][j].x;
+                v[4 * j + 1] += a[u][j].y;
+                v[4 * j + 2] += a[u][j].z;
+                v[4 * j + 3] += a[u][j].w;
+              }
+            }
           }
         }
         epi_swap<KIND>(e, n, tile_b * p.bn + ch * 16, v, T.rs, T.red + q * 256, ch * 16);
