@@ -359,6 +359,59 @@ __device__ __forceinline__ void stamp(const Params& p, int i) {
   }
 }
 
+// Split-K finish for the chunks cluster rank `split` owns (ch % S == split,
+// alternating between the two column groups g): G chunks at a time with up to
+// 4 split partials per chunk in flight (16 float4 loads per thread),
+// summed in fixed split order so the result is deterministic.
+template <int KIND, int G>
+__device__ __forceinline__ void reduce_chunks(const EpiArgs& e, const Params& p, const float* base,
+                                              size_t sstride, int split, int g, int n, int tile_b,
+                                              int nchunks, const float* rs, float* red) {
+  constexpr int SB = 4 / G;  // splits per load batch
+  const int S = p.splits;
+  // owned chunks: split + k * S for k = g, g + 2, ...
+  const int owned = (nchunks - split + S - 1) / S;
+  const int cnt = (owned - g + 1) / 2;
+#define mine(i) (split + (g + 2 * (i)) * S)
+  for (int i0 = 0; i0 < cnt; i0 += G) {
+    float v[G][16];
+#pragma unroll
+    for (int c = 0; c < G; ++c)
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[c][j] = 0.f;
+    for (int s0 = 0; s0 < S; s0 += SB) {
+      float4 a[G][SB][4];
+#pragma unroll
+      for (int c = 0; c < G; ++c)
+#pragma unroll
+        for (int u = 0; u < SB; ++u)
+          if (i0 + c < cnt && s0 + u < S) {
+            const float4* ps = reinterpret_cast<const float4*>(base + (size_t)(s0 + u) * sstride +
+                                                               (size_t)mine(i0 + c) * BM * 16);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) a[c][u][j] = __ldcg(ps + j * BM);
+          }
+#pragma unroll
+      for (int c = 0; c < G; ++c)
+#pragma unroll
+        for (int u = 0; u < SB; ++u)
+          if (i0 + c < cnt && s0 + u < S) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              v[c][4 * j] += a[c][u][j].x;
+              v[c][4 * j + 1] += a[c][u][j].y;
+              v[c][4 * j + 2] += a[c][u][j].z;
+              v[c][4 * j + 3] += a[c][u][j].w;
+            }
+          }
+    }
+#pragma unroll
+    for (int c = 0; c < G; ++c)
+      if (i0 + c < cnt) epi_swap<KIND>(e, n, tile_b * p.bn + mine(i0 + c) * 16, v[c], rs, red, mine(i0 + c) * 16);
+  }
+#undef mine
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_swap_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
@@ -462,7 +515,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // Split-K reduction through L2: every split writes its partial as
-    // [chunk][128 lanes][16 cols] (each thread 64 contiguous bytes), one
+    // [chunk][4 col quads][128 lanes][4 cols] (each warp store is 512
+    // contiguous bytes), one
     // cluster barrier, then chunk ch is reduced (fixed split order, so the
     // result is deterministic) and finished by cluster rank ch % S, reading
     // the S partials with 16-byte L2 loads. All S CTAs reduce in parallel.
@@ -470,20 +524,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const size_t slab = (size_t)nchunks * BM * 16;  // floats per (split, tile)
     float* mine = p.ws + ((size_t)split * p.total_tiles + tile_id) * slab;
     if (epi) {
-      for (int ch = g; ch < nchunks; ch += 4) {
-        const bool two = ch + 2 < nchunks;
-        uint32_t r[2][16];
-        sm100::tmem_ld16(t_lane + ch * 16, r[0]);
-        if (two) sm100::tmem_ld16(t_lane + (ch + 2) * 16, r[1]);
+      for (int ch = g; ch < nchunks; ch += 8) {  // four TMEM loads in flight per wait
+        uint32_t r[4][16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (ch + 2 * u < nchunks) sm100::tmem_ld16(t_lane + (ch + 2 * u) * 16, r[u]);
         sm100::tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (u == 1 && !two) break;
-          float4* dst = reinterpret_cast<float4*>(mine + ((size_t)(ch + 2 * u) * BM + lane_row) * 16);
+        for (int u = 0; u < 4; ++u) {
+          if (ch + 2 * u >= nchunks) break;
+          float4* dst = reinterpret_cast<float4*>(mine + (size_t)(ch + 2 * u) * BM * 16) + lane_row;
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            dst[j] = make_float4(__uint_as_float(r[u][4 * j]), __uint_as_float(r[u][4 * j + 1]),
-                                 __uint_as_float(r[u][4 * j + 2]), __uint_as_float(r[u][4 * j + 3]));
+            dst[j * BM] = make_float4(__uint_as_float(r[u][4 * j]), __uint_as_float(r[u][4 * j + 1]),
+                                      __uint_as_float(r[u][4 * j + 2]), __uint_as_float(r[u][4 * j + 3]));
         }
       }
     }
@@ -494,40 +548,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     cluster.sync();  // every split's partial is in L2
     if (threadIdx.x == 64) stamp(p, 7);
     if (epi) {
-      int k = 0;
-      for (int ch = 0; ch < nchunks; ++ch) {
-        if (ch % S != split) continue;
-        if ((k++ & 1) != g) continue;
-        float v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.f;
-        const float* base = p.ws + (size_t)tile_id * slab + ((size_t)ch * BM + lane_row) * 16;
-        const size_t sstride = (size_t)p.total_tiles * slab;
-        for (int s0 = 0; s0 < S; s0 += 4) {  // 4 splits' loads in flight, then fixed-order adds
-          float4 a[4][4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (s0 + u < S) {
-              const float4* ps = reinterpret_cast<const float4*>(base + (size_t)(s0 + u) * sstride);
-#pragma unroll
-              for (int j = 0; j < 4; ++j) a[u][j] = __ldcg(ps + j);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (s0 + u < S) {
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                v[4 * j] += a[u][j].x;
-                v[4 * j + 1] += a[u][j].y;
-                v[4 * j + 2] += a[u][j].z;
-                v[4 * j + 3] += a[u][j].w;
-              }
-            }
-          }
-        }
-        epi_swap<KIND>(e, n, tile_b * p.bn + ch * 16, v, T.rs, T.red + q * 256, ch * 16);
-      }
+      const float* base = p.ws + (size_t)tile_id * slab + lane_row * 4;
+      const size_t sstride = (size_t)p.total_tiles * slab;
+      if (S <= 2)
+        reduce_chunks<KIND, 2>(e, p, base, sstride, split, g, n, tile_b, nchunks, T.rs, T.red + q * 256);
+      else
+        reduce_chunks<KIND, 1>(e, p, base, sstride, split, g, n, tile_b, nchunks, T.rs, T.red + q * 256);
     }
     if (threadIdx.x == 64) stamp(p, 8);
     if (KIND == EPI_RESID && epi) {

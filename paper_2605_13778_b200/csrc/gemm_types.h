@@ -64,7 +64,7 @@ struct Params {
   int tiles_a, tiles_b, total_tiles;
   uint32_t smem_stage_region;  // bytes reserved for the TMA ring (>= split-K staging)
   unsigned long long* dbg;     // optional %globaltimer stamps of CTA (0,0,0) (null: off)
-  float* ws;                   // split-K partials [split][tile][chunk][128][16] (swap, S > 1)
+  float* ws;                   // split-K partials [split][tile][chunk][4][128][4] (swap, S > 1)
   EpiArgs e;
 };
 
