@@ -63,6 +63,9 @@ typedef struct {
   const void* draft_b[3];
 } sf_ae_weights_t;
 
+/* The weight pointers are borrowed (device memory owned by the caller) and must
+ * stay valid and unchanged for the handle's lifetime; the embedding weights
+ * a_w / s_w are additionally copied once, transposed, at create time. */
 int sf_ae_create(const sf_ae_config_t* cfg, const sf_ae_weights_t* weights, void** handle);
 int sf_ae_destroy(void* handle);
 

@@ -61,6 +61,37 @@ struct Params {
   int* counters;       // [tiles]
 };
 
+#ifdef SF_TRACE
+#define ATT_STAMP(i)                                                     \
+  do {                                                                   \
+    unsigned long long _t;                                               \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));               \
+    stamps[i] = _t;                                                      \
+  } while (0)
+#else
+#define ATT_STAMP(i) \
+  do {               \
+  } while (0)
+#endif
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                            uint32_t d, uint32_t bar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+      "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "f"(a), "f"(b), "r"(bar)
+               : "memory");
+}
+
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -96,6 +127,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* pv_done = bars + 10;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  __shared__ unsigned long long stamps[16];
+  (void)stamps;
+  if (threadIdx.x == 0) ATT_STAMP(0);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x, split = blockIdx.y;
@@ -127,6 +161,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) ATT_STAMP(1);
+  float m_fin = -INFINITY, l_fin = 0.f;  // softmax rows' final (m, l) for the split-KV merge
 
   if (warp == 0) {
     if (sm100::elect_one()) {
@@ -174,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t q_addr = sm100::smem_u32(sQ);
       const uint32_t p_addr = sm100::smem_u32(sP);
       sm100::mbar_wait(q_full, 0);
+      ATT_STAMP(2);
       auto issue_pv = [&](int i) {
         sm100::mbar_wait(p_full, i & 1);
         sm100::tc_fence_after();
@@ -202,6 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (i >= 1) issue_pv(i - 1);
       }
       if (nb > 0) issue_pv(nb - 1);
+      ATT_STAMP(3);
     }
     __syncwarp();
   } else {
@@ -311,6 +349,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::mbar_wait(pv_done, (nb - 1) & 1);
       sm100::tc_fence_after();
     }
+    if (r == 0) ATT_STAMP(4);
+    m_fin = m_used;
+    l_fin = l_sum;
     if (p.splits == 1) {
       const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
       __nv_bfloat16* dst = p.out + (size_t)tok * (kHeads * HD) + head * HD;
@@ -331,58 +372,114 @@ __global__ void __launch_bounds__(kThreads, 1)
           d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
         }
       }
-    } else {
-      // stage the unnormalised partial O (row-major, padded stride: conflict
-      // free) + (m, l) in this CTA's SMEM; the Q/KV region is free now
-      float* part = reinterpret_cast<float*>(sQ);
-      for (int c0 = 0; c0 < HD; c0 += 16) {
-        uint32_t o[16];
-        sm100::tmem_ld16(t_lane + 128 + c0, o);
-        sm100::tmem_ld_wait();
-#pragma unroll
-        for (int k = 0; k < 16; ++k) part[r * kPartStride + c0 + k] = __uint_as_float(o[k]);
-      }
-      float* ml = reinterpret_cast<float*>(sP);
-      ml[r] = m_used;
-      ml[BQ + r] = l_sum;
     }
   }
   if (p.splits > 1) {
-    // split-KV merge over DSMEM: the splits of a tile form one cluster; CTA
-    // `split` merges rows [split*rows, (split+1)*rows) in a fixed split order
+    // Split-KV merge through L2: every split writes its unnormalised partial
+    // O as [HD/4 quads][128 rows] float4 (each warp store is 512 contiguous
+    // bytes) plus (m, l) per row; after one cluster barrier (release/acquire
+    // at cluster scope orders the global stores) cluster rank s merges rows
+    // [s*rows, (s+1)*rows) in a fixed split order (deterministic).
     cg::cluster_group cluster = cg::this_cluster();
-    cluster.sync();
+    const int S = p.splits;
+    const int rows = (BQ + S - 1) / S;
+    const int my_r0 = split * rows;
+    const int my_nr = max(0, min(BQ, my_r0 + rows) - my_r0);
+    const size_t part_floats = (size_t)HD * BQ;
+    float4* ws_o = reinterpret_cast<float4*>(p.ws);  // [(tile*S + s)][HD/4][BQ]
+    float2* ws_ml = reinterpret_cast<float2*>(p.ws + (size_t)p.tiles * S * part_floats);
     if (warp >= 2) {
-      const int t = threadIdx.x - 64;  // 0..127: owns columns 2t, 2t+1
-      const int rows = (BQ + p.splits - 1) / p.splits;
-      const int r0 = split * rows, r1 = min(BQ, r0 + rows);
-      const float* parts[kMaxSplitsKV];
-      const float* mls[kMaxSplitsKV];
-      for (int s = 0; s < p.splits; ++s) {
-        parts[s] = cluster.map_shared_rank(reinterpret_cast<float*>(sQ), s);
-        mls[s] = cluster.map_shared_rank(reinterpret_cast<float*>(sP), s);
+      const int q = warp & 3;
+      const int r = q * 32 + lane;
+      const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
+      float4* dst = ws_o + (size_t)(tile * S + split) * (HD / 4) * BQ + r;
+      ws_ml[(size_t)(tile * S + split) * BQ + r] = make_float2(m_fin, l_fin);
+#pragma unroll 1
+      for (int c0 = 0; c0 < HD; c0 += 64) {
+        uint32_t o[4][16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sm100::tmem_ld16(t_lane + 128 + c0 + 16 * u, o[u]);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int k = 0; k < 16; k += 4)
+            __stcg(dst + (size_t)((c0 + 16 * u + k) >> 2) * BQ,
+                   make_float4(__uint_as_float(o[u][k]), __uint_as_float(o[u][k + 1]),
+                               __uint_as_float(o[u][k + 2]), __uint_as_float(o[u][k + 3])));
       }
-      for (int row = r0; row < r1; ++row) {
-        const int tok = m0 + (row >> 3), head = row & 7;
-        float mx = -INFINITY;
-        for (int s = 0; s < p.splits; ++s) mx = fmaxf(mx, mls[s][row]);
-        float L = 0.f, a0 = 0.f, a1 = 0.f;
-        for (int s = 0; s < p.splits; ++s) {
-          const float ms = mls[s][row];
-          const float wgt = ms > -INFINITY ? exp2f(ms - mx) : 0.f;
-          L += wgt * mls[s][BQ + row];
-          const float2 o = *reinterpret_cast<const float2*>(parts[s] + row * kPartStride + 2 * t);
-          a0 += wgt * o.x;
-          a1 += wgt * o.y;
+    }
+    if (threadIdx.x == 64) ATT_STAMP(5);
+    cluster.sync();
+    if (threadIdx.x == 64) ATT_STAMP(6);
+    // merge weights: wgt[row][s] = 2^(m_s - max_s m_s), inv[row] = 1 / sum_s wgt l_s
+    float* wgt = reinterpret_cast<float*>(sP);  // [rows][S]
+    float* inv = wgt + BQ * kMaxSplitsKV;       // [rows]
+    if (threadIdx.x < my_nr) {
+      const int row = my_r0 + threadIdx.x;
+      float2 ml[kMaxSplitsKV];
+#pragma unroll
+      for (int s2 = 0; s2 < kMaxSplitsKV; ++s2)
+        if (s2 < S) ml[s2] = __ldcg(ws_ml + (size_t)(tile * S + s2) * BQ + row);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int s2 = 0; s2 < kMaxSplitsKV; ++s2)
+        if (s2 < S) mx = fmaxf(mx, ml[s2].x);
+      float L = 0.f;
+#pragma unroll
+      for (int s2 = 0; s2 < kMaxSplitsKV; ++s2)
+        if (s2 < S) {
+          const float w = ml[s2].x > -INFINITY ? exp2f(ml[s2].x - mx) : 0.f;
+          wgt[threadIdx.x * kMaxSplitsKV + s2] = w;
+          L += w * ml[s2].y;
         }
-        const float inv = L > 0.f ? 1.f / L : 0.f;
-        if (tok < p.M) {
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(a0 * inv, a1 * inv);
-          *reinterpret_cast<__nv_bfloat162*>(p.out + (size_t)tok * (kHeads * HD) + head * HD + 2 * t) = b2;
+      inv[threadIdx.x] = L > 0.f ? 1.f / L : 0.f;
+    }
+    __syncthreads();
+    // (row, quad) outputs: rows fastest so the split loads are contiguous runs
+    const int total = my_nr * (HD / 4);
+    for (int idx0 = threadIdx.x; idx0 < total; idx0 += 2 * kThreads) {
+      float4 v[2][kMaxSplitsKV];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int idx = idx0 + u * kThreads;
+        if (idx < total) {
+          const int rr = idx % my_nr, c4 = idx / my_nr;
+#pragma unroll
+          for (int s2 = 0; s2 < kMaxSplitsKV; ++s2)
+            if (s2 < S)
+              v[u][s2] = __ldcg(ws_o + ((size_t)(tile * S + s2) * (HD / 4) + c4) * BQ + my_r0 + rr);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int idx = idx0 + u * kThreads;
+        if (idx < total) {
+          const int rr = idx % my_nr, c4 = idx / my_nr;
+          float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int s2 = 0; s2 < kMaxSplitsKV; ++s2)
+            if (s2 < S) {
+              const float w = wgt[rr * kMaxSplitsKV + s2];
+              a.x += w * v[u][s2].x;
+              a.y += w * v[u][s2].y;
+              a.z += w * v[u][s2].z;
+              a.w += w * v[u][s2].w;
+            }
+          const float iv = inv[rr];
+          const int row = my_r0 + rr;
+          const int tok = m0 + (row >> 3), head = row & 7;
+          if (tok < p.M) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(a.x * iv, a.y * iv);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(a.z * iv, a.w * iv);
+            uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+            *reinterpret_cast<uint2*>(p.out + (size_t)tok * (kHeads * HD) + head * HD + 4 * c4) = pk;
+          }
         }
       }
     }
-    cluster.sync();  // peers may still read this CTA's partial
+    if (threadIdx.x == 64) ATT_STAMP(7);
+    if (threadIdx.x == 64) ATT_STAMP(8);
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -390,6 +487,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::tc_fence_after();
     sm100::tmem_dealloc<kTmemCols>(tmem);
   }
+#ifdef SF_TRACE
+  if (threadIdx.x == 64 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && (blockIdx.y == 0 || blockIdx.y == gridDim.y - 1)) {
+    ATT_STAMP(9);
+    printf("attn trace blk(%d,%d) setup=%.2f q_ready=%.2f mma_done=%.2f pv_final=%.2f staged=%.2f csync1=%.2f merged=%.2f csync2=%.2f end=%.2f us\n",
+           blockIdx.x, blockIdx.y, (stamps[1] - stamps[0]) * 1e-3, (stamps[2] - stamps[0]) * 1e-3,
+           (stamps[3] - stamps[0]) * 1e-3, (stamps[4] - stamps[0]) * 1e-3, (stamps[5] - stamps[0]) * 1e-3,
+           (stamps[6] - stamps[0]) * 1e-3, (stamps[7] - stamps[0]) * 1e-3, (stamps[8] - stamps[0]) * 1e-3,
+           (stamps[9] - stamps[0]) * 1e-3);
+  }
+#endif
 }
 
 }  // namespace attn

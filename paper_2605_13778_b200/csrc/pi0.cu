@@ -112,9 +112,9 @@ struct EmbedParams {
   float taus[SF_MAX_K];
   const float* temb;    // [K][W] (mode 0) | [1][W] for this step (mode 1)
   const float* state;   // [B][S]
-  const float* a_w;     // [W][D]
+  const float* a_wt;    // [D][W] (transposed copy of a_w [W][D])
   const float* a_b;
-  const float* s_w;     // [W][S]
+  const float* s_wt;    // [S][W]
   const float* s_b;
   float* x;             // [M][W]
   bf16* xb;             // [M][W]
@@ -122,8 +122,10 @@ struct EmbedParams {
   int ssq_ld;
 };
 
-// One CTA per 16 token rows (256 threads; thread t owns features t + 256 i).
-// Each weight row is read once per CTA and reused for all 16 tokens.
+// One CTA per (16 token rows, 256 features): thread t owns feature
+// blockIdx.y * 256 + t. The embedding weights are read through transposed
+// copies ([D][W], [S][W], made once at sf_ae_create) so every weight load is
+// a coalesced 1 KB warp access, and each is reused for all 16 tokens.
 constexpr int kEmbedTok = 16;
 
 __global__ void __launch_bounds__(256) embed_kernel(const EmbedParams p) {
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(256) embed_kernel(const EmbedParams p) {
   __shared__ float in[kEmbedTok][65];
   __shared__ int kind[kEmbedTok];  // 0 padding, 1 state token, 2 action token
   __shared__ int kbr[kEmbedTok];   // branch of the token
-  __shared__ float red[8][8][kEmbedTok];
+  __shared__ float red[8][kEmbedTok];
   __shared__ int has_state;
   if (threadIdx.x == 0) has_state = 0;
   __syncthreads();
@@ -168,56 +170,62 @@ __global__ void __launch_bounds__(256) embed_kernel(const EmbedParams p) {
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_iter = p.W / 256;
-  for (int it = 0; it < n_iter; ++it) {
-    const int n = threadIdx.x + 256 * it;
-    float acc[kEmbedTok];
-    const float ab = p.a_b[n];
+  const int n = blockIdx.y * 256 + threadIdx.x;
+  float acc[kEmbedTok];
+  const float ab = p.a_b[n];
 #pragma unroll
-    for (int tk = 0; tk < kEmbedTok; ++tk) acc[tk] = ab;
-    for (int c = 0; c < p.D; ++c) {
-      const float w = p.a_w[n * p.D + c];
+  for (int tk = 0; tk < kEmbedTok; ++tk) acc[tk] = ab;
+#pragma unroll 8
+  for (int c = 0; c < p.D; ++c) {
+    const float w = __ldg(p.a_wt + c * p.W + n);
 #pragma unroll
-      for (int tk = 0; tk < kEmbedTok; ++tk) acc[tk] = fmaf(w, in[tk][c], acc[tk]);
-    }
-    if (has_state) {
-      float sacc[kEmbedTok];
-      const float sb = p.s_b[n];
+    for (int tk = 0; tk < kEmbedTok; ++tk) acc[tk] = fmaf(w, in[tk][c], acc[tk]);
+  }
+  if (has_state) {
+    float sacc[kEmbedTok];
+    const float sb = p.s_b[n];
 #pragma unroll
-      for (int tk = 0; tk < kEmbedTok; ++tk) sacc[tk] = sb;
-      for (int c = 0; c < p.S; ++c) {
-        const float w = p.s_w[n * p.S + c];
+    for (int tk = 0; tk < kEmbedTok; ++tk) sacc[tk] = sb;
+#pragma unroll 8
+    for (int c = 0; c < p.S; ++c) {
+      const float w = __ldg(p.s_wt + c * p.W + n);
 #pragma unroll
-        for (int tk = 0; tk < kEmbedTok; ++tk) sacc[tk] = fmaf(w, in[tk][c], sacc[tk]);
-      }
-#pragma unroll
-      for (int tk = 0; tk < kEmbedTok; ++tk)
-        if (kind[tk] == 1) acc[tk] = sacc[tk];
+      for (int tk = 0; tk < kEmbedTok; ++tk) sacc[tk] = fmaf(w, in[tk][c], sacc[tk]);
     }
 #pragma unroll
-    for (int tk = 0; tk < kEmbedTok; ++tk) {
-      const int m = m0 + tk;
-      float v = 0.f;
-      if (kind[tk] == 2) v = acc[tk] + p.temb[kbr[tk] * p.W + n];
-      else if (kind[tk] == 1) v = acc[tk];
-      p.x[(size_t)m * p.W + n] = v;
-      p.xb[(size_t)m * p.W + n] = __float2bfloat16_rn(v);
-      float sq = v * v;
-      for (int off = 16; off; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
-      if (lane == 0) red[warp][it][tk] = sq;
-    }
+    for (int tk = 0; tk < kEmbedTok; ++tk)
+      if (kind[tk] == 1) acc[tk] = sacc[tk];
+  }
+#pragma unroll
+  for (int tk = 0; tk < kEmbedTok; ++tk) {
+    const int m = m0 + tk;
+    float v = 0.f;
+    if (kind[tk] == 2) v = acc[tk] + p.temb[kbr[tk] * p.W + n];
+    else if (kind[tk] == 1) v = acc[tk];
+    p.x[(size_t)m * p.W + n] = v;
+    p.xb[(size_t)m * p.W + n] = __float2bfloat16_rn(v);
+    float sq = v * v;
+    for (int off = 16; off; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if (lane == 0) red[warp][tk] = sq;
   }
   __syncthreads();
-  // per-128-feature-group sum of squares: group 2*it + half, half = warp >> 2
-  const int groups = p.W / 128;
-  for (int idx = threadIdx.x; idx < groups * kEmbedTok; idx += blockDim.x) {
-    const int g = idx / kEmbedTok, tk = idx - g * kEmbedTok;
-    const int it = g >> 1, half = g & 1;
-    const float s = ((red[4 * half][it][tk] + red[4 * half + 1][it][tk]) + red[4 * half + 2][it][tk]) +
-                    red[4 * half + 3][it][tk];
-    p.ssq[(size_t)g * p.ssq_ld + m0 + tk] = s;
+  // per-128-feature-group sum of squares: warps 0-3 cover group 2y, 4-7 group 2y+1
+  if (threadIdx.x < 2 * kEmbedTok) {
+    const int half = threadIdx.x / kEmbedTok, tk = threadIdx.x % kEmbedTok;
+    const float s = ((red[4 * half][tk] + red[4 * half + 1][tk]) + red[4 * half + 2][tk]) +
+                    red[4 * half + 3][tk];
+    p.ssq[(size_t)(2 * blockIdx.y + half) * p.ssq_ld + m0 + tk] = s;
   }
   if (threadIdx.x == 0) sm100::pdl_launch_dependents();
+}
+
+// [rows][cols] -> [cols][rows] (embedding weights, once per handle)
+__global__ void transpose_f32_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                     int rows, int cols) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows * cols; i += gridDim.x * blockDim.x) {
+    const int r = i / cols, c = i - r * cols;
+    dst[(size_t)c * rows + r] = src[i];
+  }
 }
 
 // --------------------------------------------------------- verify epilogue
@@ -389,6 +397,8 @@ struct Handle {
   int temb_euler_n = -1;
   float* temb_hidden = nullptr;
   float* temb_tau_dev = nullptr;
+  float* a_wt = nullptr;  // [D][W] transposed action-embedding weights
+  float* s_wt = nullptr;  // [S][W] transposed state-embedding weights
   std::map<long long, std::unique_ptr<Buffers>> buffers;  // key: (B, K, mode)
   cudaStream_t capture_stream = nullptr;
 };
@@ -524,6 +534,11 @@ int build(Handle& h, Buffers& b, int B, int K) {
   asplit = (n_blocks + bps - 1) / bps;
   b.attn_splits = asplit;  // split-KV CTAs of a tile form one cluster (DSMEM merge)
   float* attn_ws = nullptr;
+  if (asplit > 1) {
+    // split-KV partials: [tiles][splits][HD/4][128] float4 + (m, l) [tiles][splits][128]
+    const size_t n = (size_t)b.attn_tiles * asplit * (attn::HD * attn::BQ + 2 * attn::BQ);
+    if ((rc = dalloc(&attn_ws, n))) return rc;
+  }
   b.n_counters = (max_tiles > b.attn_tiles ? max_tiles : b.attn_tiles) + 8;
   ALLOC(b.counters, (size_t)b.n_counters);
 #undef ALLOC
@@ -746,9 +761,9 @@ EmbedParams embed_params(const Handle& h, const Buffers& b, int mode, const floa
   for (int k = 0; k < b.K && k < SF_MAX_K; ++k) p.taus[k] = h.temb_taus[k];
   p.temb = temb;
   p.state = b.state;
-  p.a_w = static_cast<const float*>(h.w.a_w);
+  p.a_wt = h.a_wt;
   p.a_b = static_cast<const float*>(h.w.a_b);
-  p.s_w = static_cast<const float*>(h.w.s_w);
+  p.s_wt = h.s_wt;
   p.s_b = static_cast<const float*>(h.w.s_b);
   p.x = b.x;
   p.xb = b.xb;
@@ -770,7 +785,7 @@ int enqueue_verify(Handle& h, Buffers& b, const sf_verify_cfg_t* cfg, cudaStream
       if ((rc = gemm::launch(b.dops[i], s, pdl))) return rc;
   }
   EmbedParams ep = embed_params(h, b, 0, h.temb);
-  if ((rc = launch_pdl(embed_kernel, dim3(b.M / kEmbedTok), dim3(256), 0, s, ep, with_draft && pdl))) return rc;
+  if ((rc = launch_pdl(embed_kernel, dim3(b.M / kEmbedTok, h.cfg.width / 256), dim3(256), 0, s, ep, with_draft && pdl))) return rc;
   trace_mark(s);
   if ((rc = run_stack(h, b, s, pdl))) return rc;
   VerifyEpiParams vp{};
@@ -816,7 +831,7 @@ int enqueue_denoise(Handle& h, Buffers& b, int n_steps, cudaStream_t s, bool pdl
   if ((rc = launch_pdl(status_init_kernel, dim3(1), dim3(256), 0, s, sp, false))) return rc;
   for (int i = 0; i < n_steps; ++i) {
     EmbedParams ep = embed_params(h, b, 1, h.temb_euler + (size_t)i * W);
-    if ((rc = launch_pdl(embed_kernel, dim3(b.M / kEmbedTok), dim3(256), 0, s, ep, pdl))) return rc;
+    if ((rc = launch_pdl(embed_kernel, dim3(b.M / kEmbedTok, h.cfg.width / 256), dim3(256), 0, s, ep, pdl))) return rc;
     if ((rc = run_stack(h, b, s, pdl))) return rc;
     const int total = b.B * h.cfg.horizon * h.cfg.action_dim;
     EulerParams up{b.draft, b.vel, b.B, h.cfg.horizon, h.cfg.action_dim, b.env_rows, n_steps, i,
@@ -913,10 +928,20 @@ extern "C" int sf_ae_create(const sf_ae_config_t* cfg, const sf_ae_weights_t* w,
   int rc;
   if ((rc = dalloc(&h->temb, (size_t)SF_MAX_K * cfg->width)) ||
       (rc = dalloc(&h->temb_hidden, (size_t)64 * cfg->width)) ||
-      (rc = dalloc(&h->temb_tau_dev, 64))) {
+      (rc = dalloc(&h->temb_tau_dev, 64)) ||
+      (rc = dalloc(&h->a_wt, (size_t)cfg->action_dim * cfg->width)) ||
+      (rc = dalloc(&h->s_wt, (size_t)cfg->state_dim * cfg->width))) {
     delete h;
     return rc;
   }
+  // the embedding weights are read transposed (coalesced); the weights are
+  // immutable for the handle's lifetime (sf_ae_create contract)
+  transpose_f32_kernel<<<64, 256>>>(static_cast<const float*>(w->a_w), h->a_wt, cfg->width,
+                                    cfg->action_dim);
+  transpose_f32_kernel<<<64, 256>>>(static_cast<const float*>(w->s_w), h->s_wt, cfg->width,
+                                    cfg->state_dim);
+  SF_CHECK_CUDA(cudaGetLastError());
+  SF_CHECK_CUDA(cudaDeviceSynchronize());
   *handle = h;
   return SF_OK;
 }
@@ -936,6 +961,8 @@ extern "C" int sf_ae_destroy(void* handle) {
   cudaFree(h->temb);
   cudaFree(h->temb_hidden);
   cudaFree(h->temb_tau_dev);
+  cudaFree(h->a_wt);
+  cudaFree(h->s_wt);
   if (h->temb_euler) cudaFree(h->temb_euler);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
   delete h;
@@ -1193,7 +1220,7 @@ extern "C" int sf_ae_velocity(void* handle, int n_envs, int rows, const float* x
                                 cudaMemcpyDeviceToDevice, s));
   EmbedParams ep = embed_params(*h, *b, 1, h->temb);
   ep.draft = actions;
-  if ((rc = launch_pdl(embed_kernel, dim3(b->M / kEmbedTok), dim3(256), 0, s, ep, false))) return rc;
+  if ((rc = launch_pdl(embed_kernel, dim3(b->M / kEmbedTok, h->cfg.width / 256), dim3(256), 0, s, ep, false))) return rc;
   if ((rc = run_stack(*h, *b, s, false))) return rc;
   GatherParams gp{b->vel, v_out, n_envs, rows, cf.horizon, cf.action_dim, T_of(*h), b->env_rows};
   gather_vel_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(gp);
