@@ -55,7 +55,7 @@ __device__ __forceinline__ float gelu_tanh(float x) {
 __device__ __forceinline__ float row_scale(const EpiArgs& e, int m) {
   if (!e.ssq_in) return 1.0f;
   float s = 0.f;
-  for (int g = 0; g < e.ssq_groups; ++g) s += e.ssq_in[g * e.ssq_ld + m];
+  for (int g = 0; g < e.ssq_groups; ++g) s += __ldcg(e.ssq_in + g * e.ssq_ld + m);
   return rsqrtf(s * e.inv_width + e.eps);
 }
 
@@ -141,7 +141,7 @@ __device__ __forceinline__ void epi_swap(const EpiArgs& e, int n, int m0, const 
     float xo[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j)  // all loads before the read-modify-write stores
-      xo[j] = (nvalid && m0 + j < e.M) ? e.x[(size_t)(m0 + j) * e.N + n] : 0.f;
+      xo[j] = (nvalid && m0 + j < e.M) ? __ldcg(e.x + (size_t)(m0 + j) * e.N + n) : 0.f;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int m = m0 + j;

@@ -66,3 +66,31 @@ if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace":
     trace(208, 8192, 1024, 208, 2)
     trace(208, 2560, 1024, 208, 6)
     trace(16, 128, 64, 16, 1)
+
+
+def sweep(M):
+    """Batch-1 shape sweep: token tile (bn) x K splits for the four layer GEMMs."""
+    shapes = {"qkv": (2560, 1024), "o": (1024, 2048), "gu": (8192, 1024), "down": (1024, 4096)}
+    for name, (N, K) in shapes.items():
+        best = None
+        for bn in sorted({((M + 15) // 16) * 16, ((M + 31) // 32) * 16, ((M + 63) // 64) * 16, 32, 16}, reverse=True):
+            tiles = ((N + 127) // 128) * ((M + bn - 1) // bn)
+            for S in (1, 2, 3, 4, 6, 8, 12, 16):
+                if tiles * S > 160 or S > K // 64:
+                    continue
+                x = torch.randn(M, K, device="cuda").bfloat16()
+                w = (torch.randn(N, K, device="cuda") * 0.05).bfloat16()
+                out = torch.empty(M, N, device="cuda")
+                us = ctypes.c_float()
+                _capi.check(_capi.lib().sf_dbg_gemm_time(w.data_ptr(), N, x.data_ptr(), M, K, bn, S, 1,
+                                                         out.data_ptr(), 30, 1, ctypes.byref(us),
+                                                         torch.cuda.current_stream().cuda_stream), "time")
+                print(f"{name} M={M} bn={bn:3d} S={S:2d} ctas={tiles * S:3d}: {us.value:7.2f} us")
+                if best is None or us.value < best[0]:
+                    best = (us.value, bn, S)
+        print(f"BEST {name} M={M}: {best[0]:.2f} us bn={best[1]} S={best[2]}", flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "sweep":
+    for M in (208, 64):
+        sweep(M)
