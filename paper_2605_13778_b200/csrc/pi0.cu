@@ -594,8 +594,18 @@ int build(Handle& h, Buffers& b, int B, int K) {
     return gemm::plan(&b.sops[idx], wt, n_out, k_in, act, b.M, k_in, k_in, bn_swap,
                       stack_splits(n_out, k_in), 1, e);
   };
+  struct Spec {
+    const void* wt;
+    int n_out;
+    const void* act;
+    int k_in;
+    gemm::EpiArgs e;
+  };
+  std::vector<Spec> specs(4 * L);
   auto plan_op = [&](gemm::Op* op, const void* wt, int n_out, const void* act, int k_in,
                      const gemm::EpiArgs& e) {
+    const int idx = (int)(op - b.ops.data());
+    if (idx < 4 * L) specs[idx] = Spec{wt, n_out, act, k_in, e};
     int r = plan_mm(op, wt, n_out, act, b.M, k_in, swap ? bn_swap : bn_norm, swap, e);
     if (r) return r;
     return plan_sop((int)(op - b.ops.data()), wt, n_out, act, k_in, e);
@@ -663,6 +673,74 @@ int build(Handle& h, Buffers& b, int B, int K) {
       if ((rc = plan_mm(&b.dops[i], h.w.draft_w[i], nout[i], ins[i], B, kin[i], dbn, dswap, e)))
         return rc;
     }
+  }
+  // --- batch-1 plan tuning: the swap-AB GEMMs trade K splits (fp32 partials
+  // through L2) against token tiles (weights re-read from L2); the best mix
+  // depends on the token count, so each layer GEMM class (qkv, o, gu, down --
+  // identical across layers) is timed over a small (bn, splits) grid on this
+  // device and every layer is re-planned with the winner.
+  if (swap && getenv("SF_NO_TUNE") == nullptr) {
+    cudaStream_t ts;
+    SF_CHECK_CUDA(cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1;
+    SF_CHECK_CUDA(cudaEventCreate(&e0));
+    SF_CHECK_CUDA(cudaEventCreate(&e1));
+    float* tws = nullptr;
+    size_t tws_bytes = 0;
+    auto c16 = [](int x) { return ((x + 15) / 16) * 16; };
+    for (int cls = 0; cls < 4; ++cls) {
+      const Spec& sp = specs[cls];
+      const int tiles_a = (sp.n_out + gemm::BM - 1) / gemm::BM, nkb = sp.k_in / gemm::BK;
+      int bns[4] = {bn_swap, c16((b.M + 1) / 2), 64, 32};
+      float best = 1e30f;
+      int best_bn = bn_swap, best_s = 0;
+      for (int bi = 0; bi < 4; ++bi) {
+        const int bn = bns[bi];
+        bool dup = bn > bn_swap;
+        for (int bj = 0; bj < bi; ++bj) dup = dup || bns[bj] == bn;
+        if (dup) continue;
+        const int tiles = tiles_a * ((b.M + bn - 1) / bn);
+        const int Ss[6] = {1, 2, 3, 4, 6, 8};
+        for (int S : Ss) {
+          if (S > nkb || (S > 1 && tiles * S > nsm)) continue;
+          gemm::Op op;
+          if (gemm::plan(&op, sp.wt, sp.n_out, sp.k_in, sp.act, b.M, sp.k_in, sp.k_in, bn, S, 1, sp.e))
+            continue;
+          if (op.p.splits != S) continue;  // K does not split that way
+          if (op.ws_bytes > tws_bytes) {
+            if (tws) cudaFree(tws);
+            SF_CHECK_CUDA(cudaMalloc(&tws, op.ws_bytes));
+            tws_bytes = op.ws_bytes;
+          }
+          op.p.ws = tws;
+          // serialised launches (no PDL): with PDL, back-to-back copies of
+          // the same GEMM overlap and reward configs that leave SMs idle
+          for (int i = 0; i < 3; ++i)
+            if ((rc = gemm::launch(op, ts, false))) return rc;
+          SF_CHECK_CUDA(cudaEventRecord(e0, ts));
+          for (int i = 0; i < 20; ++i)
+            if ((rc = gemm::launch(op, ts, false))) return rc;
+          SF_CHECK_CUDA(cudaEventRecord(e1, ts));
+          SF_CHECK_CUDA(cudaEventSynchronize(e1));
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (getenv("SF_TUNE_VERBOSE"))
+            printf("tune cls %d (N=%d K=%d M=%d): bn=%d S=%d grid=(%d,%d,%d) %.2f us\n", cls, sp.n_out,
+                   sp.k_in, b.M, bn, S, op.grid.x, op.grid.y, op.grid.z, ms * 50.f);
+          if (ms < best * 0.98f) best = ms, best_bn = bn, best_s = S;
+        }
+      }
+      for (int l = 0; l < L; ++l) {
+        const Spec& q = specs[4 * l + cls];
+        if ((rc = gemm::plan(&b.ops[4 * l + cls], q.wt, q.n_out, q.k_in, q.act, b.M, q.k_in, q.k_in,
+                             best_bn, best_s, 1, q.e)))
+          return rc;
+      }
+    }
+    if (tws) cudaFree(tws);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(ts);
   }
   // --- one split-K workspace shared by every GEMM (kernels are stream-ordered;
   // with PDL a GEMM only touches it after griddepcontrol.wait)
