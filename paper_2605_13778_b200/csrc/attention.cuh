@@ -29,7 +29,7 @@ namespace attn {
 
 namespace cg = cooperative_groups;
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 softmax (2 per lane quarter)
 constexpr int BQ = 128;     // query rows per tile (16 tokens x 8 heads)
 constexpr int BKEY = 64;    // keys per block
 constexpr int HD = 256;     // head dim
@@ -39,7 +39,9 @@ constexpr uint32_t kKBytes = BKEY * HD * 2;       // 32 KB (4 chunks of 64 x 64)
 constexpr uint32_t kVBytes = HD * BKEY * 2;       // 32 KB (V^T: 256 x 64)
 constexpr uint32_t kPBytes = BQ * BKEY * 2;       // 16 KB
 constexpr uint32_t kStageBytes = kKBytes + kVBytes;
-constexpr uint32_t kSmemBytes = kQBytes + 2 * kStageBytes + kPBytes + 1024 /*bars*/ + 1024 /*align*/;
+// control region after P: mbarriers (256 B) + the softmax pair exchange (2 KB)
+constexpr uint32_t kCtlBytes = 4096;
+constexpr uint32_t kSmemBytes = kQBytes + 2 * kStageBytes + kPBytes + kCtlBytes + 1024 /*align*/;
 constexpr int kTmemCols = 512;  // S0 [0,64) S1 [64,128) O [128,384)
 constexpr int kPartStride = HD + 2;  // split-KV partial O row stride in SMEM (floats)
 constexpr int kMaxSplitsKV = 16;     // split-KV cluster size limit
@@ -123,9 +125,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* kv_empty = bars + 3;  // [2]
   uint64_t* s_full = bars + 5;    // [2]
   uint64_t* s_free = bars + 7;    // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* pv_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* p_full = bars + 9;    // [2]
+  uint64_t* pv_done = bars + 11;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
   __shared__ unsigned long long stamps[16];
   (void)stamps;
@@ -150,10 +152,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::mbar_init(&kv_full[s], 1);
       sm100::mbar_init(&kv_empty[s], 1);
       sm100::mbar_init(&s_full[s], 1);
-      sm100::mbar_init(&s_free[s], 128);
+      sm100::mbar_init(&s_free[s], 256);
     }
-    sm100::mbar_init(p_full, 128);
-    sm100::mbar_init(pv_done, 1);
+    for (int b = 0; b < 2; ++b) {
+      sm100::mbar_init(&p_full[b], 256);
+      sm100::mbar_init(&pv_done[b], 1);
+    }
     sm100::fence_barrier_init();
   }
   if (warp == 1) sm100::tmem_alloc<kTmemCols>(tmem_slot);
@@ -212,14 +216,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::mbar_wait(q_full, 0);
       ATT_STAMP(2);
       auto issue_pv = [&](int i) {
-        sm100::mbar_wait(p_full, i & 1);
+        sm100::mbar_wait(&p_full[i & 1], (i >> 1) & 1);
         sm100::tc_fence_after();
         const uint32_t v_addr = sm100::smem_u32(sKV + (i & 1) * kStageBytes + kKBytes);
+        const uint32_t pb = p_addr;
 #pragma unroll
         for (int kk = 0; kk < BKEY / 16; ++kk)
-          sm100::umma_bf16(tmem + 128, sm100::make_sw128_desc(p_addr + kk * 32),
+          sm100::umma_bf16(tmem + 128, sm100::make_sw128_desc(pb + kk * 32),
                            sm100::make_sw128_desc(v_addr + kk * 32), idesc_o, (i | kk) != 0);
-        sm100::umma_commit(pv_done);
+        sm100::umma_commit(&pv_done[i & 1]);
         sm100::umma_commit(&kv_empty[i & 1]);
       };
       for (int i = 0; i < nb; ++i) {
@@ -243,8 +248,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else {
-    // -------------------------------------------- softmax + correction + epilogue
+    // ------------------------------------------- softmax + correction + epilogue
+    // Two warps per TMEM lane quarter (warps q+2 and q+6): each owns the same
+    // 32 query rows and half of the columns (32 of a block's 64 keys; 128 of
+    // O's 256 dims). The pair exchanges row maxima / sums through SMEM.
     const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = q * 32 + lane;  // query row in the tile == TMEM lane
     const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
     const int tok = m0 + (r >> 3);
@@ -255,23 +264,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool real_q = local_q < p.segs * p.seg_len && tok < p.M;
     const int seg_lo = seg_q * p.seg_len;                         // local token range of the
     const int seg_hi = seg_lo + (t_q >= 1 ? p.seg_len : 1);       // row's visible suffix keys
+    float* xm = reinterpret_cast<float*>(bars + 32);              // [2 parity][2 half][128]
     float m_used = -INFINITY, l_sum = 0.f;
     sm100::pdl_wait();
-    if (r == 0) sm100::pdl_launch_dependents();
+    if (threadIdx.x == 64) sm100::pdl_launch_dependents();
     for (int i = 0; i < nb; ++i) {
       const int j = j0 + i;
       const int s = i & 1;
       sm100::mbar_wait(&s_full[s], (i >> 1) & 1);
       sm100::tc_fence_after();
-      uint32_t raw[4][16];
+      uint32_t raw[2][16];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) sm100::tmem_ld16(t_lane + s * BKEY + c * 16, raw[c]);
+      for (int c = 0; c < 2; ++c) sm100::tmem_ld16(t_lane + s * BKEY + half * 32 + c * 16, raw[c]);
       sm100::tmem_ld_wait();
       sm100::tc_fence_before();
       sm100::mbar_arrive(&s_free[s]);
-      // The valid keys of a row inside one block are a contiguous column range
-      // [lo, hi): prefix keys < P; suffix keys = the row's own segment, only
-      // its state token for the state row (block mask).
+      // valid keys of the row inside this block: [lo, hi) (block mask)
       int lo = 0, hi;
       if (j < p.n_prefix_blocks) {
         hi = p.prefix_len - j * BKEY;
@@ -282,14 +290,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         hi = 0;
       }
-      float sv[64];
+      lo -= half * 32;
+      hi -= half * 32;
+      float sv[32];
       float mb = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const float x = __uint_as_float(raw[c >> 4][c & 15]) * p.scale_log2;
+      for (int c = 0; c < 32; ++c) {
+        const float x = __uint_as_float(raw[c >> 4][c & 15]);
         sv[c] = (c >= lo && c < hi) ? x : -INFINITY;
         mb = fmaxf(mb, sv[c]);
       }
+      // pair max (raw scores; the positive scale commutes with max)
+      xm[(s * 2 + half) * BQ + r] = mb;
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+      mb = fmaxf(xm[(s * 2) * BQ + r], xm[(s * 2 + 1) * BQ + r]) * p.scale_log2;
       const float m_new = fmaxf(m_used, mb);
       bool rescale = false;
       float alpha = 1.f;
@@ -303,14 +317,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       // P(i) overwrites P(i-1) and O may be rescaled: PV(i-1) must be done
+      // (both warps of a pair decide the rescale alike)
       if (i >= 1) {
-        sm100::mbar_wait(pv_done, (i - 1) & 1);
+        sm100::mbar_wait(&pv_done[(i - 1) & 1], ((i - 1) >> 1) & 1);
         sm100::tc_fence_after();
       }
-      if (__any_sync(0xffffffffu, rescale) && i >= 1) {
+      const bool any_rescale = __any_sync(0xffffffffu, rescale);
+      if (any_rescale && i >= 1) {
         l_sum *= alpha;
 #pragma unroll 1
-        for (int c0 = 0; c0 < HD; c0 += 16) {
+        for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 16) {
           uint32_t o[16];
           sm100::tmem_ld16(t_lane + 128 + c0, o);
           sm100::tmem_ld_wait();
@@ -322,80 +338,95 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if (rescale) {
         l_sum *= alpha;
       }
-      // P row (64 keys, bf16) into the SWIZZLE_128B K-major tile: 16 B chunk c
-      // of row r lives at chunk (c ^ (r & 7)).
+      // P row half (32 keys, bf16) into the SWIZZLE_128B K-major tile: 16 B
+      // chunk c of row r lives at chunk (c ^ (r & 7)). p = 2^(x*scale - m).
       uint8_t* prow = sP + r * 128;
-      // masked scores are -inf -> exp2 gives 0; rows with nothing valid yet use 0
       const float mu = m_used == -INFINITY ? 0.f : m_used;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < 4; ++c) {
         uint32_t w[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const float p0 = exp2f(sv[c * 8 + 2 * k] - mu);
-          const float p1 = exp2f(sv[c * 8 + 2 * k + 1] - mu);
+          const float p0 = exp2f(fmaf(sv[c * 8 + 2 * k], p.scale_log2, -mu));
+          const float p1 = exp2f(fmaf(sv[c * 8 + 2 * k + 1], p.scale_log2, -mu));
           l_sum += p0 + p1;
           __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
           w[k] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        const int cc = half * 4 + c;
+        *reinterpret_cast<uint4*>(prow + ((cc ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
       fence_async_smem();
       sm100::tc_fence_before();
-      sm100::mbar_arrive(p_full);
+      sm100::mbar_arrive(&p_full[i & 1]);
     }
     // ---- epilogue: O row (256 fp32) is final once the last PV retires
     if (nb > 0) {
-      sm100::mbar_wait(pv_done, (nb - 1) & 1);
+      sm100::mbar_wait(&pv_done[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
       sm100::tc_fence_after();
     }
-    if (r == 0) ATT_STAMP(4);
+    // pair sum of l (each warp summed its own columns); the parity slot of
+    // block nb was last read at block nb - 2, before the pair's last barrier
+    {
+      const int ps = nb & 1;
+      xm[(ps * 2 + half) * BQ + r] = l_sum;
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+      l_sum = xm[(ps * 2) * BQ + r] + xm[(ps * 2 + 1) * BQ + r];
+    }
+    if (r == 0 && half == 0) ATT_STAMP(4);
     m_fin = m_used;
     l_fin = l_sum;
     if (p.splits == 1) {
       const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
       __nv_bfloat16* dst = p.out + (size_t)tok * (kHeads * HD) + head * HD;
-      for (int c0 = 0; c0 < HD; c0 += 16) {
-        uint32_t o[16];
-        sm100::tmem_ld16(t_lane + 128 + c0, o);
+      for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 32) {
+        uint32_t o[2][16];
+        sm100::tmem_ld16(t_lane + 128 + c0, o[0]);
+        sm100::tmem_ld16(t_lane + 128 + c0 + 16, o[1]);
         sm100::tmem_ld_wait();
-        uint32_t w[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[2 * k]) * inv,
-                                                    __uint_as_float(o[2 * k + 1]) * inv);
-          w[k] = *reinterpret_cast<uint32_t*>(&b2);
-        }
-        if (tok < p.M) {
-          uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
-          d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
-          d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        for (int u = 0; u < 2; ++u) {
+          uint32_t w[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[u][2 * k]) * inv,
+                                                      __uint_as_float(o[u][2 * k + 1]) * inv);
+            w[k] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          if (tok < p.M) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst + c0 + 16 * u);
+            d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          }
         }
       }
     }
   }
   if (p.splits > 1) {
     // Split-KV merge through L2: every split writes its unnormalised partial
-    // O as [HD/4 quads][128 rows] float4 (each warp store is 512 contiguous
-    // bytes) plus (m, l) per row; after one cluster barrier (release/acquire
-    // at cluster scope orders the global stores) cluster rank s merges rows
-    // [s*rows, (s+1)*rows) in a fixed split order (deterministic).
+    // O in bf16 (the merged output is bf16 too; writes are the slow side of
+    // L2, ~35 GB/s per SM) as [HD/8 octets][128 rows] uint4 (each warp store
+    // is 512 contiguous bytes) plus fp32 (m, l) per row; after one cluster
+    // barrier (release/acquire at cluster scope orders the global stores)
+    // cluster rank s merges rows [s*rows, (s+1)*rows) in a fixed split order
+    // (deterministic), accumulating in fp32.
     cg::cluster_group cluster = cg::this_cluster();
     const int S = p.splits;
     const int rows = (BQ + S - 1) / S;
     const int my_r0 = split * rows;
     const int my_nr = max(0, min(BQ, my_r0 + rows) - my_r0);
-    const size_t part_floats = (size_t)HD * BQ;
-    float4* ws_o = reinterpret_cast<float4*>(p.ws);  // [(tile*S + s)][HD/4][BQ]
-    float2* ws_ml = reinterpret_cast<float2*>(p.ws + (size_t)p.tiles * S * part_floats);
+    const size_t part_words = (size_t)HD * BQ / 2;  // bf16 pairs per (tile, split)
+    uint4* ws_o = reinterpret_cast<uint4*>(p.ws);  // [(tile*S + s)][HD/8][BQ]
+    float2* ws_ml = reinterpret_cast<float2*>(p.ws + (size_t)p.tiles * S * part_words);
     if (warp >= 2) {
       const int q = warp & 3;
+      const int half = (warp - 2) >> 2;
       const int r = q * 32 + lane;
       const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
-      float4* dst = ws_o + (size_t)(tile * S + split) * (HD / 4) * BQ + r;
-      ws_ml[(size_t)(tile * S + split) * BQ + r] = make_float2(m_fin, l_fin);
+      uint4* dst = ws_o + (size_t)(tile * S + split) * (HD / 8) * BQ + r;
+      if (half == 0) ws_ml[(size_t)(tile * S + split) * BQ + r] = make_float2(m_fin, l_fin);
 #pragma unroll 1
-      for (int c0 = 0; c0 < HD; c0 += 64) {
+      for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 64) {
         uint32_t o[4][16];
 #pragma unroll
         for (int u = 0; u < 4; ++u) sm100::tmem_ld16(t_lane + 128 + c0 + 16 * u, o[u]);
@@ -403,10 +434,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int k = 0; k < 16; k += 4)
-            __stcg(dst + (size_t)((c0 + 16 * u + k) >> 2) * BQ,
-                   make_float4(__uint_as_float(o[u][k]), __uint_as_float(o[u][k + 1]),
-                               __uint_as_float(o[u][k + 2]), __uint_as_float(o[u][k + 3])));
+          for (int k = 0; k < 16; k += 8) {
+            uint32_t w[4];
+#pragma unroll
+            for (int z = 0; z < 4; ++z) {
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[u][k + 2 * z]),
+                                                        __uint_as_float(o[u][k + 2 * z + 1]));
+              w[z] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            __stcg(dst + (size_t)((c0 + 16 * u + k) >> 3) * BQ, make_uint4(w[0], w[1], w[2], w[3]));
+          }
       }
     }
     if (threadIdx.x == 64) ATT_STAMP(5);
@@ -436,45 +473,64 @@ __global__ void __launch_bounds__(kThreads, 1)
       inv[threadIdx.x] = L > 0.f ? 1.f / L : 0.f;
     }
     __syncthreads();
-    // (row, quad) outputs: rows fastest so the split loads are contiguous runs
-    const int total = my_nr * (HD / 4);
-    for (int idx0 = threadIdx.x; idx0 < total; idx0 += 2 * kThreads) {
-      float4 v[2][kMaxSplitsKV];
+    // (row, octet) outputs: rows fastest so the split loads are contiguous runs;
+    // unconditional (clamped) loads keep every split's octet in registers
+    const int total = my_nr * (HD / 8);
+    constexpr int IT = 3;  // items per thread per round: all their split loads in flight at once
+    for (int base = threadIdx.x; base < total; base += IT * kThreads) {
+      float a[IT][8];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int idx = idx0 + u * kThreads;
-        if (idx < total) {
-          const int rr = idx % my_nr, c4 = idx / my_nr;
+      for (int it = 0; it < IT; ++it)
 #pragma unroll
-          for (int s2 = 0; s2 < kMaxSplitsKV; ++s2)
-            if (s2 < S)
-              v[u][s2] = __ldcg(ws_o + ((size_t)(tile * S + s2) * (HD / 4) + c4) * BQ + my_r0 + rr);
+        for (int z = 0; z < 8; ++z) a[it][z] = 0.f;
+      for (int s0 = 0; s0 < S; s0 += 8) {
+        uint4 v[IT][8];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+          const int idx = min(base + it * kThreads, total - 1);
+          const int rr = idx % my_nr, c8 = idx / my_nr;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int su = min(s0 + u, S - 1);
+            v[it][u] = __ldcg(ws_o + ((size_t)(tile * S + su) * (HD / 8) + c8) * BQ + my_r0 + rr);
+          }
+        }
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+          const int idx = min(base + it * kThreads, total - 1);
+          const int rr = idx % my_nr;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (s0 + u < S) {
+              const float w = wgt[rr * kMaxSplitsKV + s0 + u];
+              const uint32_t pk[4] = {v[it][u].x, v[it][u].y, v[it][u].z, v[it][u].w};
+#pragma unroll
+              for (int z = 0; z < 4; ++z) {
+                const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&pk[z]);
+                const float2 f = __bfloat1622float2(b2);
+                a[it][2 * z] += w * f.x;
+                a[it][2 * z + 1] += w * f.y;
+              }
+            }
         }
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int idx = idx0 + u * kThreads;
-        if (idx < total) {
-          const int rr = idx % my_nr, c4 = idx / my_nr;
-          float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int it = 0; it < IT; ++it) {
+        const int idx = base + it * kThreads;
+        if (idx >= total) break;
+        const int rr = idx % my_nr, c8 = idx / my_nr;
+        const float iv = inv[rr];
+        const int row = my_r0 + rr;
+        const int tok = m0 + (row >> 3), head = row & 7;
+        if (tok < p.M) {
+          uint32_t w4[4];
 #pragma unroll
-          for (int s2 = 0; s2 < kMaxSplitsKV; ++s2)
-            if (s2 < S) {
-              const float w = wgt[rr * kMaxSplitsKV + s2];
-              a.x += w * v[u][s2].x;
-              a.y += w * v[u][s2].y;
-              a.z += w * v[u][s2].z;
-              a.w += w * v[u][s2].w;
-            }
-          const float iv = inv[rr];
-          const int row = my_r0 + rr;
-          const int tok = m0 + (row >> 3), head = row & 7;
-          if (tok < p.M) {
-            __nv_bfloat162 lo = __floats2bfloat162_rn(a.x * iv, a.y * iv);
-            __nv_bfloat162 hi = __floats2bfloat162_rn(a.z * iv, a.w * iv);
-            uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
-            *reinterpret_cast<uint2*>(p.out + (size_t)tok * (kHeads * HD) + head * HD + 4 * c4) = pk;
+          for (int z = 0; z < 4; ++z) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(a[it][2 * z] * iv, a[it][2 * z + 1] * iv);
+            w4[z] = *reinterpret_cast<uint32_t*>(&b2);
           }
+          *reinterpret_cast<uint4*>(p.out + (size_t)tok * (kHeads * HD) + head * HD + 8 * c8) =
+              make_uint4(w4[0], w4[1], w4[2], w4[3]);
         }
       }
     }
