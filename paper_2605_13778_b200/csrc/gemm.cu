@@ -4,6 +4,7 @@
 
 #include <cudaTypedefs.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -47,6 +48,22 @@ KernelFn swap_fn() {
 template <int KIND>
 KernelFn persistent_fn() {
   return gemm_persistent_kernel<KIND>;
+}
+template <int KIND>
+KernelFn pair_fn() {
+  return gemm_pair_kernel<KIND>;
+}
+
+KernelFn pick_pair(int kind) {
+  switch (kind) {
+    case EPI_F32: return pair_fn<EPI_F32>();
+    case EPI_BF16: return pair_fn<EPI_BF16>();
+    case EPI_QKV: return pair_fn<EPI_QKV>();
+    case EPI_RESID: return pair_fn<EPI_RESID>();
+    case EPI_GEGLU: return pair_fn<EPI_GEGLU>();
+    case EPI_TANH_BF16: return pair_fn<EPI_TANH_BF16>();
+  }
+  return nullptr;
 }
 
 KernelFn pick(int kind, bool swap) {
@@ -143,6 +160,29 @@ int plan(Op* op, const void* A, int rows_a, int lda, const void* B, int rows_b, 
     op->cluster = 1;
   }
   op->fn = reinterpret_cast<void*>(pick(e.kind, swap_ab));
+  op->pair = false;
+  // batched shapes with whole 256-wide feature tiles run on 2-SM CTA pairs
+  // (gemm_pair_kernel): 256 x 256 tiles, half of A and B per SM
+  if (!swap_ab && bn == 256 && rows_a >= 4 * 256 && getenv("SF_NO_PAIR") == nullptr) {
+    p.tiles_a = (rows_a + 255) / 256;
+    p.tiles_b = (rows_b + 255) / 256;
+    p.total_tiles = p.tiles_a * p.tiles_b;
+    const size_t budget2 = 227 * 1024 - kTailBytes - 1024;
+    int st = (int)(budget2 / kPairStageBytes);
+    st = st > 16 ? 16 : st;
+    p.stages = st;
+    p.smem_stage_region = (uint32_t)((size_t)st * kPairStageBytes);
+    op->smem = p.smem_stage_region + kTailBytes + 1024;
+    int pairs = num_sms() / 2;
+    pairs = p.total_tiles < pairs ? p.total_tiles : pairs;
+    op->grid = dim3(2 * pairs, 1, 1);
+    op->cluster = 2;
+    op->pair = true;
+    op->fn = reinterpret_cast<void*>(pick_pair(e.kind));
+    int rc = make_map(&op->ta, A, rows_a, K, lda, BM);
+    if (rc) return rc;
+    return make_map(&op->tb, B, rows_b, K, ldb, BM);
+  }
   int rc = make_map(&op->ta, A, rows_a, K, lda, BM);
   if (rc) return rc;
   return make_map(&op->tb, B, rows_b, K, ldb, bn);
@@ -150,8 +190,8 @@ int plan(Op* op, const void* A, int rows_a, int lda, const void* B, int rows_b, 
 
 int launch(const Op& op, cudaStream_t stream, bool pdl) {
   SF_REQUIRE(op.ws_bytes == 0 || op.p.ws, "split-K GEMM launched without a workspace");
-  static bool attr_done[2 * EPI_KINDS] = {};
-  const int slot = op.p.e.kind * 2 + (op.p.swap_ab ? 1 : 0);
+  static bool attr_done[3 * EPI_KINDS] = {};
+  const int slot = op.p.e.kind * 3 + (op.pair ? 2 : op.p.swap_ab ? 1 : 0);
   KernelFn fn = reinterpret_cast<KernelFn>(op.fn);
   if (!attr_done[slot]) {
     SF_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -170,9 +210,9 @@ int launch(const Op& op, cudaStream_t stream, bool pdl) {
   ++na;
   if (op.cluster > 1) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = 1;
+    attr[na].val.clusterDim.x = op.pair ? 2 : 1;
     attr[na].val.clusterDim.y = 1;
-    attr[na].val.clusterDim.z = op.cluster;
+    attr[na].val.clusterDim.z = op.pair ? 1 : op.cluster;
     ++na;
   }
   cfg.attrs = attr;

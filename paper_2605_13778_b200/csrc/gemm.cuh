@@ -109,7 +109,7 @@ __device__ __forceinline__ void epi_swap(const EpiArgs& e, int n, int m0, const 
         int t = local % e.seg_len;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          csv[j] = __ldg(e.rope + (e.pos0 + t) * 128 + i);
+          csv[j] = __ldg(e.rope + (size_t)i * e.rope_ld + e.pos0 + t);
           if (++local == e.env_rows) local = 0, t = -1;
           if (++t == e.seg_len) t = 0;
         }
@@ -163,8 +163,9 @@ __device__ __forceinline__ void epi_swap(const EpiArgs& e, int n, int m0, const 
 // NORMAL: thread = token m (fixed), columns = features n0 + j (16-aligned).
 template <int KIND>
 __device__ __forceinline__ void epi_normal(const EpiArgs& e, int m, int n0, float (&v)[16], float rs,
-                                           float& ssq_acc) {
-  if (m >= e.M) return;
+                                           float& ssq_acc, __nv_bfloat16* vbuf = nullptr) {
+  // the warp-cooperative V^T transpose needs every lane, valid row or not
+  if (m >= e.M && !(KIND == EPI_QKV && vbuf && n0 >= e.q_features + 256)) return;
   const bool full = n0 + 16 <= e.N;
   if (KIND == EPI_F32 || KIND == EPI_BF16 || KIND == EPI_TANH_BF16) {
 #pragma unroll
@@ -219,7 +220,8 @@ __device__ __forceinline__ void epi_normal(const EpiArgs& e, int m, int n0, floa
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const float a = v[2 * (p + u)] * rs, b = v[2 * (p + u) + 1] * rs;
-          const float2 cs = e.rope[pos * 128 + i0 + p + u];
+          // table is position-fastest: a warp's consecutive tokens read consecutive entries
+          const float2 cs = __ldg(e.rope + (size_t)(i0 + p + u) * e.rope_ld + pos);
           ya[u] = a * cs.x - b * cs.y;
           yb[u] = b * cs.x + a * cs.y;
         }
@@ -232,8 +234,30 @@ __device__ __forceinline__ void epi_normal(const EpiArgs& e, int m, int n0, floa
       *reinterpret_cast<uint4*>(base + 128 + i0) = make_uint4(wb[0], wb[1], wb[2], wb[3]);
     } else {
       const int d0 = n0 - e.q_features - 256;
+      if (vbuf) {
+        // V^T through a per-warp SMEM transpose: 16 features x 32 tokens, then
+        // each lane stores two 16 B runs (8 consecutive tokens of one feature)
+        const int lane = threadIdx.x & 31;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) e.vt[(size_t)(d0 + j) * e.vt_ld + m] = __float2bfloat16_rn(v[j] * rs);
+        for (int j = 0; j < 16; ++j) vbuf[j * 32 + lane] = __float2bfloat16_rn(v[j] * rs);
+        __syncwarp();
+        const int m0w = m - lane;  // first token of the warp
+        const int d = lane >> 1;
+#pragma unroll
+        for (int o2 = 0; o2 < 2; ++o2) {
+          const int o = (lane & 1) * 2 + o2;  // token octet
+          const uint4 val = *reinterpret_cast<const uint4*>(vbuf + d * 32 + o * 8);
+          if (m0w + o * 8 + 7 < e.M)
+            *reinterpret_cast<uint4*>(e.vt + (size_t)(d0 + d) * e.vt_ld + m0w + o * 8) = val;
+          else
+            for (int z = 0; z < 8; ++z)
+              if (m0w + o * 8 + z < e.M) e.vt[(size_t)(d0 + d) * e.vt_ld + m0w + o * 8 + z] = vbuf[d * 32 + o * 8 + z];
+        }
+        __syncwarp();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) e.vt[(size_t)(d0 + j) * e.vt_ld + m] = __float2bfloat16_rn(v[j] * rs);
+      }
     }
   } else if (KIND == EPI_RESID) {
     float* xr = e.x + (size_t)m * e.N + n0;
@@ -331,6 +355,7 @@ struct Tail {
   float* rs;             // [256]
   float* red;            // [4][256]
   float* sred;           // [2][2][128] (normal-mode ssq partials per warp group)
+  __nv_bfloat16* vbuf;   // [8 warps][16 x 32] V^T transpose staging (QKV epilogue)
 };
 
 __device__ __forceinline__ Tail carve_tail(uint8_t* smem, const Params& p) {
@@ -344,10 +369,11 @@ __device__ __forceinline__ Tail carve_tail(uint8_t* smem, const Params& p) {
   t.rs = reinterpret_cast<float*>(t.tmem_slot + 4);
   t.red = t.rs + 256;
   t.sred = t.red + 4 * 256;
+  t.vbuf = reinterpret_cast<__nv_bfloat16*>(t.sred + 2 * 2 * 128);
   return t;
 }
 
-constexpr size_t kTailBytes = 8 * (2 * 16 + 4) + 16 + 4 * (256 + 4 * 256 + 2 * 2 * 128);
+constexpr size_t kTailBytes = 8 * (2 * 16 + 4) + 16 + 4 * (256 + 4 * 256 + 2 * 2 * 128) + 8 * 16 * 32 * 2;
 
 // -------------------------------------------------- batch-1: swap + cluster split-K
 
@@ -667,7 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[u][j]);
           float acc = 0.f;
-          epi_normal<KIND>(e, m, tb * p.bn + c * 16, v, rs, acc);
+          epi_normal<KIND>(e, m, tb * p.bn + c * 16, v, rs, acc, T.vbuf + (warp - 2) * 512);
           if (c * 16 < 128) ssq0 += acc;
           else ssq1 += acc;
         }
@@ -694,6 +720,204 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     sm100::tc_fence_after();
     sm100::tmem_dealloc<512>(tmem);
+  }
+}
+
+// ------------------------------------------------- batched: 2-SM CTA pairs
+//
+// gemm_pair_kernel: the batched GEMM on CTA pairs (cluster of 2 on one TPC)
+// with tcgen05.mma.cta_group::2: one 256 x 256 tile per pair and k-block,
+// CTA rank r holds A rows [r*128, r*128+128) and B rows (features)
+// [r*128, r*128+128) of the tile; the pair's MMA reads both halves, so each
+// SM loads 32 KB per 64-deep k-block instead of 48 KB for a 128 x 256 tile
+// (the L2 -> SMEM ingress, ~93 GB/s per SM measured, is what bounds the
+// 1-SM kernel). Only the leader (rank 0) issues MMAs; its full barrier counts
+// the bytes of both CTAs' TMA loads (the peer signals it through
+// .cta_group::2), the commit is multicast to both CTAs' empty / tmem_full
+// barriers, and both CTAs' epilogue threads release the leader's tmem_empty.
+// Each CTA's TMEM holds its own 128 rows x 256 columns (two accumulators).
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// TMA load whose completion is counted on the leader CTA's mbarrier.
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* m, uint32_t bar_cluster, void* dst,
+                                                 int c0, int c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.cta_group::2.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(sm100::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          sm100::smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
+               : "memory");
+}
+
+constexpr uint32_t kPairStageBytes = 2 * BM * BK * 2;  // A half + B half: 32 KB
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tma_a,
+                     const __grid_constant__ CUtensorMap tma_b, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const Tail T = carve_tail(smem, p);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int tiles_n = p.tiles_b;  // 256-feature tiles
+  cg::cluster_group cluster = cg::this_cluster();
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      sm100::mbar_init(&T.full[s], 1);
+      sm100::mbar_init(&T.empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      sm100::mbar_init(&T.tmem_full[a], 1);
+      sm100::mbar_init(&T.tmem_empty[a], 2 * kEpiThreads);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        sm100::smem_u32(T.tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  sm100::tc_fence_before();
+  cluster.sync();  // barriers of both CTAs initialised, TMEM allocated in both
+  sm100::tc_fence_after();
+  const uint32_t tmem = *T.tmem_slot;
+
+  if (warp == 0) {
+    if (sm100::elect_one()) {
+      sm100::tma_prefetch_desc(&tma_a);
+      sm100::tma_prefetch_desc(&tma_b);
+      const uint64_t pol_w = sm100::policy_evict_last();
+      const uint64_t pol_x = sm100::policy_evict_first();
+      int kiter = 0;
+      bool first = true;
+      for (int t = pair; t < p.total_tiles; t += n_pairs) {
+        const int tm = t / tiles_n, tn = t % tiles_n;
+        const int a_row = tm * 256 + rank * BM, b_row = tn * 256 + rank * BM;
+        for (int i = 0; i < p.num_kb; ++i, ++kiter) {
+          const int s = kiter % p.stages;
+          if (kiter >= p.stages) sm100::mbar_wait(&T.empty[s], ((kiter / p.stages) & 1) ^ 1);
+          uint8_t* st = smem + (size_t)s * kPairStageBytes;
+          const uint32_t fb = mapa_shared(sm100::smem_u32(&T.full[s]), 0);
+          if (leader) sm100::mbar_arrive_expect_tx(&T.full[s], 2 * kPairStageBytes);
+          tma_load_2d_pair(&tma_b, fb, st + BM * BK * 2, i * BK, b_row, pol_w);
+          if (first && i == 0) sm100::pdl_wait();  // weights before, activations after
+          tma_load_2d_pair(&tma_a, fb, st, i * BK, a_row, pol_x);
+        }
+        first = false;
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && sm100::elect_one()) {
+      const uint32_t idesc = sm100::make_idesc_bf16(256, 256);
+      int kiter = 0, it = 0;
+      for (int t = pair; t < p.total_tiles; t += n_pairs, ++it) {
+        const int a = it & 1;
+        if (it >= 2) sm100::mbar_wait(&T.tmem_empty[a], ((it >> 1) & 1) ^ 1);
+        sm100::tc_fence_after();
+        for (int i = 0; i < p.num_kb; ++i, ++kiter) {
+          const int s = kiter % p.stages;
+          sm100::mbar_wait(&T.full[s], (kiter / p.stages) & 1);
+          sm100::tc_fence_after();
+          const uint32_t a_addr = sm100::smem_u32(smem + (size_t)s * kPairStageBytes);
+          const uint32_t b_addr = a_addr + BM * BK * 2;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_bf16_pair(tmem + a * 256, sm100::make_sw128_desc(a_addr + kk * 32),
+                           sm100::make_sw128_desc(b_addr + kk * 32), idesc, (i | kk) != 0);
+          umma_commit_pair(&T.empty[s]);
+        }
+        umma_commit_pair(&T.tmem_full[a]);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    const int g = (warp - 2) >> 2;
+    const int lane_row = q * 32 + lane;
+    const EpiArgs& e = p.e;
+    const uint32_t te = mapa_shared(sm100::smem_u32(&T.tmem_empty[0]), 0);
+    sm100::pdl_wait();
+    if (threadIdx.x == 64) sm100::pdl_launch_dependents();
+    int it = 0;
+    for (int t = pair; t < p.total_tiles; t += n_pairs, ++it) {
+      const int tm = t / tiles_n, tn = t % tiles_n;
+      const int a = it & 1;
+      const int m = tm * 256 + rank * BM + lane_row;
+      const float rs = (KIND != EPI_RESID && KIND != EPI_TANH_BF16 && m < e.M) ? row_scale(e, m) : 1.f;
+      sm100::mbar_wait(&T.tmem_full[a], (it >> 1) & 1);
+      sm100::tc_fence_after();
+      const uint32_t t_lane = tmem + a * 256 + ((uint32_t)(q * 32) << 16);
+      float ssq0 = 0.f, ssq1 = 0.f;
+      for (int ch = g; ch < 16; ch += 4) {  // two TMEM loads in flight per wait
+        uint32_t r[2][16];
+        sm100::tmem_ld16(t_lane + ch * 16, r[0]);
+        sm100::tmem_ld16(t_lane + (ch + 2) * 16, r[1]);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int c = ch + 2 * u;
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[u][j]);
+          float acc = 0.f;
+          if (tn * 256 + c * 16 < e.N)
+            epi_normal<KIND>(e, m, tn * 256 + c * 16, v, rs, acc, T.vbuf + (warp - 2) * 512);
+          if (c * 16 < 128) ssq0 += acc;
+          else ssq1 += acc;
+        }
+      }
+      sm100::tc_fence_before();
+      mbar_arrive_remote(te + a * 8);
+      if (KIND == EPI_RESID) {
+        T.sred[(g * 2 + 0) * 128 + lane_row] = ssq0;
+        T.sred[(g * 2 + 1) * 128 + lane_row] = ssq1;
+        epi_bar();
+        if (g == 0 && m < e.M) {
+          for (int fg = 0; fg < 2; ++fg)
+            e.ssq_out[(size_t)(tn * 2 + fg) * e.ssq_out_ld + m] =
+                T.sred[fg * 128 + lane_row] + T.sred[(2 + fg) * 128 + lane_row];
+        }
+        epi_bar();
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  cluster.sync();  // both CTAs done with TMEM and with each other's barriers
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 

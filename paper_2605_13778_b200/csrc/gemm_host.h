@@ -15,7 +15,8 @@ struct Op {
   CUtensorMap tb;
   Params p;
   dim3 grid;
-  int cluster = 1;   // split-K cluster size (swap kernel)
+  int cluster = 1;   // split-K cluster size (swap kernel) / 2 for CTA pairs
+  bool pair = false;  // batched GEMM on 2-SM CTA pairs (gemm_pair_kernel)
   size_t smem = 0;
   size_t ws_bytes = 0;  // split-K workspace the caller must attach as p.ws
   void* fn = nullptr;  // specialised kernel

@@ -45,7 +45,8 @@ struct EpiArgs {
   __nv_bfloat16* k;
   __nv_bfloat16* vt;
   int vt_ld;
-  const float2* rope;  // [pos][head_dim/2] (cos, sin)
+  const float2* rope;  // [head_dim/2][rope_ld] (cos, sin): position fastest
+  int rope_ld;
   int q_features;      // q_heads * head_dim
   int env_rows, seg_len, pos0;
   // RESID (x, xb are [M, N] row-major)

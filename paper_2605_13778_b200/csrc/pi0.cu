@@ -19,7 +19,10 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <stdlib.h>
+
 #include <map>
+#include <tuple>
 #include <memory>
 #include <vector>
 
@@ -220,6 +223,15 @@ __global__ void __launch_bounds__(256) embed_kernel(const EmbedParams p) {
   if (threadIdx.x == 0) sm100::pdl_launch_dependents();
 }
 
+// [rows][cols] -> [cols][rows] of 8-byte elements (RoPE table, once per handle)
+__global__ void transpose_u64_kernel(const unsigned long long* __restrict__ src,
+                                     unsigned long long* __restrict__ dst, int rows, int cols) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows * cols; i += gridDim.x * blockDim.x) {
+    const int r = i / cols, c = i - r * cols;
+    dst[(size_t)c * rows + r] = src[i];
+  }
+}
+
 // [rows][cols] -> [cols][rows] (embedding weights, once per handle)
 __global__ void transpose_f32_kernel(const float* __restrict__ src, float* __restrict__ dst,
                                      int rows, int cols) {
@@ -407,6 +419,7 @@ struct Handle {
   float* temb_tau_dev = nullptr;
   float* a_wt = nullptr;  // [D][W] transposed action-embedding weights
   float* s_wt = nullptr;  // [S][W] transposed state-embedding weights
+  float2* rope_t = nullptr;  // [head_dim/2][P + 1 + H] position-fastest RoPE table
   std::map<long long, std::unique_ptr<Buffers>> buffers;  // key: (B, K, mode)
   cudaStream_t capture_stream = nullptr;
 };
@@ -535,6 +548,7 @@ int build(Handle& h, Buffers& b, int B, int K) {
   const int n_blocks = n_prefix_blocks + (63 + 2 * T + attn::BKEY - 1) / attn::BKEY;
   b.attn_tiles = b.M / 16;
   int asplit = 148 / b.attn_tiles;
+  if (getenv("SF_ATTN_SPLITS")) asplit = atoi(getenv("SF_ATTN_SPLITS"));  // debug override
   if (asplit < 1) asplit = 1;
   if (asplit > n_blocks) asplit = n_blocks;
   if (asplit > attn::kMaxSplitsKV) asplit = attn::kMaxSplitsKV;
@@ -617,7 +631,8 @@ int build(Handle& h, Buffers& b, int B, int K) {
     e.k = b.ks;
     e.vt = b.vt;
     e.vt_ld = b.m_ld;
-    e.rope = static_cast<const float2*>(h.w.rope);
+    e.rope = h.rope_t;
+    e.rope_ld = c.prefix_len + 1 + c.horizon;
     e.q_features = nq;
     e.env_rows = b.env_rows;
     e.seg_len = T;
@@ -688,8 +703,22 @@ int build(Handle& h, Buffers& b, int B, int K) {
     float* tws = nullptr;
     size_t tws_bytes = 0;
     auto c16 = [](int x) { return ((x + 15) / 16) * 16; };
+    // decisions are cached per (shape, rows) for the process: every handle of
+    // the same shape then runs the same plan (bitwise-identical results)
+    static std::map<std::tuple<int, int, int, int>, std::pair<int, int>> tuned;
     for (int cls = 0; cls < 4; ++cls) {
       const Spec& sp = specs[cls];
+      const auto key = std::make_tuple(sp.n_out, sp.k_in, b.M, sp.e.kind);
+      auto hit = tuned.find(key);
+      if (hit != tuned.end()) {
+        for (int l = 0; l < L; ++l) {
+          const Spec& q = specs[4 * l + cls];
+          if ((rc = gemm::plan(&b.ops[4 * l + cls], q.wt, q.n_out, q.k_in, q.act, b.M, q.k_in,
+                               q.k_in, hit->second.first, hit->second.second, 1, q.e)))
+            return rc;
+        }
+        continue;
+      }
       const int tiles_a = (sp.n_out + gemm::BM - 1) / gemm::BM, nkb = sp.k_in / gemm::BK;
       int bns[4] = {bn_swap, c16((b.M + 1) / 2), 64, 32};
       float best = 1e30f;
@@ -730,6 +759,7 @@ int build(Handle& h, Buffers& b, int B, int K) {
           if (ms < best * 0.98f) best = ms, best_bn = bn, best_s = S;
         }
       }
+      tuned[key] = std::make_pair(best_bn, best_s);
       for (int l = 0; l < L; ++l) {
         const Spec& q = specs[4 * l + cls];
         if ((rc = gemm::plan(&b.ops[4 * l + cls], q.wt, q.n_out, q.k_in, q.act, b.M, q.k_in, q.k_in,
@@ -1186,7 +1216,8 @@ extern "C" int sf_ae_create(const sf_ae_config_t* cfg, const sf_ae_weights_t* w,
       (rc = dalloc(&h->temb_hidden, (size_t)64 * cfg->width)) ||
       (rc = dalloc(&h->temb_tau_dev, 64)) ||
       (rc = dalloc(&h->a_wt, (size_t)cfg->action_dim * cfg->width)) ||
-      (rc = dalloc(&h->s_wt, (size_t)cfg->state_dim * cfg->width))) {
+      (rc = dalloc(&h->s_wt, (size_t)cfg->state_dim * cfg->width)) ||
+      (rc = dalloc(&h->rope_t, (size_t)(cfg->head_dim / 2) * (cfg->prefix_len + 1 + cfg->horizon)))) {
     delete h;
     return rc;
   }
@@ -1196,6 +1227,9 @@ extern "C" int sf_ae_create(const sf_ae_config_t* cfg, const sf_ae_weights_t* w,
                                     cfg->action_dim);
   transpose_f32_kernel<<<64, 256>>>(static_cast<const float*>(w->s_w), h->s_wt, cfg->width,
                                     cfg->state_dim);
+  transpose_u64_kernel<<<64, 256>>>(static_cast<const unsigned long long*>(w->rope),
+                                    reinterpret_cast<unsigned long long*>(h->rope_t),
+                                    cfg->prefix_len + 1 + cfg->horizon, cfg->head_dim / 2);
   SF_CHECK_CUDA(cudaGetLastError());
   SF_CHECK_CUDA(cudaDeviceSynchronize());
   *handle = h;
@@ -1219,6 +1253,7 @@ extern "C" int sf_ae_destroy(void* handle) {
   cudaFree(h->temb_tau_dev);
   cudaFree(h->a_wt);
   cudaFree(h->s_wt);
+  cudaFree(h->rope_t);
   if (h->temb_euler) cudaFree(h->temb_euler);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
   delete h;

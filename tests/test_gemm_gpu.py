@@ -74,3 +74,26 @@ def test_rms_row_scale_and_bf16_store(swap):
     ssq = torch.rand(8, M, device="cuda") * 100 + 1
     out, ref = _run(M, N, K, 208 if swap else 256, 0 if swap else 1, swap, kind=1, ssq=ssq)
     torch.testing.assert_close(out, ref, rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("M,N,K", [
+    (1024, 512, 1024),
+    (1500, 768, 2048),   # ragged last row tile; 3 feature tiles (odd pair count)
+    (4096, 2560, 1024),  # qkv-shaped; more tiles than CTA pairs
+])
+def test_pair_kernel(M, N, K):
+    """Batched shapes (bn = 256, >= 1024 rows) run on 2-SM CTA pairs
+    (tcgen05.mma.cta_group::2, gemm_pair_kernel)."""
+    import torch
+
+    out, ref = _run(M, N, K, 256, 1, swap=False)
+    torch.testing.assert_close(out, ref, rtol=2e-3, atol=2e-3)
+
+
+def test_pair_kernel_rms_bf16():
+    import torch
+
+    M, N, K = 2048, 1024, 1024
+    ssq = torch.rand(8, M, device="cuda") * 100 + 1
+    out, ref = _run(M, N, K, 256, 1, False, kind=1, ssq=ssq)
+    torch.testing.assert_close(out, ref, rtol=1e-2, atol=1e-2)
