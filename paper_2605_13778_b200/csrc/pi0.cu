@@ -260,7 +260,7 @@ struct VerifyEpiParams {
   int* out_result;     // [B][8]
 };
 
-__global__ void __launch_bounds__(256) verify_epi_kernel(const VerifyEpiParams p) {
+__global__ void __launch_bounds__(1024) verify_epi_kernel(const VerifyEpiParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   sm100::pdl_wait();
   const int e = blockIdx.x;
@@ -1105,7 +1105,7 @@ int enqueue_verify(Handle& h, Buffers& b, const sf_verify_cfg_t* cfg, cudaStream
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  rc = launch_pdl(verify_epi_kernel, dim3(b.B), dim3(256), smem, s, vp, pdl);
+  rc = launch_pdl(verify_epi_kernel, dim3(b.B), dim3(b.B <= 16 ? 1024 : 256), smem, s, vp, pdl);
   trace_mark(s);
   return rc;
 }
