@@ -302,10 +302,26 @@ def run_ours(args, rank, world, local):
             traffic = json.loads(prof.read_text()).get("gate_up_gemm_dram_bytes")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "kernel": "gemm_kernel (layer gate/up, normal orientation)",
+    roofline = {"bound": "tensor", "kernel": "gemm_pair_kernel<GEGLU> (layer gate/up, 2-SM CTA pairs)",
                 "achieved": gu_tflops, "peak": tc_peak, "unit": "TFLOP/s", "frac": gu_tflops / tc_peak,
                 "traffic": traffic, "peak_kind": f"{peak_kind} burst bf16",
                 "algorithmic_flops_per_launch": gu_flops, "ms_per_launch": gu_ms}
+
+    # whole-step tensor utilisation: algorithmic FLOPs of one speculative round
+    # for every env (draft MLP + 18-layer verify over K branches + head) / step time
+    T = cfg.seg_len
+    lay = cfg.width * (cfg.q_heads * cfg.head_dim + 2 * cfg.head_dim) + cfg.q_heads * cfg.head_dim * cfg.width \
+        + 2 * cfg.mlp * cfg.width + cfg.mlp * cfg.width
+    gemm_f = 2.0 * rows_alg * (cfg.layers * lay + cfg.width * D)
+    keys = K * ((cfg.prefix_len + 1) + H * (cfg.prefix_len + T))  # per env: state + action rows
+    attn_f = 4.0 * E * keys * cfg.q_heads * cfg.head_dim * cfg.layers
+    draft_f = 2.0 * E * (cfg.draft_in * cfg.draft_hidden + cfg.draft_hidden ** 2 + cfg.draft_hidden * H * D)
+    step_f = gemm_f + attn_f + draft_f
+    step_tflops = step_f / (ms / 1e3) / 1e12
+    roofline_step = {"bound": "tensor", "kernel": "whole speculative-round step (all kernels)",
+                     "achieved": step_tflops, "peak": tc_sust, "unit": "TFLOP/s",
+                     "frac": step_tflops / tc_sust, "peak_kind": f"{peak_kind} sustained bf16",
+                     "algorithmic_flops_per_step": step_f, "gemm_flops": gemm_f, "attn_flops": attn_f}
 
     line = {
         "metric": METRIC, "value": value, "unit": "rounds/s", "n_gpus": world, "steps": args.steps,
@@ -318,6 +334,7 @@ def run_ours(args, rank, world, local):
                    "l2": "inputs larger than L2 (627 MB weights + 14.7 MB KV per env per step)",
                    "parallelism": f"envs sharded dp{world}, no hot-path collective"},
         "roofline": roofline,
+        "roofline_step": roofline_step,
         "decisions": {"flash_accepted": counts[0], "flash_rejected_fallback": counts[1],
                       "flash_phase_fallback": counts[2]},
         "e2e": {"value": args.envs / (e2e_ms / 1e3),

@@ -694,7 +694,28 @@ int build(Handle& h, Buffers& b, int B, int K) {
   // depends on the token count, so each layer GEMM class (qkv, o, gu, down --
   // identical across layers) is timed over a small (bn, splits) grid on this
   // device and every layer is re-planned with the winner.
-  if (swap && getenv("SF_NO_TUNE") == nullptr) {
+  // Default (deterministic across processes): a static rule distilled from the
+  // measured (bn, splits) sweeps (scripts/gemm_sweep.py sweep): above 128
+  // token rows use two token tiles (weights re-read from L2 beat fp32 partials),
+  // then as many K splits as keep one wave with clusters <= 6 CTAs (8- and
+  // 16-CTA clusters schedule poorly). SF_TUNE=1 times candidates instead.
+  if (swap && getenv("SF_TUNE") == nullptr) {
+    const int bn = b.M > 128 ? (((b.M + 1) / 2 + 15) / 16) * 16 : bn_swap;
+    const int tiles_b = (b.M + bn - 1) / bn;
+    for (int cls = 0; cls < 4; ++cls) {
+      const Spec& sp = specs[cls];
+      const int tiles = ((sp.n_out + gemm::BM - 1) / gemm::BM) * tiles_b, nkb = sp.k_in / gemm::BK;
+      int S = nsm / tiles;
+      S = S > 6 ? 6 : (S < 1 ? 1 : S);
+      S = S > nkb ? nkb : S;
+      for (int l = 0; l < L; ++l) {
+        const Spec& q = specs[4 * l + cls];
+        if ((rc = gemm::plan(&b.ops[4 * l + cls], q.wt, q.n_out, q.k_in, q.act, b.M, q.k_in, q.k_in,
+                             bn, S, 1, q.e)))
+          return rc;
+      }
+    }
+  } else if (swap && getenv("SF_NO_TUNE") == nullptr) {
     cudaStream_t ts;
     SF_CHECK_CUDA(cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking));
     cudaEvent_t e0, e1;
