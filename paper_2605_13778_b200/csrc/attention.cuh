@@ -121,16 +121,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sP = sKV + 2 * kStageBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kPBytes);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* k_full = bars + 1;    // [2] K half of a stage landed
+  uint64_t* k_empty = bars + 3;   // [2] S(i) retired: K slot free
   uint64_t* s_full = bars + 5;    // [2]
   uint64_t* s_free = bars + 7;    // [2]
   uint64_t* p_full = bars + 9;    // [2]
   uint64_t* pv_done = bars + 11;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* v_full = bars + 13;   // [2] V^T half landed
+  uint64_t* v_empty = bars + 15;  // [2] PV(i) retired: V slot free
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
   __shared__ unsigned long long stamps[16];
   (void)stamps;
+#ifdef SF_TRACE
+  __shared__ unsigned long long bt[6][16];  // per key block: kv_full, S commit, s_full seen, p arrive, PV commit, pv seen
+#define BT(k, i)                                                  \
+  do {                                                            \
+    unsigned long long _t;                                        \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));        \
+    if ((i) < 16) bt[k][i] = _t;                                  \
+  } while (0)
+#else
+#define BT(k, i) \
+  do {           \
+  } while (0)
+#endif
   if (threadIdx.x == 0) ATT_STAMP(0);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -149,8 +164,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     sm100::mbar_init(q_full, 1);
     for (int s = 0; s < 2; ++s) {
-      sm100::mbar_init(&kv_full[s], 1);
-      sm100::mbar_init(&kv_empty[s], 1);
+      sm100::mbar_init(&k_full[s], 1);
+      sm100::mbar_init(&k_empty[s], 1);
+      sm100::mbar_init(&v_full[s], 1);
+      sm100::mbar_init(&v_empty[s], 1);
       sm100::mbar_init(&s_full[s], 1);
       sm100::mbar_init(&s_free[s], 256);
     }
@@ -176,35 +193,63 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::tma_prefetch_desc(&tm_ks);
       sm100::tma_prefetch_desc(&tm_vs);
       const uint64_t pol_keep = sm100::policy_evict_last();
-      auto load_block = [&](int i, bool prefix_only) -> bool {
+      // K and V^T halves of a key block are separate slots: K(i) reuses the
+      // slot of K(i-2) once S(i-2) retired, V(i) the slot of V(i-2) once
+      // PV(i-2) retired, so S(i) never waits behind the PV chain.
+      auto load_k = [&](int i) {
         const int j = j0 + i;
-        const bool is_prefix = j < p.n_prefix_blocks;
-        if (prefix_only && !is_prefix) return false;
         const int s = i & 1;
         uint8_t* st = sKV + s * kStageBytes;
-        sm100::mbar_arrive_expect_tx(&kv_full[s], kStageBytes);
-        if (is_prefix) {
+        sm100::mbar_arrive_expect_tx(&k_full[s], kKBytes);
+        if (j < p.n_prefix_blocks) {
           for (int c = 0; c < 4; ++c)
-            tma_load_3d(&tm_kp, &kv_full[s], st + c * (BKEY * 128), c * 64, j * BKEY, env, pol_keep);
-          tma_load_3d(&tm_vp, &kv_full[s], st + kKBytes, j * BKEY, 0, env, pol_keep);
+            tma_load_3d(&tm_kp, &k_full[s], st + c * (BKEY * 128), c * 64, j * BKEY, env, pol_keep);
         } else {
           const int row0 = sb + (j - p.n_prefix_blocks) * BKEY;
           for (int c = 0; c < 4; ++c)
-            sm100::tma_load_2d(&tm_ks, &kv_full[s], st + c * (BKEY * 128), c * 64, row0, pol_keep);
-          sm100::tma_load_2d(&tm_vs, &kv_full[s], st + kKBytes, row0, 0, pol_keep);
+            sm100::tma_load_2d(&tm_ks, &k_full[s], st + c * (BKEY * 128), c * 64, row0, pol_keep);
         }
-        return true;
+      };
+      auto load_v = [&](int i) {
+        const int j = j0 + i;
+        const int s = i & 1;
+        uint8_t* st = sKV + s * kStageBytes + kKBytes;
+        sm100::mbar_arrive_expect_tx(&v_full[s], kVBytes);
+        if (j < p.n_prefix_blocks) {
+          tma_load_3d(&tm_vp, &v_full[s], st, j * BKEY, 0, env, pol_keep);
+        } else {
+          const int row0 = sb + (j - p.n_prefix_blocks) * BKEY;
+          sm100::tma_load_2d(&tm_vs, &v_full[s], st, row0, 0, pol_keep);
+        }
       };
       // prefix K/V do not depend on the previous kernel: issue before the PDL wait
-      int issued = 0;
-      while (issued < min(2, nb) && load_block(issued, true)) ++issued;
+      int nk = 0, nv = 0;
+      while (nk < min(2, nb) && j0 + nk < p.n_prefix_blocks) {
+        load_k(nk);
+        load_v(nk);
+        ++nk;
+        ++nv;
+      }
       sm100::pdl_wait();
       sm100::mbar_arrive_expect_tx(q_full, kQBytes);
       for (int c = 0; c < 4; ++c)
         sm100::tma_load_2d(&tm_q, q_full, sQ + c * (BQ * 128), c * 64, m0 * kHeads, pol_keep);
-      for (int i = issued; i < nb; ++i) {
-        if (i >= 2) sm100::mbar_wait(&kv_empty[i & 1], ((i >> 1) & 1) ^ 1);
-        load_block(i, false);
+      // two independent streams, issued in readiness order (polling)
+      const long long t0 = clock64();
+      while (nk < nb || nv < nb) {
+        if (nk < nb && (nk < 2 || sm100::mbar_try_wait(sm100::smem_u32(&k_empty[nk & 1]), ((nk >> 1) & 1) ^ 1))) {
+          load_k(nk);
+          ++nk;
+        }
+        if (nv < nb && nv < nk &&
+            (nv < 2 || sm100::mbar_try_wait(sm100::smem_u32(&v_empty[nv & 1]), ((nv >> 1) & 1) ^ 1))) {
+          load_v(nv);
+          ++nv;
+        }
+        if (clock64() - t0 > (1ll << 33)) {
+          printf("sf: attention producer timeout (block %d)\n", blockIdx.x);
+          __trap();
+        }
       }
     }
   } else if (warp == 1) {
@@ -218,6 +263,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_pv = [&](int i) {
         sm100::mbar_wait(&p_full[i & 1], (i >> 1) & 1);
         sm100::tc_fence_after();
+        sm100::mbar_wait(&v_full[i & 1], (i >> 1) & 1);
+        sm100::tc_fence_after();
         const uint32_t v_addr = sm100::smem_u32(sKV + (i & 1) * kStageBytes + kKBytes);
         const uint32_t pb = p_addr;
 #pragma unroll
@@ -225,11 +272,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::umma_bf16(tmem + 128, sm100::make_sw128_desc(pb + kk * 32),
                            sm100::make_sw128_desc(v_addr + kk * 32), idesc_o, (i | kk) != 0);
         sm100::umma_commit(&pv_done[i & 1]);
-        sm100::umma_commit(&kv_empty[i & 1]);
+        sm100::umma_commit(&v_empty[i & 1]);
+        BT(4, i);
       };
       for (int i = 0; i < nb; ++i) {
         const int s = i & 1;
-        sm100::mbar_wait(&kv_full[s], (i >> 1) & 1);
+        sm100::mbar_wait(&k_full[s], (i >> 1) & 1);
+        BT(0, i);
         if (i >= 2) sm100::mbar_wait(&s_free[s], ((i >> 1) & 1) ^ 1);
         sm100::tc_fence_after();
         const uint32_t k_addr = sm100::smem_u32(sKV + s * kStageBytes);
@@ -241,6 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                            kk != 0);
         }
         sm100::umma_commit(&s_full[s]);
+        sm100::umma_commit(&k_empty[s]);
+        BT(1, i);
         if (i >= 1) issue_pv(i - 1);
       }
       if (nb > 0) issue_pv(nb - 1);
@@ -272,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int j = j0 + i;
       const int s = i & 1;
       sm100::mbar_wait(&s_full[s], (i >> 1) & 1);
+      if (threadIdx.x == 64) BT(2, i);
       sm100::tc_fence_after();
       uint32_t raw[2][16];
 #pragma unroll
@@ -318,8 +370,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // P(i) overwrites P(i-1) and O may be rescaled: PV(i-1) must be done
       // (both warps of a pair decide the rescale alike)
+      // exponentials first (registers): only the P store and an O rescale
+      // have to wait for PV(i-1), so the MUFU work overlaps it
+      const float mu = m_used == -INFINITY ? 0.f : m_used;
+      uint32_t pw[16];
+      float lp = 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float p0 = exp2f(fmaf(sv[2 * k], p.scale_log2, -mu));
+        const float p1 = exp2f(fmaf(sv[2 * k + 1], p.scale_log2, -mu));
+        lp += p0 + p1;
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+        pw[k] = *reinterpret_cast<uint32_t*>(&b2);
+      }
       if (i >= 1) {
         sm100::mbar_wait(&pv_done[(i - 1) & 1], ((i - 1) >> 1) & 1);
+        if (threadIdx.x == 64) BT(5, i - 1);
         sm100::tc_fence_after();
       }
       const bool any_rescale = __any_sync(0xffffffffu, rescale);
@@ -341,24 +407,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       // P row half (32 keys, bf16) into the SWIZZLE_128B K-major tile: 16 B
       // chunk c of row r lives at chunk (c ^ (r & 7)). p = 2^(x*scale - m).
       uint8_t* prow = sP + r * 128;
-      const float mu = m_used == -INFINITY ? 0.f : m_used;
+      l_sum += lp;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t w[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float p0 = exp2f(fmaf(sv[c * 8 + 2 * k], p.scale_log2, -mu));
-          const float p1 = exp2f(fmaf(sv[c * 8 + 2 * k + 1], p.scale_log2, -mu));
-          l_sum += p0 + p1;
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-          w[k] = *reinterpret_cast<uint32_t*>(&b2);
-        }
         const int cc = half * 4 + c;
-        *reinterpret_cast<uint4*>(prow + ((cc ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(prow + ((cc ^ (r & 7)) << 4)) =
+            make_uint4(pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
       }
       fence_async_smem();
       sm100::tc_fence_before();
       sm100::mbar_arrive(&p_full[i & 1]);
+      if (threadIdx.x == 64) BT(3, i);
     }
     // ---- epilogue: O row (256 fp32) is final once the last PV retires
     if (nb > 0) {
@@ -551,8 +610,370 @@ __global__ void __launch_bounds__(kThreads, 1)
            (stamps[3] - stamps[0]) * 1e-3, (stamps[4] - stamps[0]) * 1e-3, (stamps[5] - stamps[0]) * 1e-3,
            (stamps[6] - stamps[0]) * 1e-3, (stamps[7] - stamps[0]) * 1e-3, (stamps[8] - stamps[0]) * 1e-3,
            (stamps[9] - stamps[0]) * 1e-3);
+    if (gridDim.y == 1)
+      for (int i = 0; i < 16 && i < nb; ++i)
+        printf("  blk %d: kv_full %.2f S_commit %.2f s_seen %.2f p_arrive %.2f PV_commit %.2f pv_seen %.2f\n", i,
+               (bt[0][i] - stamps[0]) * 1e-3, (bt[1][i] - stamps[0]) * 1e-3, (bt[2][i] - stamps[0]) * 1e-3,
+               (bt[3][i] - stamps[0]) * 1e-3, (bt[4][i] - stamps[0]) * 1e-3,
+               i + 1 < nb ? (bt[5][i] - stamps[0]) * 1e-3 : -1.0);
   }
 #endif
+}
+
+// ------------------------------------------------ batched: 2-SM CTA pairs
+//
+// attn_pair_kernel: two consecutive query tiles of one env run on a CTA pair
+// (cluster of 2) with tcgen05.mma.cta_group::2: S = Q K^T is one 256 x 64
+// MMA per key block and O += P V one 256 x 256 MMA, each CTA holding its own
+// 128 query rows (Q, P, S and O in its TMEM) but only HALF of every key block
+// (32 keys of K, 128 dims of V^T): 32 KB per block per SM instead of 64 KB,
+// so the same SMEM holds a 4-deep K/V ring. The K/V stream (L2 -> SMEM,
+// ~93 GB/s per SM) and its latency, not the tensor pipe, bound the 1-SM
+// kernel. The leader (rank 0) issues every MMA; its barriers count both
+// CTAs' TMA bytes and both CTAs' softmax arrivals; commits are multicast.
+// Splits == 1 only (batched rounds). Tiles pair up inside an env; an odd last
+// tile is paired with a dummy partner whose rows are computed and dropped.
+
+constexpr int kPairStages = 4;
+constexpr uint32_t kPairKBytes = 32 * HD * 2;     // 16 KB: 32 keys x 256 dims (4 chunks of 32 x 64)
+constexpr uint32_t kPairVBytes = (HD / 2) * BKEY * 2;  // 16 KB: 128 dims x 64 keys
+constexpr uint32_t kPairStageBytes = kPairKBytes + kPairVBytes;
+constexpr uint32_t kPairSmemBytes = kQBytes + kPairStages * kPairStageBytes + kPBytes + kCtlBytes + 1024;
+
+__device__ __forceinline__ uint32_t pair_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t pair_mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void pair_load_2d(const CUtensorMap* m, uint32_t bar, void* dst, int c0, int c1,
+                                             uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.cta_group::2.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(sm100::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void pair_load_3d(const CUtensorMap* m, uint32_t bar, void* dst, int c0, int c1,
+                                             int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.cta_group::2.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(sm100::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void pair_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void pair_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          sm100::smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void pair_arrive(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kp,
+                     const __grid_constant__ CUtensorMap tm_vp, const __grid_constant__ CUtensorMap tm_ks,
+                     const __grid_constant__ CUtensorMap tm_vs, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + kQBytes;  // kPairStages x [K half 16 KB | V^T half 16 KB]
+  uint8_t* sP = sKV + kPairStages * kPairStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kPBytes);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;    // [4]
+  uint64_t* kv_empty = bars + 5;   // [4]
+  uint64_t* s_full = bars + 9;     // [2]
+  uint64_t* s_free = bars + 11;    // [2]
+  uint64_t* p_full = bars + 13;    // [2]
+  uint64_t* pv_done = bars + 15;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  float* xm = reinterpret_cast<float*>(bars + 32);  // softmax pair exchange [2][2][128]
+  cg::cluster_group cluster = cg::this_cluster();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = pair_rank();
+  const bool leader = rank == 0;
+  const int tiles_env = p.env_rows / 16;
+  const int pairs_env = (tiles_env + 1) / 2;
+  const int pr = blockIdx.x >> 1;
+  const int env = pr / pairs_env, jp = pr - env * pairs_env;
+  const int tloc = 2 * jp + (int)rank;  // tile inside the env
+  const bool valid = tloc < tiles_env;
+  const int env_start = env * p.env_rows;
+  const int m0 = env_start + tloc * 16;  // first token of this CTA's tile (dummy: next env)
+  // shared key blocks: suffix blocks cover the segments of the pair's 32 tokens
+  const int pair_m0 = env_start + 2 * jp * 16;
+  const int seg_first = (pair_m0 - env_start) / p.seg_len;
+  const int sb = (env_start + seg_first * p.seg_len) & ~(BKEY - 1);
+  const int nb = p.n_blocks;
+
+  if (warp == 0 && lane == 0) {
+    sm100::mbar_init(q_full, 1);
+    for (int s = 0; s < kPairStages; ++s) {
+      sm100::mbar_init(&kv_full[s], 1);
+      sm100::mbar_init(&kv_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      sm100::mbar_init(&s_full[b], 1);
+      sm100::mbar_init(&s_free[b], 2 * 256);
+      sm100::mbar_init(&p_full[b], 2 * 256);
+      sm100::mbar_init(&pv_done[b], 1);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        sm100::smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  sm100::tc_fence_before();
+  cluster.sync();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (sm100::elect_one()) {
+      sm100::tma_prefetch_desc(&tm_q);
+      sm100::tma_prefetch_desc(&tm_kp);
+      sm100::tma_prefetch_desc(&tm_vp);
+      sm100::tma_prefetch_desc(&tm_ks);
+      sm100::tma_prefetch_desc(&tm_vs);
+      const uint64_t pol = sm100::policy_evict_last();
+      auto load_block = [&](int i, bool prefix_only) -> bool {
+        const int j = i;
+        const bool is_prefix = j < p.n_prefix_blocks;
+        if (prefix_only && !is_prefix) return false;
+        const int s = i % kPairStages;
+        uint8_t* st = sKV + s * kPairStageBytes;
+        const uint32_t fb = pair_mapa(sm100::smem_u32(&kv_full[s]), 0);
+        if (leader) sm100::mbar_arrive_expect_tx(&kv_full[s], 2 * kPairStageBytes);
+        if (is_prefix) {
+          for (int c = 0; c < 4; ++c)
+            pair_load_3d(&tm_kp, fb, st + c * (32 * 128), c * 64, j * BKEY + rank * 32, env, pol);
+          pair_load_3d(&tm_vp, fb, st + kPairKBytes, j * BKEY, rank * (HD / 2), env, pol);
+        } else {
+          const int row0 = sb + (j - p.n_prefix_blocks) * BKEY;
+          for (int c = 0; c < 4; ++c)
+            pair_load_2d(&tm_ks, fb, st + c * (32 * 128), c * 64, row0 + rank * 32, pol);
+          pair_load_2d(&tm_vs, fb, st + kPairKBytes, row0, rank * (HD / 2), pol);
+        }
+        return true;
+      };
+      int issued = 0;
+      while (issued < min(kPairStages, nb) && load_block(issued, true)) ++issued;
+      sm100::pdl_wait();
+      const uint32_t qb = pair_mapa(sm100::smem_u32(q_full), 0);
+      if (leader) sm100::mbar_arrive_expect_tx(q_full, 2 * kQBytes);
+      for (int c = 0; c < 4; ++c)
+        pair_load_2d(&tm_q, qb, sQ + c * (BQ * 128), c * 64, m0 * kHeads, pol);
+      for (int i = issued; i < nb; ++i) {
+        if (i >= kPairStages) sm100::mbar_wait(&kv_empty[i % kPairStages], ((i / kPairStages) & 1) ^ 1);
+        load_block(i, false);
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && sm100::elect_one()) {
+      const uint32_t idesc_s = sm100::make_idesc_bf16(256, BKEY);
+      const uint32_t idesc_o = sm100::make_idesc_bf16(256, HD);
+      const uint32_t q_addr = sm100::smem_u32(sQ);
+      const uint32_t p_addr = sm100::smem_u32(sP);
+      sm100::mbar_wait(q_full, 0);
+      auto issue_pv = [&](int i) {
+        sm100::mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+        sm100::tc_fence_after();
+        const uint32_t v_addr = sm100::smem_u32(sKV + (i % kPairStages) * kPairStageBytes + kPairKBytes);
+#pragma unroll
+        for (int kk = 0; kk < BKEY / 16; ++kk)
+          pair_mma(tmem + 128, sm100::make_sw128_desc(p_addr + kk * 32),
+                   sm100::make_sw128_desc(v_addr + kk * 32), idesc_o, (i | kk) != 0);
+        pair_commit(&pv_done[i & 1]);
+        pair_commit(&kv_empty[i % kPairStages]);
+      };
+      for (int i = 0; i < nb; ++i) {
+        const int s = i % kPairStages, b = i & 1;
+        sm100::mbar_wait(&kv_full[s], (i / kPairStages) & 1);
+        if (i >= 2) sm100::mbar_wait(&s_free[b], ((i >> 1) & 1) ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t k_addr = sm100::smem_u32(sKV + s * kPairStageBytes);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const int c = kk >> 2, w = kk & 3;
+          pair_mma(tmem + b * BKEY, sm100::make_sw128_desc(q_addr + c * (BQ * 128) + w * 32),
+                   sm100::make_sw128_desc(k_addr + c * (32 * 128) + w * 32), idesc_s, kk != 0);
+        }
+        pair_commit(&s_full[b]);
+        if (i >= 1) issue_pv(i - 1);
+      }
+      if (nb > 0) issue_pv(nb - 1);
+    }
+    __syncwarp();
+  } else {
+    // softmax (as attn_kernel: 2 warps per TMEM lane quarter, column halves)
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
+    const int tok = m0 + (r >> 3);
+    const int head = r & 7;
+    const int local_q = tok - env_start;
+    const int seg_q = local_q / p.seg_len;
+    const int t_q = local_q - seg_q * p.seg_len;
+    const bool real_q = valid && local_q < p.segs * p.seg_len && tok < p.M;
+    const int seg_lo = seg_q * p.seg_len;
+    const int seg_hi = seg_lo + (t_q >= 1 ? p.seg_len : 1);
+    const uint32_t sfree_l = pair_mapa(sm100::smem_u32(s_free), 0);
+    const uint32_t pfull_l = pair_mapa(sm100::smem_u32(p_full), 0);
+    float m_used = -INFINITY, l_sum = 0.f;
+    sm100::pdl_wait();
+    if (threadIdx.x == 64) sm100::pdl_launch_dependents();
+    for (int i = 0; i < nb; ++i) {
+      const int j = i;
+      const int b = i & 1;
+      sm100::mbar_wait(&s_full[b], (i >> 1) & 1);
+      sm100::tc_fence_after();
+      uint32_t raw[2][16];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) sm100::tmem_ld16(t_lane + b * BKEY + half * 32 + c * 16, raw[c]);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      pair_arrive(sfree_l + b * 8);
+      int lo = 0, hi;
+      if (j < p.n_prefix_blocks) {
+        hi = p.prefix_len - j * BKEY;
+      } else if (real_q) {
+        const int base = sb + (j - p.n_prefix_blocks) * BKEY - env_start;
+        lo = seg_lo - base;
+        hi = seg_hi - base;
+      } else {
+        hi = 0;
+      }
+      lo -= half * 32;
+      hi -= half * 32;
+      float sv[32];
+      float mb = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const float x = __uint_as_float(raw[c >> 4][c & 15]);
+        sv[c] = (c >= lo && c < hi) ? x : -INFINITY;
+        mb = fmaxf(mb, sv[c]);
+      }
+      xm[(b * 2 + half) * BQ + r] = mb;
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+      mb = fmaxf(xm[(b * 2) * BQ + r], xm[(b * 2 + 1) * BQ + r]) * p.scale_log2;
+      const float m_new = fmaxf(m_used, mb);
+      bool rescale = false;
+      float alpha = 1.f;
+      if (m_new > -INFINITY) {
+        if (m_used == -INFINITY) {
+          m_used = m_new;
+        } else if (m_new > m_used + 8.f) {
+          alpha = exp2f(m_used - m_new);
+          m_used = m_new;
+          rescale = true;
+        }
+      }
+      // exponentials first (registers): only the P store and an O rescale
+      // have to wait for PV(i-1), so the MUFU work overlaps it
+      const float mu = m_used == -INFINITY ? 0.f : m_used;
+      uint32_t pw[16];
+      float lp = 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float p0 = exp2f(fmaf(sv[2 * k], p.scale_log2, -mu));
+        const float p1 = exp2f(fmaf(sv[2 * k + 1], p.scale_log2, -mu));
+        lp += p0 + p1;
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+        pw[k] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      if (i >= 1) {
+        sm100::mbar_wait(&pv_done[(i - 1) & 1], ((i - 1) >> 1) & 1);
+        sm100::tc_fence_after();
+      }
+      const bool any_rescale = __any_sync(0xffffffffu, rescale);
+      if (any_rescale && i >= 1) {
+        l_sum *= alpha;
+#pragma unroll 1
+        for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 16) {
+          uint32_t o[16];
+          sm100::tmem_ld16(t_lane + 128 + c0, o);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 16; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+          sm100::tmem_st16(t_lane + 128 + c0, o);
+        }
+        sm100::tmem_st_wait();
+      } else if (rescale) {
+        l_sum *= alpha;
+      }
+      uint8_t* prow = sP + r * 128;
+      l_sum += lp;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int cc = half * 4 + c;
+        *reinterpret_cast<uint4*>(prow + ((cc ^ (r & 7)) << 4)) =
+            make_uint4(pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
+      }
+      fence_async_smem();
+      sm100::tc_fence_before();
+      pair_arrive(pfull_l + b * 8);
+    }
+    if (nb > 0) {
+      sm100::mbar_wait(&pv_done[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
+      sm100::tc_fence_after();
+    }
+    {
+      const int ps = nb & 1;
+      xm[(ps * 2 + half) * BQ + r] = l_sum;
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+      l_sum = xm[(ps * 2) * BQ + r] + xm[(ps * 2 + 1) * BQ + r];
+    }
+    const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
+    __nv_bfloat16* dst = p.out + (size_t)tok * (kHeads * HD) + head * HD;
+    for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 32) {
+      uint32_t o[2][16];
+      sm100::tmem_ld16(t_lane + 128 + c0, o[0]);
+      sm100::tmem_ld16(t_lane + 128 + c0 + 16, o[1]);
+      sm100::tmem_ld_wait();
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        uint32_t w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[u][2 * k]) * inv,
+                                                    __uint_as_float(o[u][2 * k + 1]) * inv);
+          w[k] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        if (valid && tok < p.M) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + c0 + 16 * u);
+          d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  cluster.sync();  // the peer's barriers / TMEM are no longer referenced
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
 }
 
 }  // namespace attn

@@ -385,6 +385,8 @@ struct Buffers {
   attn::Params ap{};
   int attn_tiles = 0, attn_splits = 1;
   std::vector<CUtensorMap> attn_maps;  // per layer: q, kp, vp, ks, vs
+  std::vector<CUtensorMap> attn_pair_maps;  // 2-SM pair kernel: half-block boxes (batched)
+  bool attn_pair = false;
   cudaGraphExec_t graph = nullptr;
   int graph_key = 0;
   int graph_kernels = 0;  // kernel nodes in `graph` (launch accounting)
@@ -841,6 +843,28 @@ int build(Handle& h, Buffers& b, int B, int K) {
     if ((rc = gemm::make_map(&mp[3], b.ks, b.M, c.head_dim, c.head_dim, attn::BKEY))) return rc;
     if ((rc = gemm::make_map(&mp[4], b.vt, c.head_dim, b.m_ld, b.m_ld, c.head_dim))) return rc;
   }
+  // 2-SM attention for batched rounds (one split): each CTA of a pair loads
+  // half of every key block (32 keys of K, 128 dims of V^T)
+  // (opt-in, SF_ATTN_PAIR=1: measured slower than the 1-SM kernel with split
+  // K/V slots -- the key-block chain is latency-, not ingress-bound)
+  b.attn_pair = b.attn_splits == 1 && b.env_rows / 16 >= 2 && getenv("SF_ATTN_PAIR") != nullptr;
+  if (b.attn_pair) {
+    b.attn_pair_maps.resize(5 * L);
+    for (int l = 0; l < L; ++l) {
+      CUtensorMap* mp = &b.attn_pair_maps[5 * l];
+      mp[0] = b.attn_maps[5 * l];
+      const bf16* kp = h.k_prefix + (size_t)l * E * c.prefix_len * c.head_dim;
+      const bf16* vp = h.vt_prefix + (size_t)l * E * c.head_dim * c.prefix_len;
+      if ((rc = make_map_3d(&mp[1], kp, c.head_dim, c.prefix_len, E, (uint64_t)c.head_dim * 2,
+                            (uint64_t)c.prefix_len * c.head_dim * 2, 64, 32)))
+        return rc;
+      if ((rc = make_map_3d(&mp[2], vp, c.prefix_len, c.head_dim, E, (uint64_t)c.prefix_len * 2,
+                            (uint64_t)c.prefix_len * c.head_dim * 2, attn::BKEY, c.head_dim / 2)))
+        return rc;
+      if ((rc = gemm::make_map(&mp[3], b.ks, b.M, c.head_dim, c.head_dim, 32))) return rc;
+      if ((rc = gemm::make_map(&mp[4], b.vt, c.head_dim, b.m_ld, b.m_ld, c.head_dim / 2))) return rc;
+    }
+  }
   // --- batch-1 layer-stack megakernel: phases, tensor maps, counters
   if (want_stack && b.attn_tiles * b.attn_splits <= nsm && b.attn_tiles <= stack::kMaxTileSlots) {
     const uint32_t b_bytes = (uint32_t)bn_swap * gemm::BK * 2;
@@ -985,7 +1009,38 @@ int launch_stack(const Buffers& b, cudaStream_t s, bool pdl) {
   return SF_OK;
 }
 
+int launch_attn_pair(const Buffers& b, int l, cudaStream_t s, bool pdl) {
+  static bool attr = false;
+  if (!attr) {
+    SF_CHECK_CUDA(cudaFuncSetAttribute(attn::attn_pair_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)attn::kPairSmemBytes));
+    attr = true;
+  }
+  const CUtensorMap* mp = &b.attn_pair_maps[5 * l];
+  const int tiles_env = b.env_rows / 16;
+  const int pairs = b.B * ((tiles_env + 1) / 2);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(attn::kThreads);
+  cfg.dynamicSmemBytes = attn::kPairSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute a[2];
+  a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  a[1].id = cudaLaunchAttributeClusterDimension;
+  a[1].val.clusterDim.x = 2;
+  a[1].val.clusterDim.y = 1;
+  a[1].val.clusterDim.z = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 2;
+  SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, attn::attn_pair_kernel, mp[0], mp[1], mp[2], mp[3], mp[4], b.ap));
+  count_launch();
+  return SF_OK;
+}
+
 int launch_attn(const Buffers& b, int l, cudaStream_t s, bool pdl) {
+  if (b.attn_pair) return launch_attn_pair(b, l, s, pdl);
   static bool attr = false;
   if (!attr) {
     SF_CHECK_CUDA(cudaFuncSetAttribute(attn::attn_kernel,

@@ -217,3 +217,36 @@ def test_full_size_cfg3_verify_vs_oracle():
                                atol=1e-2 * scale)
     if tuple(branch[0].cpu().numpy()) != ref["branch_prefixes"]:
         assert np.abs(ref["distances"] - 4.0).min() < 5e-2
+
+
+def test_attention_pair_kernel_matches_single_sm():
+    """Batched rounds (one KV split) run attention on 2-SM CTA pairs
+    (attn_pair_kernel, odd tile counts paired with a dummy partner); it must
+    agree with the 1-SM kernel on the same inputs."""
+    import os
+
+    import torch
+
+    from paper_2605_13778_b200 import pi0
+    from paper_2605_13778_b200.verifier import VerifierConfig
+
+    _, dcfg = _pair()
+    E = 64  # 3 query tiles per env, 192 tiles -> one KV split per tile
+    rng = np.random.default_rng(11)
+    H, D, S = dcfg.horizon, dcfg.action_dim, dcfg.state_dim
+    d = torch.from_numpy(rng.standard_normal((E, H, D)).astype(np.float32)).cuda()
+    e = torch.from_numpy(rng.standard_normal((E, H, D)).astype(np.float32)).cuda()
+    s = torch.from_numpy(rng.standard_normal((E, S)).astype(np.float32)).cuda()
+    cfg = VerifierConfig(timesteps=(0.2, 0.4, 0.6, 0.8), delta=0.5)
+    outs = []
+    for flag in (None, "1"):
+        if flag:
+            os.environ["SF_ATTN_PAIR"] = flag
+        else:
+            os.environ.pop("SF_ATTN_PAIR", None)
+        ae = pi0.ActionExpert(dcfg, seed=0, n_envs=E, kv_seed=1)
+        outs.append([t.clone() for t in ae.verify_batch(cfg, d, e, s)])
+    os.environ.pop("SF_ATTN_PAIR", None)
+    (r0, d0, _, _), (r1, d1, _, _) = outs
+    torch.testing.assert_close(r1, r0, rtol=2e-3, atol=2e-3 * r0.abs().max().item())
+    torch.testing.assert_close(d1, d0, rtol=2e-3, atol=2e-3 * d0.abs().max().item())
