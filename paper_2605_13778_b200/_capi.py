@@ -20,6 +20,9 @@ SF_MAX_K = 16
 SF_METRIC = {"l2": 0, "linf": 1}
 SF_RESULT_WORDS = 8
 RES_PREFIX, RES_SWITCH, RES_PATH, RES_PLANNED, RES_NONFINITE = 0, 1, 2, 3, 4
+# specflow_b200.h: SF_PATH_* device path codes, SF_RES_* result word indices
+SF_PATH_FLASH_ACCEPTED, SF_PATH_FLASH_REJECTED, SF_PATH_FLASH_PHASE = 0, 1, 2
+SF_RES_PREFIX, SF_RES_SWITCH, SF_RES_PATH, SF_RES_PLANNED, SF_RES_NONFINITE = 0, 1, 2, 3, 4
 PATH_CODES = ("flash_accepted", "flash_rejected_fallback", "flash_phase_fallback")
 
 
