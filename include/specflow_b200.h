@@ -47,6 +47,8 @@ extern "C" {
 #define SF_PATH_FLASH_ACCEPTED 0
 #define SF_PATH_FLASH_REJECTED 1 /* "flash_rejected_fallback" */
 #define SF_PATH_FLASH_PHASE 2    /* "flash_phase_fallback" */
+#define SF_PATH_FULL 3           /* "full" (no cache yet, or full-only mode) */
+#define SF_PATH_PERIODIC 4       /* "periodic_refresh" (runtime.py:247-253, :263) */
 
 /* result words written by every verify entry point */
 #define SF_RES_PREFIX 0    /* min over branches (verifier.py:147) */
@@ -172,6 +174,23 @@ int sf_gripper_switch(int precision, const void* values, int n_chunks, int horiz
  * status[0] set to `step` on the first non-finite result (caller inits to -1). */
 int sf_euler_update(int precision, void* values, const void* velocity, int count, int n, int step,
                     int* status, void* stream);
+
+/* Device-side round bookkeeping of a batch of independent envs
+ * (run_episode, runtime.py:238-320), after a batched flash attempt:
+ *   forced = PF > 0 && fsr[e] >= PF;  use_flash = mode_flash && has_cache[e] && !forced
+ *   !use_flash            -> path FULL (PERIODIC if forced in flash mode), planned = R
+ *   flash rejected/phase  -> path from result[e] (SF_RES_PATH), planned = R
+ *   flash accepted        -> planned = result[e][SF_RES_PLANNED], fsr[e] += 1
+ *   every full round      -> fsr[e] = 0, has_cache[e] = 1
+ * Envs needing the full (Euler) path are compacted in env order into
+ * fb_idx[0 .. *fb_count) (one CTA, block scan: deterministic), so the Euler
+ * denoise runs on that bucket only (sf_ae_denoise_envs with env_map = fb_idx).
+ * result: [n_envs][SF_RESULT_WORDS] device words of the flash round (ignored
+ * where use_flash is 0); fsr, has_cache: [n_envs] in/out; path, planned,
+ * fb_idx: [n_envs] out; fb_count: [1] out. All device pointers. */
+int sf_replan_update(int n_envs, const int* result, int* fsr, int* has_cache, int mode_flash,
+                     int periodic_refresh, int replan_size, int* path, int* planned, int* fb_idx,
+                     int* fb_count, void* stream);
 
 #ifdef __cplusplus
 }

@@ -108,6 +108,13 @@ int sf_ae_profile_verify(void* handle, int n_envs, const sf_verify_cfg_t* cfg, c
 int sf_ae_denoise(void* handle, int n_envs, int num_steps, const float* start, const float* state,
                   float* chunk_out, int* status, int flags, void* stream);
 
+/* sf_ae_denoise on a compacted batch: batch env e attends to prefix-KV pool
+ * slot env_map[e] (device [n_envs], values in [0, n_prefix_envs); NULL =
+ * identity). Used for the fallback bucket of a batched replanning round
+ * (sf_replan_update). */
+int sf_ae_denoise_envs(void* handle, int n_envs, const int* env_map, int num_steps, const float* start,
+                       const float* state, float* chunk_out, int* status, int flags, void* stream);
+
 /* Field protocol: velocities for n_envs x rows states x [..][rows][H][D] at
  * taus[rows] (HOST). */
 int sf_ae_velocity(void* handle, int n_envs, int rows, const float* x, const double* taus,

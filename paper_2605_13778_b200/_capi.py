@@ -22,6 +22,7 @@ SF_RESULT_WORDS = 8
 RES_PREFIX, RES_SWITCH, RES_PATH, RES_PLANNED, RES_NONFINITE = 0, 1, 2, 3, 4
 # specflow_b200.h: SF_PATH_* device path codes, SF_RES_* result word indices
 SF_PATH_FLASH_ACCEPTED, SF_PATH_FLASH_REJECTED, SF_PATH_FLASH_PHASE = 0, 1, 2
+SF_PATH_FULL, SF_PATH_PERIODIC = 3, 4
 SF_RES_PREFIX, SF_RES_SWITCH, SF_RES_PATH, SF_RES_PLANNED, SF_RES_NONFINITE = 0, 1, 2, 3, 4
 PATH_CODES = ("flash_accepted", "flash_rejected_fallback", "flash_phase_fallback")
 
@@ -91,6 +92,8 @@ SIGNATURES = {
     "sf_ae_verify": (_I, [_P, _I, ctypes.POINTER(SfVerifyCfg), _P, _P, _P, _P,
                           ctypes.POINTER(SfVerifyOut), _I, _P]),
     "sf_ae_denoise": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, _P]),
+    "sf_ae_denoise_envs": (_I, [_P, _I, _P, _I, _P, _P, _P, _P, _I, _P]),
+    "sf_replan_update": (_I, [_I, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P]),
     "sf_ae_flash_round": (_I, [_P, _I, ctypes.POINTER(SfVerifyCfg), _P, _P, _P, _P,
                                ctypes.POINTER(SfVerifyOut), _I, _P]),
     "sf_ae_time_op": (_I, [_P, _I, _I, _I, _I, _P]),

@@ -61,6 +61,7 @@ struct Params {
   __nv_bfloat16* out;  // [M, 8*256]
   float* ws;           // [tiles][splits][128][HD + 2]
   int* counters;       // [tiles]
+  const int* env_map;  // [envs] prefix-KV pool slot of each batch env (compacted batches)
 };
 
 #ifdef SF_TRACE
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::tma_prefetch_desc(&tm_ks);
       sm100::tma_prefetch_desc(&tm_vs);
       const uint64_t pol_keep = sm100::policy_evict_last();
+      const int slot = p.env_map ? __ldg(p.env_map + env) : env;  // prefix-KV pool slot
       // K and V^T halves of a key block are separate slots: K(i) reuses the
       // slot of K(i-2) once S(i-2) retired, V(i) the slot of V(i-2) once
       // PV(i-2) retired, so S(i) never waits behind the PV chain.
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::mbar_arrive_expect_tx(&k_full[s], kKBytes);
         if (j < p.n_prefix_blocks) {
           for (int c = 0; c < 4; ++c)
-            tma_load_3d(&tm_kp, &k_full[s], st + c * (BKEY * 128), c * 64, j * BKEY, env, pol_keep);
+            tma_load_3d(&tm_kp, &k_full[s], st + c * (BKEY * 128), c * 64, j * BKEY, slot, pol_keep);
         } else {
           const int row0 = sb + (j - p.n_prefix_blocks) * BKEY;
           for (int c = 0; c < 4; ++c)
@@ -216,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* st = sKV + s * kStageBytes + kKBytes;
         sm100::mbar_arrive_expect_tx(&v_full[s], kVBytes);
         if (j < p.n_prefix_blocks) {
-          tma_load_3d(&tm_vp, &v_full[s], st, j * BKEY, 0, env, pol_keep);
+          tma_load_3d(&tm_vp, &v_full[s], st, j * BKEY, 0, slot, pol_keep);
         } else {
           const int row0 = sb + (j - p.n_prefix_blocks) * BKEY;
           sm100::tma_load_2d(&tm_vs, &v_full[s], st, row0, 0, pol_keep);
@@ -756,6 +758,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::tma_prefetch_desc(&tm_ks);
       sm100::tma_prefetch_desc(&tm_vs);
       const uint64_t pol = sm100::policy_evict_last();
+      const int slot = p.env_map ? __ldg(p.env_map + env) : env;  // prefix-KV pool slot
       auto load_block = [&](int i, bool prefix_only) -> bool {
         const int j = i;
         const bool is_prefix = j < p.n_prefix_blocks;
@@ -766,8 +769,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (leader) sm100::mbar_arrive_expect_tx(&kv_full[s], 2 * kPairStageBytes);
         if (is_prefix) {
           for (int c = 0; c < 4; ++c)
-            pair_load_3d(&tm_kp, fb, st + c * (32 * 128), c * 64, j * BKEY + rank * 32, env, pol);
-          pair_load_3d(&tm_vp, fb, st + kPairKBytes, j * BKEY, rank * (HD / 2), env, pol);
+            pair_load_3d(&tm_kp, fb, st + c * (32 * 128), c * 64, j * BKEY + rank * 32, slot, pol);
+          pair_load_3d(&tm_vp, fb, st + kPairKBytes, j * BKEY, rank * (HD / 2), slot, pol);
         } else {
           const int row0 = sb + (j - p.n_prefix_blocks) * BKEY;
           for (int c = 0; c < 4; ++c)

@@ -376,6 +376,8 @@ struct Buffers {
   int* branch = nullptr;   // [B][K]
   int* result = nullptr;   // [B][8]
   int* status = nullptr;   // [B][2] Euler status
+  int* env_map = nullptr;  // [B] prefix-KV pool slot per batch env (read by attention)
+  int* env_ident = nullptr;  // [B] identity map
   float* ws = nullptr;
   size_t ws_bytes = 0;
   int* counters = nullptr;
@@ -525,6 +527,14 @@ int build(Handle& h, Buffers& b, int B, int K) {
   ALLOC(b.branch, (size_t)B * K);
   ALLOC(b.result, (size_t)B * SF_RESULT_WORDS);
   ALLOC(b.status, (size_t)B * 2);
+  ALLOC(b.env_map, (size_t)B);
+  ALLOC(b.env_ident, (size_t)B);
+  {
+    std::vector<int> ident(B);
+    for (int i = 0; i < B; ++i) ident[i] = i;
+    SF_CHECK_CUDA(cudaMemcpy(b.env_ident, ident.data(), sizeof(int) * B, cudaMemcpyHostToDevice));
+    SF_CHECK_CUDA(cudaMemcpy(b.env_map, ident.data(), sizeof(int) * B, cudaMemcpyHostToDevice));
+  }
   const int b_ld = ((B + 63) / 64) * 64;
   b.has_draft = c.draft_in > 0 && h.w.draft_w[0] != nullptr;
   if (b.has_draft) {
@@ -825,7 +835,8 @@ int build(Handle& h, Buffers& b, int B, int K) {
   ap.scale_log2 = 1.4426950408889634f / sqrtf((float)c.head_dim);
   ap.out = b.attn;
   ap.ws = attn_ws;
-  ap.counters = b.counters;  // shared with split-K GEMMs: kernels are stream-ordered
+  ap.counters = b.counters;
+  ap.env_map = b.env_map;  // shared with split-K GEMMs: kernels are stream-ordered
   b.attn_maps.resize(5 * L);
   const int E = h.n_prefix_envs;
   for (int l = 0; l < L; ++l) {
@@ -1320,7 +1331,7 @@ extern "C" int sf_ae_destroy(void* handle) {
     if (b.graph) cudaGraphExecDestroy(b.graph);
     void* ptrs[] = {b.x, b.xb, b.ssq, b.q, b.ks, b.vt, b.attn, b.h, b.vel, b.draft, b.eps,
                     b.state, b.signs, b.recon, b.dist, b.branch, b.result, b.status, b.ws,
-                    b.counters, b.ap.ws, b.sws, b.d_maps, b.d_ctr};
+                    b.counters, b.ap.ws, b.sws, b.d_maps, b.d_ctr, b.env_map, b.env_ident};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -1349,7 +1360,7 @@ extern "C" int sf_ae_set_prefix(void* handle, const void* k_prefix, const void* 
     if (b.graph) cudaGraphExecDestroy(b.graph);
     void* ptrs[] = {b.x, b.xb, b.ssq, b.q, b.ks, b.vt, b.attn, b.h, b.vel, b.draft, b.eps,
                     b.state, b.signs, b.recon, b.dist, b.branch, b.result, b.status, b.ws,
-                    b.counters, b.ap.ws, b.sws, b.d_maps, b.d_ctr};
+                    b.counters, b.ap.ws, b.sws, b.d_maps, b.d_ctr, b.env_map, b.env_ident};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -1510,9 +1521,20 @@ extern "C" int sf_ae_profile_verify(void* handle, int n_envs, const sf_verify_cf
   return rc;
 }
 
+extern "C" int sf_ae_denoise_envs(void* handle, int n_envs, const int* env_map, int num_steps,
+                                  const float* start, const float* state, float* chunk_out,
+                                  int* status, int flags, void* stream);
+
 extern "C" int sf_ae_denoise(void* handle, int n_envs, int num_steps, const float* start,
                              const float* state, float* chunk_out, int* status, int flags,
                              void* stream) {
+  return sf_ae_denoise_envs(handle, n_envs, nullptr, num_steps, start, state, chunk_out, status,
+                            flags, stream);
+}
+
+extern "C" int sf_ae_denoise_envs(void* handle, int n_envs, const int* env_map, int num_steps,
+                                  const float* start, const float* state, float* chunk_out,
+                                  int* status, int flags, void* stream) {
   auto* h = static_cast<Handle*>(handle);
   SF_REQUIRE(h && start && state && chunk_out && status, "null argument");
   SF_REQUIRE(h->k_prefix, "no prefix KV bound (sf_ae_set_prefix)");
@@ -1537,6 +1559,10 @@ extern "C" int sf_ae_denoise(void* handle, int n_envs, int num_steps, const floa
     }
   }
   const size_t hd = (size_t)n_envs * c.horizon * c.action_dim;
+  // batch env e attends to pool slot env_map[e] (fallback envs compacted by
+  // sf_replan_update); identity when no map is given
+  SF_CHECK_CUDA(cudaMemcpyAsync(b->env_map, env_map ? env_map : b->env_ident, sizeof(int) * n_envs,
+                                cudaMemcpyDeviceToDevice, s));
   SF_CHECK_CUDA(cudaMemcpyAsync(b->draft, start, hd * 4, cudaMemcpyDeviceToDevice, s));
   SF_CHECK_CUDA(cudaMemcpyAsync(b->state, state, (size_t)n_envs * c.state_dim * 4,
                                 cudaMemcpyDeviceToDevice, s));

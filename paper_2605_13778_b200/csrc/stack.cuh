@@ -482,7 +482,8 @@ __device__ __forceinline__ bool attn_load_block(const Args& a, const PhaseRef& P
   uint8_t* st = sm.kv + s * attn::kStageBytes;
   const uint64_t pol = sm100::policy_evict_last();
   sm100::mbar_arrive_expect_tx(&C.kv_full[s], attn::kStageBytes);
-  const int env = t.env_start / a.ap.env_rows;
+  const int env = a.ap.env_map ? __ldg(a.ap.env_map + t.env_start / a.ap.env_rows)
+                                : t.env_start / a.ap.env_rows;
   if (is_prefix) {
     for (int c = 0; c < 4; ++c)
       attn::tma_load_3d(&P.am[1], &C.kv_full[s], st + c * (attn::BKEY * 128), c * 64, j * attn::BKEY,

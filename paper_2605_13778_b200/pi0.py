@@ -310,6 +310,22 @@ class ActionExpert:
                                               self.flags, s), "ae denoise")
         return chunk, status
 
+    def denoise_envs(self, env_map: torch.Tensor, start: torch.Tensor, state: torch.Tensor,
+                     n_steps: int, chunk: torch.Tensor | None = None,
+                     status: torch.Tensor | None = None, stream=None):
+        """Euler full path on a compacted batch: row e attends to prefix-KV pool
+        slot env_map[e] (int32 device tensor)."""
+        B = start.shape[0]
+        dev = start.device
+        chunk = torch.empty_like(start) if chunk is None else chunk
+        status = torch.empty((B, 2), dtype=torch.int32, device=dev) if status is None else status
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _capi.check(_capi.lib().sf_ae_denoise_envs(self._h, B, env_map.data_ptr(), n_steps,
+                                                   start.data_ptr(), state.data_ptr(),
+                                                   chunk.data_ptr(), status.data_ptr(), self.flags, s),
+                    "ae denoise envs")
+        return chunk, status
+
     def velocity_batch(self, x: torch.Tensor, taus, state: torch.Tensor) -> torch.Tensor:
         """x [B, R, H, D] f32 -> v [B, R, H, D] (field protocol, batched)."""
         B, R = x.shape[0], x.shape[1]
@@ -372,3 +388,62 @@ class ActionExpert:
                 raise FloatingPointError(f"velocity produced non-finite values at tau={step / n}")
             raise FloatingPointError(f"denoising diverged at step {step} (tau={step / n})")
         return chunk[0].double().cpu().numpy()
+
+
+class BatchedReplanner:
+    """Device-side replanning rounds for B independent envs (run_episode,
+    runtime.py:219-334, minus the conveyor): per round one batched flash graph
+    (draft + K-branch verify + gate + decision for every env), the round
+    bookkeeping on the device (``sf_replan_update``: periodic-refresh counter,
+    path codes, planned prefix with the cap, fallback compaction), then the
+    10-step Euler full path only on the compacted fallback bucket (padded to a
+    power of two so each bucket size keeps one CUDA graph;
+    ``sf_ae_denoise_envs`` maps bucket rows to their envs' prefix KV). The
+    only host sync per round is the fallback count. Returns device tensors:
+    the chunk to execute [B, H, D] (draft for accepted envs, full-path chunk
+    otherwise), path codes (``_capi.SF_PATH_*``), planned prefix lengths."""
+
+    def __init__(self, ae: ActionExpert, n_envs: int, vcfg, replan_size: int = 12,
+                 periodic_refresh: int = 2, phase_fallback: bool = True, prefix_cap: bool = True,
+                 flash: bool = True, num_steps: int = 10):
+        if n_envs > ae.n_envs:
+            raise ValueError(f"{n_envs} envs but the prefix pool holds {ae.n_envs}")
+        self.ae, self.n, self.vcfg = ae, n_envs, vcfg
+        self.replan_size, self.periodic_refresh = replan_size, periodic_refresh
+        self.phase_fallback, self.prefix_cap, self.flash = phase_fallback, prefix_cap, flash
+        self.num_steps = num_steps
+        dev = _device.device()
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.fsr = torch.zeros(n_envs, **i32)        # flash rounds since the last full round
+        self.has_cache = torch.zeros(n_envs, **i32)  # a full round has produced a context
+        self.path = torch.empty(n_envs, **i32)
+        self.planned = torch.empty(n_envs, **i32)
+        self.fb_idx = torch.empty(n_envs, **i32)
+        self.fb_count = torch.zeros(1, **i32)
+        self.round_index = 0
+
+    def round(self, obs: torch.Tensor, eps_verify: torch.Tensor, eps_denoise: torch.Tensor,
+              state: torch.Tensor, signs: torch.Tensor):
+        ae, n = self.ae, self.n
+        s = torch.cuda.current_stream().cuda_stream
+        draft, _, _, branch, result = ae.flash_batch(
+            self.vcfg, obs, eps_verify, state, signs, phase_fallback=self.phase_fallback,
+            prefix_cap=self.prefix_cap, replan_size=self.replan_size)
+        _capi.check(_capi.lib().sf_replan_update(
+            n, result.data_ptr(), self.fsr.data_ptr(), self.has_cache.data_ptr(), int(self.flash),
+            self.periodic_refresh, self.replan_size, self.path.data_ptr(), self.planned.data_ptr(),
+            self.fb_idx.data_ptr(), self.fb_count.data_ptr(), s), "replan update")
+        chunk = draft
+        n_fb = int(self.fb_count.item())
+        if n_fb:
+            bucket = min(n, 1 << (n_fb - 1).bit_length())
+            idx = self.fb_idx[:bucket].clone()
+            if bucket > n_fb:
+                idx[n_fb:] = idx[0]  # padding rows repeat a real env; results dropped
+            full, _ = ae.denoise_envs(idx, eps_denoise.index_select(0, idx),
+                                      state.index_select(0, idx), self.num_steps)
+            chunk = draft.clone()
+            chunk.index_copy_(0, idx[:n_fb].long(), full[:n_fb])
+        self.round_index += 1
+        return chunk, self.path, self.planned, branch, result
+

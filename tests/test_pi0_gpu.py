@@ -250,3 +250,104 @@ def test_attention_pair_kernel_matches_single_sm():
     (r0, d0, _, _), (r1, d1, _, _) = outs
     torch.testing.assert_close(r1, r0, rtol=2e-3, atol=2e-3 * r0.abs().max().item())
     torch.testing.assert_close(d1, d0, rtol=2e-3, atol=2e-3 * d0.abs().max().item())
+
+
+def _replan_ref(result, fsr, has_cache, mode_flash, pf, r):
+    """run_episode bookkeeping (runtime.py:238-320) for one round of B envs."""
+    B = len(fsr)
+    path, planned, idx = np.zeros(B, int), np.zeros(B, int), []
+    fsr, has_cache = fsr.copy(), has_cache.copy()
+    for e in range(B):
+        forced = pf > 0 and fsr[e] >= pf
+        use = mode_flash and has_cache[e] and not forced
+        if not use:
+            path[e], planned[e] = (4 if (forced and mode_flash) else 3), r
+        else:
+            path[e] = result[e, 2]
+            planned[e] = result[e, 3] if path[e] == 0 else r
+        if path[e] == 0:
+            fsr[e] += 1
+        else:
+            fsr[e], has_cache[e] = 0, 1
+            idx.append(e)
+    return path, planned, fsr, has_cache, np.array(idx, int)
+
+
+def test_replan_update_matches_run_episode_bookkeeping():
+    import torch
+
+    from paper_2605_13778_b200 import _capi
+
+    rng = np.random.default_rng(21)
+    B, pf, r = 3000, 2, 12
+    for mode_flash in (1, 0):
+        result = np.zeros((B, 8), np.int32)
+        result[:, 2] = rng.integers(0, 3, B)
+        result[:, 3] = rng.integers(1, 13, B)
+        fsr = rng.integers(0, 4, B).astype(np.int32)
+        hc = rng.integers(0, 2, B).astype(np.int32)
+        want = _replan_ref(result, fsr, hc, mode_flash, pf, r)
+        t = lambda a: torch.from_numpy(a).cuda()
+        d_res, d_fsr, d_hc = t(result), t(fsr), t(hc)
+        path, planned, idx = (torch.empty(B, dtype=torch.int32, device="cuda") for _ in range(3))
+        cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _capi.check(_capi.lib().sf_replan_update(
+            B, d_res.data_ptr(), d_fsr.data_ptr(), d_hc.data_ptr(), mode_flash, pf, r, path.data_ptr(),
+            planned.data_ptr(), idx.data_ptr(), cnt.data_ptr(), torch.cuda.current_stream().cuda_stream),
+            "replan")
+        n = int(cnt.item())
+        np.testing.assert_array_equal(path.cpu().numpy(), want[0])
+        np.testing.assert_array_equal(planned.cpu().numpy(), want[1])
+        np.testing.assert_array_equal(d_fsr.cpu().numpy(), want[2])
+        np.testing.assert_array_equal(d_hc.cpu().numpy(), want[3])
+        np.testing.assert_array_equal(idx[:n].cpu().numpy(), want[4])
+
+
+def test_denoise_envs_compacted_matches_full_batch():
+    import torch
+
+    from paper_2605_13778_b200 import pi0
+
+    _, dcfg = _pair()
+    ae = pi0.ActionExpert(dcfg, seed=0, n_envs=4, kv_seed=1)
+    rng = np.random.default_rng(4)
+    H, D, S = dcfg.horizon, dcfg.action_dim, dcfg.state_dim
+    start = torch.from_numpy(rng.standard_normal((4, H, D)).astype(np.float32)).cuda()
+    state = torch.from_numpy(rng.standard_normal((4, S)).astype(np.float32)).cuda()
+    full, _ = ae.denoise_batch(start, state, 4)
+    m = torch.tensor([2, 0], dtype=torch.int32, device="cuda")
+    sub, status = ae.denoise_envs(m, start[[2, 0]], state[[2, 0]], 4)
+    assert (status[:, 0] == -1).all()
+    torch.testing.assert_close(sub, full[[2, 0]], rtol=1e-3, atol=1e-3 * full.abs().max().item())
+
+
+def test_batched_replanner_rounds():
+    import torch
+
+    from paper_2605_13778_b200 import _capi, pi0
+    from paper_2605_13778_b200.verifier import VerifierConfig
+
+    _, dcfg = _pair()
+    B = 6
+    ae = pi0.ActionExpert(dcfg, seed=0, n_envs=B, kv_seed=1)
+    vc = VerifierConfig(timesteps=(0.25, 0.5, 0.75), delta=1e9, gripper_window=0)
+    rp = pi0.BatchedReplanner(ae, B, vc, replan_size=4, periodic_refresh=2)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    H, D, S = dcfg.horizon, dcfg.action_dim, dcfg.state_dim
+    mk = lambda *sh: torch.randn(sh, generator=g, device="cuda")
+    paths = []
+    for _ in range(4):
+        obs, ev, ed, st = mk(B, dcfg.draft_in), mk(B, H, D), mk(B, H, D), mk(B, S)
+        signs = torch.ones(B, device="cuda")
+        chunk, path, planned, _, result = rp.round(obs, ev, ed, st, signs)
+        paths.append(path.cpu().numpy().copy())
+        p = path.cpu().numpy()
+        assert torch.isfinite(chunk).all()
+        # accepted envs execute the draft, with the capped prefix
+        acc = p == _capi.SF_PATH_FLASH_ACCEPTED
+        assert (planned.cpu().numpy()[~acc] == 4).all()
+    # round 0: no context yet -> full; delta = inf accepts every flash attempt
+    assert (paths[0] == _capi.SF_PATH_FULL).all()
+    assert (paths[1] == _capi.SF_PATH_FLASH_ACCEPTED).all()
+    assert (paths[2] == _capi.SF_PATH_FLASH_ACCEPTED).all()
+    assert (paths[3] == _capi.SF_PATH_PERIODIC).all()  # PF = 2 flash rounds since the refresh
