@@ -718,7 +718,9 @@ int build(Handle& h, Buffers& b, int B, int K) {
       const Spec& sp = specs[cls];
       const int tiles = ((sp.n_out + gemm::BM - 1) / gemm::BM) * tiles_b, nkb = sp.k_in / gemm::BK;
       int S = nsm / tiles;
-      S = S > 6 ? 6 : (S < 1 ? 1 : S);
+      // 8-CTA clusters only while they fill at most half the GPU
+      S = S > 8 ? 8 : (S < 1 ? 1 : S);
+      if (S > 6 && tiles * S > nsm / 2) S = 6;
       S = S > nkb ? nkb : S;
       for (int l = 0; l < L; ++l) {
         const Spec& q = specs[4 * l + cls];
