@@ -62,6 +62,12 @@ struct Params {
   float* ws;           // [tiles][splits][128][HD + 2]
   int* counters;       // [tiles]
   const int* env_map;  // [envs] prefix-KV pool slot of each batch env (compacted batches)
+  // prefix K / V^T as per-block SMEM images ([slot][block][32 KB], already
+  // SWIZZLE_128B): one 32 KB bulk copy per operand instead of 4 + 1 tensor
+  // boxes of 128 B rows (null: use the tensor maps)
+  const uint8_t* k_img;
+  const uint8_t* v_img;
+  int img_blocks;      // key blocks per env image
 };
 
 #ifdef SF_TRACE
@@ -95,10 +101,33 @@ __device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uin
                : "memory");
 }
 
+// MUFU ex2 (flush-to-zero; ex2(-inf) = +0 for masked keys)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// sm_100 three-input max
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float y;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(y) : "f"(a), "f"(b), "f"(c));
+  return y;
+}
+
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// contiguous global -> shared bulk copy, completion counted on `bar` (bytes)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                          uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          sm100::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(sm100::smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 
 __device__ __forceinline__ void tma_load_3d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0,
                                             int c1, int c2, uint64_t policy) {
@@ -203,7 +232,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = i & 1;
         uint8_t* st = sKV + s * kStageBytes;
         sm100::mbar_arrive_expect_tx(&k_full[s], kKBytes);
-        if (j < p.n_prefix_blocks) {
+        if (j < p.n_prefix_blocks && p.k_img) {
+          bulk_load(st, p.k_img + ((size_t)slot * p.img_blocks + j) * kKBytes, kKBytes, &k_full[s], pol_keep);
+        } else if (j < p.n_prefix_blocks) {
           for (int c = 0; c < 4; ++c)
             tma_load_3d(&tm_kp, &k_full[s], st + c * (BKEY * 128), c * 64, j * BKEY, slot, pol_keep);
         } else {
@@ -217,7 +248,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = i & 1;
         uint8_t* st = sKV + s * kStageBytes + kKBytes;
         sm100::mbar_arrive_expect_tx(&v_full[s], kVBytes);
-        if (j < p.n_prefix_blocks) {
+        if (j < p.n_prefix_blocks && p.v_img) {
+          bulk_load(st, p.v_img + ((size_t)slot * p.img_blocks + j) * kVBytes, kVBytes, &v_full[s], pol_keep);
+        } else if (j < p.n_prefix_blocks) {
           tma_load_3d(&tm_vp, &v_full[s], st, j * BKEY, 0, slot, pol_keep);
         } else {
           const int row0 = sb + (j - p.n_prefix_blocks) * BKEY;
@@ -239,12 +272,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       // two independent streams, issued in readiness order (polling)
       const long long t0 = clock64();
       while (nk < nb || nv < nb) {
-        if (nk < nb && (nk < 2 || sm100::mbar_try_wait(sm100::smem_u32(&k_empty[nk & 1]), ((nk >> 1) & 1) ^ 1))) {
+        if (nk < nb && (nk < 2 || sm100::mbar_test(sm100::smem_u32(&k_empty[nk & 1]), ((nk >> 1) & 1) ^ 1))) {
           load_k(nk);
           ++nk;
         }
         if (nv < nb && nv < nk &&
-            (nv < 2 || sm100::mbar_try_wait(sm100::smem_u32(&v_empty[nv & 1]), ((nv >> 1) & 1) ^ 1))) {
+            (nv < 2 || sm100::mbar_test(sm100::smem_u32(&v_empty[nv & 1]), ((nv >> 1) & 1) ^ 1))) {
           load_v(nv);
           ++nv;
         }
@@ -347,12 +380,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       lo -= half * 32;
       hi -= half * 32;
       float sv[32];
-      float mb = -INFINITY;
+      float mb;
+      if (lo <= 0 && hi >= 32) {  // fully visible half-block (every prefix block but the last)
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const float x = __uint_as_float(raw[c >> 4][c & 15]);
-        sv[c] = (c >= lo && c < hi) ? x : -INFINITY;
-        mb = fmaxf(mb, sv[c]);
+        for (int c = 0; c < 32; ++c) sv[c] = __uint_as_float(raw[c >> 4][c & 15]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float x = __uint_as_float(raw[c >> 4][c & 15]);
+          sv[c] = (c >= lo && c < hi) ? x : -INFINITY;
+        }
+      }
+      {  // 3-input max tree
+        float t[11];
+#pragma unroll
+        for (int c = 0; c < 10; ++c) t[c] = fmax3(sv[3 * c], sv[3 * c + 1], sv[3 * c + 2]);
+        t[10] = fmaxf(sv[30], sv[31]);
+        const float u0 = fmax3(t[0], t[1], t[2]), u1 = fmax3(t[3], t[4], t[5]);
+        const float u2 = fmax3(t[6], t[7], t[8]), u3 = fmaxf(t[9], t[10]);
+        mb = fmaxf(fmax3(u0, u1, u2), u3);
       }
       // pair max (raw scores; the positive scale commutes with max)
       xm[(s * 2 + half) * BQ + r] = mb;
@@ -379,8 +425,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       float lp = 0.f;
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
-        const float p0 = exp2f(fmaf(sv[2 * k], p.scale_log2, -mu));
-        const float p1 = exp2f(fmaf(sv[2 * k + 1], p.scale_log2, -mu));
+        const float p0 = ex2_approx(fmaf(sv[2 * k], p.scale_log2, -mu));
+        const float p1 = ex2_approx(fmaf(sv[2 * k + 1], p.scale_log2, -mu));
         lp += p0 + p1;
         __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
         pw[k] = *reinterpret_cast<uint32_t*>(&b2);
@@ -870,12 +916,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       lo -= half * 32;
       hi -= half * 32;
       float sv[32];
-      float mb = -INFINITY;
+      float mb;
+      if (lo <= 0 && hi >= 32) {  // fully visible half-block (every prefix block but the last)
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const float x = __uint_as_float(raw[c >> 4][c & 15]);
-        sv[c] = (c >= lo && c < hi) ? x : -INFINITY;
-        mb = fmaxf(mb, sv[c]);
+        for (int c = 0; c < 32; ++c) sv[c] = __uint_as_float(raw[c >> 4][c & 15]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float x = __uint_as_float(raw[c >> 4][c & 15]);
+          sv[c] = (c >= lo && c < hi) ? x : -INFINITY;
+        }
+      }
+      {  // 3-input max tree
+        float t[11];
+#pragma unroll
+        for (int c = 0; c < 10; ++c) t[c] = fmax3(sv[3 * c], sv[3 * c + 1], sv[3 * c + 2]);
+        t[10] = fmaxf(sv[30], sv[31]);
+        const float u0 = fmax3(t[0], t[1], t[2]), u1 = fmax3(t[3], t[4], t[5]);
+        const float u2 = fmax3(t[6], t[7], t[8]), u3 = fmaxf(t[9], t[10]);
+        mb = fmaxf(fmax3(u0, u1, u2), u3);
       }
       xm[(b * 2 + half) * BQ + r] = mb;
       asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
@@ -899,8 +958,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       float lp = 0.f;
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
-        const float p0 = exp2f(fmaf(sv[2 * k], p.scale_log2, -mu));
-        const float p1 = exp2f(fmaf(sv[2 * k + 1], p.scale_log2, -mu));
+        const float p0 = ex2_approx(fmaf(sv[2 * k], p.scale_log2, -mu));
+        const float p1 = ex2_approx(fmaf(sv[2 * k + 1], p.scale_log2, -mu));
         lp += p0 + p1;
         __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
         pw[k] = *reinterpret_cast<uint32_t*>(&b2);

@@ -232,6 +232,46 @@ __global__ void transpose_u64_kernel(const unsigned long long* __restrict__ src,
   }
 }
 
+// Prefix K / V^T pool -> per-key-block SMEM images (SWIZZLE_128B, the layout
+// TMA would write): K block j of (layer, env) = 4 chunks of [64 keys][64 dims],
+// 16 B unit u of row r stored at unit (u ^ (r & 7)); V^T block = [256 dims][64
+// keys] likewise by dim row. Keys >= P are zero. One thread per 16 B unit.
+__global__ void prefix_image_kernel(const bf16* __restrict__ kp, const bf16* __restrict__ vp,
+                                    uint8_t* __restrict__ kimg, uint8_t* __restrict__ vimg, int LE,
+                                    int P, int nblk) {
+  const size_t units_per_blk = 32768 / 16;  // 2048
+  const size_t total = (size_t)LE * nblk * units_per_blk;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t le = i / (nblk * units_per_blk);
+    const int rem = (int)(i - le * nblk * units_per_blk);
+    const int j = rem / (int)units_per_blk, u = rem % (int)units_per_blk;
+    // destination unit u -> (row, swizzled column unit)
+    {  // K: chunk c (dims c*64..), row = key kk, unit position w holds column unit w ^ (kk & 7)
+      const int c = u >> 9, rr = (u >> 3) & 63, w = u & 7;
+      const int cu = w ^ (rr & 7);
+      const int key = j * 64 + rr, d0 = c * 64 + cu * 8;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (key < P) v = *reinterpret_cast<const uint4*>(kp + ((size_t)le * P + key) * 256 + d0);
+      reinterpret_cast<uint4*>(kimg + ((size_t)le * nblk + j) * 32768)[u] = v;
+    }
+    {  // V^T: row = dim (256 rows of 128 B), unit position w holds key unit w ^ (dim & 7)
+      const int dim = u >> 3, w = u & 7;
+      const int cu = w ^ (dim & 7);
+      const int key0 = j * 64 + cu * 8;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      const bf16* src = vp + ((size_t)le * 256 + dim) * P + key0;
+      if (key0 + 8 <= P && (P % 8) == 0) {
+        v = *reinterpret_cast<const uint4*>(src);
+      } else {
+        bf16 t[8];
+        for (int z = 0; z < 8; ++z) t[z] = key0 + z < P ? src[z] : __float2bfloat16_rn(0.f);
+        v = *reinterpret_cast<const uint4*>(t);
+      }
+      reinterpret_cast<uint4*>(vimg + ((size_t)le * nblk + j) * 32768)[u] = v;
+    }
+  }
+}
+
 // [rows][cols] -> [cols][rows] (embedding weights, once per handle)
 __global__ void transpose_f32_kernel(const float* __restrict__ src, float* __restrict__ dst,
                                      int rows, int cols) {
@@ -389,6 +429,9 @@ struct Buffers {
   std::vector<CUtensorMap> attn_maps;  // per layer: q, kp, vp, ks, vs
   std::vector<CUtensorMap> attn_pair_maps;  // 2-SM pair kernel: half-block boxes (batched)
   bool attn_pair = false;
+  const uint8_t* k_img = nullptr;  // handle's prefix block images (null: tensor maps)
+  const uint8_t* v_img = nullptr;
+  int img_blocks = 0, n_img_envs = 0;
   cudaGraphExec_t graph = nullptr;
   int graph_key = 0;
   int graph_kernels = 0;  // kernel nodes in `graph` (launch accounting)
@@ -424,6 +467,9 @@ struct Handle {
   float* a_wt = nullptr;  // [D][W] transposed action-embedding weights
   float* s_wt = nullptr;  // [S][W] transposed state-embedding weights
   float2* rope_t = nullptr;  // [head_dim/2][P + 1 + H] position-fastest RoPE table
+  uint8_t* k_img = nullptr;  // [L][E][nblk][32 KB] prefix K block images (attention)
+  uint8_t* v_img = nullptr;  // [L][E][nblk][32 KB] prefix V^T block images
+  int img_blocks = 0;
   std::map<long long, std::unique_ptr<Buffers>> buffers;  // key: (B, K, mode)
   cudaStream_t capture_stream = nullptr;
 };
@@ -838,7 +884,11 @@ int build(Handle& h, Buffers& b, int B, int K) {
   ap.out = b.attn;
   ap.ws = attn_ws;
   ap.counters = b.counters;
-  ap.env_map = b.env_map;  // shared with split-K GEMMs: kernels are stream-ordered
+  ap.env_map = b.env_map;
+  b.k_img = h.k_img;
+  b.v_img = h.v_img;
+  b.img_blocks = h.img_blocks;
+  b.n_img_envs = h.n_prefix_envs;  // shared with split-K GEMMs: kernels are stream-ordered
   b.attn_maps.resize(5 * L);
   const int E = h.n_prefix_envs;
   for (int l = 0; l < L; ++l) {
@@ -1082,7 +1132,14 @@ int launch_attn(const Buffers& b, int l, cudaStream_t s, bool pdl) {
   }
   cfg.attrs = a;
   cfg.numAttrs = na;
-  SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, attn::attn_kernel, mp[0], mp[1], mp[2], mp[3], mp[4], b.ap));
+  attn::Params ap = b.ap;
+  if (b.k_img) {  // this layer's slice of the prefix block images
+    const size_t per_layer = (size_t)b.n_img_envs * b.img_blocks * 32768;
+    ap.k_img = b.k_img + (size_t)l * per_layer;
+    ap.v_img = b.v_img + (size_t)l * per_layer;
+    ap.img_blocks = b.img_blocks;
+  }
+  SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, attn::attn_kernel, mp[0], mp[1], mp[2], mp[3], mp[4], ap));
   count_launch();
   return SF_OK;
 }
@@ -1343,6 +1400,8 @@ extern "C" int sf_ae_destroy(void* handle) {
   cudaFree(h->a_wt);
   cudaFree(h->s_wt);
   cudaFree(h->rope_t);
+  if (h->k_img) cudaFree(h->k_img);
+  if (h->v_img) cudaFree(h->v_img);
   if (h->temb_euler) cudaFree(h->temb_euler);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
   delete h;
@@ -1356,6 +1415,29 @@ extern "C" int sf_ae_set_prefix(void* handle, const void* k_prefix, const void* 
   h->k_prefix = static_cast<const bf16*>(k_prefix);
   h->vt_prefix = static_cast<const bf16*>(vt_prefix);
   h->n_prefix_envs = n_envs;
+  // block images of the pool (re-laid out once; the attention streams each
+  // 64-key block of K and V^T with one bulk copy)
+  {
+    const sf_ae_config_t& c = h->cfg;
+    if (h->k_img) cudaFree(h->k_img);
+    if (h->v_img) cudaFree(h->v_img);
+    h->k_img = h->v_img = nullptr;
+    h->img_blocks = 0;
+    const int nblk = (c.prefix_len + 63) / 64;
+    const size_t bytes = (size_t)c.layers * n_envs * nblk * 32768;
+    if (getenv("SF_NO_KV_IMAGES") == nullptr && c.head_dim == 256 &&
+        cudaMalloc(&h->k_img, bytes) == cudaSuccess && cudaMalloc(&h->v_img, bytes) == cudaSuccess) {
+      prefix_image_kernel<<<148 * 8, 256>>>(h->k_prefix, h->vt_prefix, h->k_img, h->v_img,
+                                            c.layers * n_envs, c.prefix_len, nblk);
+      SF_CHECK_CUDA(cudaGetLastError());
+      SF_CHECK_CUDA(cudaDeviceSynchronize());
+      h->img_blocks = nblk;
+    } else {
+      cudaGetLastError();  // out of memory is not fatal: the tensor-map path stays
+      if (h->k_img) cudaFree(h->k_img);
+      h->k_img = nullptr;
+    }
+  }
   // plans embed the prefix tensor maps: drop them
   for (auto& kv : h->buffers) {
     Buffers& b = *kv.second;
