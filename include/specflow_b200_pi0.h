@@ -125,6 +125,38 @@ int sf_ae_velocity(void* handle, int n_envs, int rows, const float* x, const dou
 int sf_fill_hash_uniform(void* dst, int is_bf16, int64_t n, uint64_t seed, uint64_t tid, double std,
                          void* stream);
 
+/* ---- context refresh: VLM prefix prefill -> prefix KV pool ----
+ * A Gemma-style decoder (8 query heads x 256 sharing one KV head, GeGLU MLP
+ * `mlp`, RMSNorm gains folded into the weights, RoPE base 1e4) over the P
+ * prefix tokens of each env with bidirectional prefix attention; layer l's K
+ * and V are the Action Expert's prefix pool entries (flowpolicy.py:156-161
+ * encode_context at pi0 scale). Weights use the Action Expert's device layout
+ * (QKV rows interleaved for RoPE pairs, gate/up rows interleaved). */
+typedef struct {
+  int width;       /* 2048 for a Gemma-2B-style prefix encoder */
+  int layers;
+  int q_heads;     /* 8 */
+  int head_dim;    /* 256 */
+  int mlp;         /* 16384 */
+  int prefix_len;  /* P (multiple of 16) */
+  float eps;
+} sf_vlm_config_t;
+
+typedef struct {
+  const void* qkv[SF_AE_MAX_LAYERS];   /* [8*256 + 2*256][W] bf16 */
+  const void* o[SF_AE_MAX_LAYERS];     /* [W][8*256] bf16 */
+  const void* gu[SF_AE_MAX_LAYERS];    /* [2*mlp][W] bf16 */
+  const void* down[SF_AE_MAX_LAYERS];  /* [W][mlp] bf16 */
+  const void* rope;                    /* [P][128] float2 (cos, sin) */
+} sf_vlm_weights_t;
+
+int sf_vlm_create(const sf_vlm_config_t* cfg, const sf_vlm_weights_t* weights, void** handle);
+int sf_vlm_destroy(void* handle);
+/* x [n_envs][P][W] f32 token embeddings -> k_pool [L][n_envs][P][256] bf16 and
+ * vt_pool [L][n_envs][256][P] bf16 (the sf_ae_set_prefix layout). Async on
+ * `stream`. */
+int sf_vlm_prefill(void* handle, int n_envs, const float* x, void* k_pool, void* vt_pool, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -246,3 +246,73 @@ def make_prefix_kv(cfg: AEConfig, seed: int = 1, env: int = 0):
         kp.append(bf16(hash_uniform(seed, t, (cfg.prefix_len, cfg.head_dim), 1.0)))
         vtp.append(bf16(hash_uniform(seed, t + 1, (cfg.head_dim, cfg.prefix_len), 1.0)))
     return kp, vtp
+
+
+# ---------------------------------------------------------------- VLM prefill
+# Context refresh: the prefix encoder whose per-layer K / V
+# form the Action Expert's prefix KV pool. Builder-defined (the reference's
+# encode_context, flowpolicy.py:156-161, is a tiny MLP; the paper's prefix is
+# the Gemma-2B VLM): a decoder stack with bidirectional prefix
+# attention, same block structure and numerics conventions as the Action
+# Expert above.
+
+TID_VLM_BASE = 1000  # + 4 * layer + {0: qkv, 1: o, 2: gu, 3: down}
+
+
+@dataclass(frozen=True)
+class VLMConfig:
+    width: int = 2048
+    layers: int = 18
+    q_heads: int = 8
+    head_dim: int = 256
+    mlp: int = 16384
+    prefix_len: int = 800
+    eps: float = 1e-6
+    rope_base: float = 10000.0
+
+
+def make_vlm_weights(cfg: VLMConfig, seed: int = 7, std: float = 0.02):
+    def g(tid, *shape):
+        return bf16(hash_uniform(seed, tid, shape, std))
+
+    W, nq = cfg.width, cfg.q_heads * cfg.head_dim
+    out = []
+    for l in range(cfg.layers):
+        b = TID_VLM_BASE + 4 * l
+        out.append({"qkv": g(b + 0, nq + 2 * cfg.head_dim, W), "o": g(b + 1, W, nq),
+                    "gu": g(b + 2, 2 * cfg.mlp, W), "down": g(b + 3, W, cfg.mlp)})
+    return out
+
+
+def prefill_kv(cfg: VLMConfig, layers, x):
+    """One env: token embeddings x [P, W] -> per-layer K [L][P, 256] and
+    V^T [L][256, P] (bf16-valued float32), bidirectional attention over the
+    P prefix tokens at RoPE positions 0..P-1."""
+    P = cfg.prefix_len
+    cs = rope_table(cfg, P)
+    pos = np.arange(P)
+    scale = 1.0 / np.sqrt(cfg.head_dim)
+    nq = cfg.q_heads * cfg.head_dim
+    x = x.astype(np.float32).copy()
+    ks, vts = [], []
+    for L in layers:
+        r = _rms(x, cfg.eps)
+        qkv = _mm(bf16(x), L["qkv"]) * r[:, None]
+        q = qkv[:, :nq].reshape(P, cfg.q_heads, cfg.head_dim)
+        k = qkv[:, nq: nq + cfg.head_dim].reshape(P, 1, cfg.head_dim)
+        v = bf16(qkv[:, nq + cfg.head_dim:])
+        q = bf16(_rope(q, cs, pos))
+        k = bf16(_rope(k, cs, pos))[:, 0]
+        ks.append(k)
+        vts.append(np.ascontiguousarray(v.T))
+        s = np.einsum("thd,kd->thk", q, k).astype(np.float32) * scale
+        m = s.max(-1, keepdims=True)
+        p = np.exp(s - m)
+        lsum = p.sum(-1, keepdims=True)
+        o = np.einsum("thk,kd->thd", bf16(p), v).astype(np.float32) / lsum
+        x = x + _mm(bf16(o.reshape(P, nq)), L["o"])
+        r2 = _rms(x, cfg.eps)
+        gu = _mm(bf16(x), L["gu"]) * r2[:, None]
+        h = bf16(gelu_tanh(gu[:, : cfg.mlp]) * gu[:, cfg.mlp:])
+        x = x + _mm(h, L["down"])
+    return np.stack(ks), np.stack(vts)

@@ -94,6 +94,9 @@ SIGNATURES = {
     "sf_ae_denoise": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, _P]),
     "sf_ae_denoise_envs": (_I, [_P, _I, _P, _I, _P, _P, _P, _P, _I, _P]),
     "sf_replan_update": (_I, [_I, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "sf_vlm_create": (_I, [_P, _P, _P]),
+    "sf_vlm_destroy": (_I, [_P]),
+    "sf_vlm_prefill": (_I, [_P, _I, _P, _P, _P, _P]),
     "sf_ae_flash_round": (_I, [_P, _I, ctypes.POINTER(SfVerifyCfg), _P, _P, _P, _P,
                                ctypes.POINTER(SfVerifyOut), _I, _P]),
     "sf_ae_time_op": (_I, [_P, _I, _I, _I, _I, _P]),

@@ -1713,3 +1713,319 @@ namespace pi0 {
 
 }  // namespace pi0
 }  // namespace sf
+
+// ===========================================================================
+// Context refresh: VLM prefix prefill -> prefix KV pool (
+// the pi0 analogue of encode_context, flowpolicy.py:156-161, runtime.py:166).
+// A Gemma-style decoder stack (width W, 8 query heads x 256 sharing one KV
+// head, GeGLU MLP, RMSNorm folded into the weights, RoPE) runs over the P
+// prefix tokens of every env with bidirectional prefix attention, and its
+// per-layer K / V are written straight into the pool layout the Action Expert
+// attends to: K [L][E][P][256] (the QKV epilogue's row-major K output IS that
+// layout) and V^T [L][E][256][P] (one transpose-copy per layer). Same kernels
+// as the Action Expert: tcgen05 GEMMs (2-SM pairs at >= 1024 rows) with fused
+// RMS/RoPE/residual/GeGLU epilogues, and the MQA attention kernel with
+// prefix-only keys (segs = 0).
+// ===========================================================================
+namespace sf {
+namespace pi0 {
+
+struct VlmBuffers {
+  int E = 0, M = 0, m_ld = 0;
+  float* x = nullptr;
+  bf16* xb = nullptr;
+  float* ssq = nullptr;
+  bf16* q = nullptr;
+  bf16* vt = nullptr;  // [256][m_ld] V^T of the current layer
+  bf16* attn = nullptr;
+  bf16* h = nullptr;
+  float* ws = nullptr;
+  float* attn_ws = nullptr;
+  int* counters = nullptr;
+  int* env_ident = nullptr;
+  std::vector<gemm::Op> ops;  // per layer: qkv, o, gu, down
+  std::vector<CUtensorMap> maps;  // per layer: q, kp, vp, ks (dummy), vs (dummy)
+  attn::Params ap{};
+  int attn_tiles = 0, attn_splits = 1;
+  void* k_pool = nullptr;
+  void* vt_pool = nullptr;
+};
+
+struct VlmHandle {
+  sf_vlm_config_t cfg{};
+  sf_vlm_weights_t w{};
+  float2* rope_t = nullptr;  // [128][P] position-fastest
+  std::map<long long, std::unique_ptr<VlmBuffers>> buffers;
+};
+
+__global__ void prefill_embed_kernel(const float* __restrict__ x_in, float* x, bf16* xb, float* ssq,
+                                     int M, int W, int ssq_ld) {
+  // one warp per (row, 128-feature group)
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int groups = W / 128;
+  if (warp >= M * groups) return;
+  const int m = warp / groups, g = warp - m * groups;
+  const float4 v = reinterpret_cast<const float4*>(x_in + (size_t)m * W + g * 128)[lane];
+  reinterpret_cast<float4*>(x + (size_t)m * W + g * 128)[lane] = v;
+  __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+  reinterpret_cast<uint2*>(xb + (size_t)m * W + g * 128)[lane] =
+      make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+  float sq = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if (lane == 0) ssq[(size_t)g * ssq_ld + m] = sq;
+}
+
+// V^T [256][m_ld] (env-major columns) -> pool slice [E][256][P]
+__global__ void vt_to_pool_kernel(const bf16* __restrict__ vt, bf16* __restrict__ pool, int E, int P,
+                                  int m_ld) {
+  const size_t total = (size_t)E * 256 * P / 8;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t o = i * 8;  // pool element index (8 consecutive keys)
+    const int p = (int)(o % P);
+    const size_t ed = o / P;
+    const int d = (int)(ed % 256), e = (int)(ed / 256);
+    const bf16* src = vt + (size_t)d * m_ld + (size_t)e * P + p;
+    bf16* dst = pool + o;
+    if (p + 8 <= P && (P % 8) == 0) {
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+    } else {
+      for (int z = 0; z < 8 && p + z < P; ++z) dst[z] = src[z];
+    }
+  }
+}
+
+int vlm_build(VlmHandle& h, VlmBuffers& b, int E, void* k_pool, void* vt_pool) {
+  const sf_vlm_config_t& c = h.cfg;
+  const int W = c.width, P = c.prefix_len, L = c.layers, nq = 8 * 256;
+  b.E = E;
+  b.M = E * P;
+  b.m_ld = ((b.M + 63) / 64) * 64;
+  b.k_pool = k_pool;
+  b.vt_pool = vt_pool;
+  int rc;
+#define VALLOC(ptr, n) \
+  if ((rc = dalloc(&(ptr), (n)))) return rc
+  VALLOC(b.x, (size_t)b.M * W);
+  VALLOC(b.xb, (size_t)b.m_ld * W);
+  VALLOC(b.ssq, (size_t)(W / 128) * b.m_ld);
+  VALLOC(b.q, (size_t)b.m_ld * nq);
+  VALLOC(b.vt, (size_t)256 * b.m_ld);
+  VALLOC(b.attn, (size_t)b.m_ld * nq);
+  VALLOC(b.h, (size_t)b.m_ld * c.mlp);
+  VALLOC(b.env_ident, (size_t)E);
+  {
+    std::vector<int> id(E);
+    for (int i = 0; i < E; ++i) id[i] = i;
+    SF_CHECK_CUDA(cudaMemcpy(b.env_ident, id.data(), sizeof(int) * E, cudaMemcpyHostToDevice));
+  }
+  auto epi_base = [&](int kind) {
+    gemm::EpiArgs e{};
+    e.kind = kind;
+    e.M = b.M;
+    e.ssq_in = b.ssq;
+    e.ssq_groups = W / 128;
+    e.ssq_ld = b.m_ld;
+    e.inv_width = 1.f / (float)W;
+    e.eps = c.eps;
+    return e;
+  };
+  b.ops.resize(4 * L);
+  const bool swap = b.M <= 256;
+  const int bn = swap ? ((b.M + 15) / 16) * 16 : 256;
+  auto plan_op = [&](gemm::Op* op, const void* wt, int n_out, const void* act, int k_in,
+                     const gemm::EpiArgs& e) {
+    if (swap) return gemm::plan(op, wt, n_out, k_in, act, b.M, k_in, k_in, bn, 0, 1, e);
+    return gemm::plan(op, act, b.M, k_in, wt, n_out, k_in, k_in, bn, 1, 0, e);
+  };
+  for (int l = 0; l < L; ++l) {
+    gemm::EpiArgs e = epi_base(gemm::EPI_QKV);
+    e.N = nq + 512;
+    e.q = b.q;
+    e.k = static_cast<bf16*>(k_pool) + (size_t)l * E * P * 256;  // row m = e*P + p: pool layout
+    e.vt = b.vt;
+    e.vt_ld = b.m_ld;
+    e.rope = h.rope_t;
+    e.rope_ld = P;
+    e.q_features = nq;
+    e.env_rows = P;
+    e.seg_len = P;
+    e.pos0 = 0;
+    if ((rc = plan_op(&b.ops[4 * l + 0], h.w.qkv[l], e.N, b.xb, W, e))) return rc;
+    gemm::EpiArgs eo = epi_base(gemm::EPI_RESID);
+    eo.ssq_in = nullptr;
+    eo.N = W;
+    eo.x = b.x;
+    eo.xb = b.xb;
+    eo.ssq_out = b.ssq;
+    eo.ssq_out_ld = b.m_ld;
+    if ((rc = plan_op(&b.ops[4 * l + 1], h.w.o[l], W, b.attn, nq, eo))) return rc;
+    gemm::EpiArgs eg = epi_base(gemm::EPI_GEGLU);
+    eg.N = 2 * c.mlp;
+    eg.out_bf16 = b.h;
+    eg.ld_bf16 = c.mlp;
+    if ((rc = plan_op(&b.ops[4 * l + 2], h.w.gu[l], eg.N, b.xb, W, eg))) return rc;
+    if ((rc = plan_op(&b.ops[4 * l + 3], h.w.down[l], W, b.h, c.mlp, eo))) return rc;
+  }
+  size_t need = 0;
+  for (auto& op : b.ops) need = op.ws_bytes > need ? op.ws_bytes : need;
+  if (need) {
+    VALLOC(b.ws, need / sizeof(float));
+    for (auto& op : b.ops) op.p.ws = b.ws;
+  }
+  // attention: prefix-only keys (segs = 0), bidirectional over the P tokens
+  const int npb = (P + attn::BKEY - 1) / attn::BKEY;
+  b.attn_tiles = b.M / 16;
+  int asplit = 148 / b.attn_tiles;
+  asplit = asplit < 1 ? 1 : (asplit > npb ? npb : asplit);
+  asplit = asplit > attn::kMaxSplitsKV ? attn::kMaxSplitsKV : asplit;
+  const int bps = (npb + asplit - 1) / asplit;
+  asplit = (npb + bps - 1) / bps;
+  b.attn_splits = asplit;
+  if (asplit > 1) VALLOC(b.attn_ws, (size_t)b.attn_tiles * asplit * (attn::HD * attn::BQ + 2 * attn::BQ));
+  VALLOC(b.counters, (size_t)b.attn_tiles + 8);
+#undef VALLOC
+  attn::Params& ap = b.ap;
+  ap.M = b.M;
+  ap.env_rows = P;
+  ap.seg_len = P;
+  ap.segs = 0;
+  ap.prefix_len = P;
+  ap.n_prefix_blocks = npb;
+  ap.n_blocks = npb;
+  ap.blocks_per_split = bps;
+  ap.splits = asplit;
+  ap.tiles = b.attn_tiles;
+  ap.scale_log2 = 1.4426950408889634f / 16.f;
+  ap.out = b.attn;
+  ap.ws = b.attn_ws;
+  ap.counters = b.counters;
+  ap.env_map = b.env_ident;
+  b.maps.resize(5 * L);
+  for (int l = 0; l < L; ++l) {
+    CUtensorMap* mp = &b.maps[5 * l];
+    if ((rc = gemm::make_map(&mp[0], b.q, b.M * attn::kHeads, 256, 256, attn::BQ))) return rc;
+    const bf16* kp = static_cast<const bf16*>(k_pool) + (size_t)l * E * P * 256;
+    const bf16* vp = static_cast<const bf16*>(vt_pool) + (size_t)l * E * 256 * P;
+    if ((rc = make_map_3d(&mp[1], kp, 256, P, E, 512, (uint64_t)P * 512, 64, attn::BKEY))) return rc;
+    if ((rc = make_map_3d(&mp[2], vp, P, 256, E, (uint64_t)P * 2, (uint64_t)P * 512, attn::BKEY, 256)))
+      return rc;
+    // suffix maps are never used (no suffix blocks) but must be valid descriptors
+    mp[3] = mp[0];
+    mp[4] = mp[0];
+  }
+  return SF_OK;
+}
+
+int vlm_enqueue(VlmHandle& h, VlmBuffers& b, const float* x_in, cudaStream_t s) {
+  const sf_vlm_config_t& c = h.cfg;
+  const int L = c.layers, P = c.prefix_len;
+  int rc;
+  const int warps = b.M * (c.width / 128);
+  prefill_embed_kernel<<<(warps * 32 + 255) / 256, 256, 0, s>>>(x_in, b.x, b.xb, b.ssq, b.M, c.width,
+                                                                b.m_ld);
+  SF_CHECK_CUDA(cudaGetLastError());
+  count_launch();
+  static bool attr = false;
+  if (!attr) {
+    SF_CHECK_CUDA(cudaFuncSetAttribute(attn::attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)attn::kSmemBytes));
+    SF_CHECK_CUDA(cudaFuncSetAttribute(attn::attn_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  for (int l = 0; l < L; ++l) {
+    if ((rc = gemm::launch(b.ops[4 * l + 0], s, false))) return rc;
+    bf16* vpool = static_cast<bf16*>(b.vt_pool) + (size_t)l * b.E * 256 * P;
+    vt_to_pool_kernel<<<148 * 4, 256, 0, s>>>(b.vt, vpool, b.E, P, b.m_ld);
+    SF_CHECK_CUDA(cudaGetLastError());
+    count_launch();
+    const CUtensorMap* mp = &b.maps[5 * l];
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(b.attn_tiles, b.attn_splits);
+    cfg.blockDim = dim3(attn::kThreads);
+    cfg.dynamicSmemBytes = attn::kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute a[1];
+    int na = 0;
+    if (b.attn_splits > 1) {
+      a[0].id = cudaLaunchAttributeClusterDimension;
+      a[0].val.clusterDim.x = 1;
+      a[0].val.clusterDim.y = b.attn_splits;
+      a[0].val.clusterDim.z = 1;
+      na = 1;
+    }
+    cfg.attrs = a;
+    cfg.numAttrs = na;
+    SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, attn::attn_kernel, mp[0], mp[1], mp[2], mp[3], mp[4], b.ap));
+    count_launch();
+    if ((rc = gemm::launch(b.ops[4 * l + 1], s, false))) return rc;
+    if ((rc = gemm::launch(b.ops[4 * l + 2], s, false))) return rc;
+    if ((rc = gemm::launch(b.ops[4 * l + 3], s, false))) return rc;
+  }
+  return SF_OK;
+}
+
+}  // namespace pi0
+}  // namespace sf
+
+using sf::pi0::VlmBuffers;
+using sf::pi0::VlmHandle;
+
+extern "C" int sf_vlm_create(const sf_vlm_config_t* cfg, const sf_vlm_weights_t* w, void** handle) {
+  SF_REQUIRE(cfg && w && handle, "null argument");
+  SF_REQUIRE(cfg->q_heads == 8 && cfg->head_dim == 256, "the attention kernel is built for 8 x 256 MQA");
+  SF_REQUIRE(cfg->width % 256 == 0 && cfg->width <= 4096, "width must be a multiple of 256 (<= 4096)");
+  SF_REQUIRE(cfg->layers >= 1 && cfg->layers <= SF_AE_MAX_LAYERS, "bad layer count");
+  SF_REQUIRE(cfg->mlp % 128 == 0, "mlp must be a multiple of 128");
+  SF_REQUIRE(cfg->prefix_len >= 16 && cfg->prefix_len % 16 == 0, "prefix_len must be a multiple of 16");
+  auto* h = new VlmHandle();
+  h->cfg = *cfg;
+  h->w = *w;
+  int rc;
+  if ((rc = sf::pi0::dalloc(&h->rope_t, (size_t)128 * cfg->prefix_len))) {
+    delete h;
+    return rc;
+  }
+  sf::pi0::transpose_u64_kernel<<<64, 256>>>(static_cast<const unsigned long long*>(w->rope),
+                                             reinterpret_cast<unsigned long long*>(h->rope_t),
+                                             cfg->prefix_len, 128);
+  SF_CHECK_CUDA(cudaGetLastError());
+  SF_CHECK_CUDA(cudaDeviceSynchronize());
+  *handle = h;
+  return SF_OK;
+}
+
+extern "C" int sf_vlm_destroy(void* handle) {
+  auto* h = static_cast<VlmHandle*>(handle);
+  if (!h) return SF_OK;
+  for (auto& kv : h->buffers) {
+    VlmBuffers& b = *kv.second;
+    void* ptrs[] = {b.x, b.xb, b.ssq, b.q, b.vt, b.attn, b.h, b.ws, b.attn_ws, b.counters, b.env_ident};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+  cudaFree(h->rope_t);
+  delete h;
+  return SF_OK;
+}
+
+extern "C" int sf_vlm_prefill(void* handle, int n_envs, const float* x, void* k_pool, void* vt_pool,
+                              void* stream) {
+  auto* h = static_cast<VlmHandle*>(handle);
+  SF_REQUIRE(h && x && k_pool && vt_pool && n_envs >= 1, "bad prefill arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  // plans embed the pool pointers: key on (envs, pools)
+  const long long key = (long long)n_envs ^ ((long long)(uintptr_t)k_pool << 8) ^
+                        ((long long)(uintptr_t)vt_pool << 20);
+  auto it = h->buffers.find(key);
+  VlmBuffers* b;
+  if (it == h->buffers.end()) {
+    auto nb = std::make_unique<VlmBuffers>();
+    int rc = sf::pi0::vlm_build(*h, *nb, n_envs, k_pool, vt_pool);
+    if (rc) return rc;
+    b = nb.get();
+    h->buffers[key] = std::move(nb);
+  } else {
+    b = it->second.get();
+  }
+  return sf::pi0::vlm_enqueue(*h, *b, x, s);
+}

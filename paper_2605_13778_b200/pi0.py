@@ -227,6 +227,18 @@ class ActionExpert:
         self.n_envs = n_envs
         self.kv_seed = kv_seed
 
+    def bind_prefix(self, k_pool: torch.Tensor, vt_pool: torch.Tensor):
+        """Attend to an externally produced prefix KV pool (e.g. the output of
+        VLMPrefill.prefill: K [L, E, P, 256], V^T [L, E, 256, P] bf16)."""
+        cfg = self.cfg
+        L, E, P, hd = k_pool.shape
+        if (L, P, hd) != (cfg.layers, cfg.prefix_len, cfg.head_dim) or tuple(vt_pool.shape) != (L, E, hd, P):
+            raise ValueError("prefix pool shape does not match the Action Expert config")
+        self.k_prefix, self.vt_prefix = k_pool, vt_pool
+        _capi.check(_capi.lib().sf_ae_set_prefix(self._h, k_pool.data_ptr(), vt_pool.data_ptr(), E),
+                    "prefix")
+        self.n_envs = E
+
     def __del__(self):
         try:
             if getattr(self, "_h", None):
@@ -446,4 +458,95 @@ class BatchedReplanner:
             chunk.index_copy_(0, idx[:n_fb].long(), full[:n_fb])
         self.round_index += 1
         return chunk, self.path, self.planned, branch, result
+
+
+# ---------------------------------------------------------------- VLM prefill
+
+@dataclass(frozen=True)
+class VLMConfig:
+    """Gemma-2B-style prefix encoder (context refresh)."""
+    width: int = 2048
+    layers: int = 18
+    q_heads: int = 8
+    head_dim: int = 256
+    mlp: int = 16384
+    prefix_len: int = 800
+    eps: float = 1e-6
+    rope_base: float = 10000.0
+
+
+class _VlmConfigC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("width", "layers", "q_heads", "head_dim", "mlp",
+                                            "prefix_len")] + [("eps", ctypes.c_float)]
+
+
+class _VlmWeightsC(ctypes.Structure):
+    _fields_ = [("qkv", ctypes.c_void_p * _MAXL), ("o", ctypes.c_void_p * _MAXL),
+                ("gu", ctypes.c_void_p * _MAXL), ("down", ctypes.c_void_p * _MAXL),
+                ("rope", ctypes.c_void_p)]
+
+
+TID_VLM_BASE = 1000
+
+
+class VLMPrefill:
+    """Context refresh at pi0 scale: token embeddings of the P prefix tokens
+    per env -> the prefix KV pool the Action Expert attends to (the
+    encode_context analogue, flowpolicy.py:156-161; runtime.py:166 refreshes
+    the cache on every full round). Random-init weights from the shared
+    counter-based initialiser (oracle/pi0_oracle.py make_vlm_weights)."""
+
+    def __init__(self, cfg: VLMConfig = VLMConfig(), seed: int = 7, std: float = 0.02):
+        self.cfg = cfg
+        dev = _device.device()
+        W, nq, L = cfg.width, cfg.q_heads * cfg.head_dim, cfg.layers
+        b16 = torch.bfloat16
+        self._keep = []
+        w = _VlmWeightsC()
+        pq, pg = qkv_row_perm(cfg).to(dev), gu_row_perm(cfg).to(dev)
+        for l in range(L):
+            b = TID_VLM_BASE + 4 * l
+            qkv = _fill(torch.empty((nq + 2 * cfg.head_dim, W), dtype=b16, device=dev), seed, b, std)
+            qkv = qkv.index_select(0, pq).contiguous()
+            gu = _fill(torch.empty((2 * cfg.mlp, W), dtype=b16, device=dev), seed, b + 2, std)
+            gu = gu.index_select(0, pg).contiguous()
+            o = _fill(torch.empty((W, nq), dtype=b16, device=dev), seed, b + 1, std)
+            down = _fill(torch.empty((W, cfg.mlp), dtype=b16, device=dev), seed, b + 3, std)
+            self._keep += [qkv, gu, o, down]
+            w.qkv[l], w.o[l], w.gu[l], w.down[l] = (qkv.data_ptr(), o.data_ptr(), gu.data_ptr(),
+                                                    down.data_ptr())
+        rope = torch.from_numpy(rope_table(cfg, cfg.prefix_len)).to(dev)
+        self._keep.append(rope)
+        w.rope = rope.data_ptr()
+        c = _VlmConfigC(W, L, cfg.q_heads, cfg.head_dim, cfg.mlp, cfg.prefix_len, cfg.eps)
+        self._c, self._w = c, w
+        h = ctypes.c_void_p()
+        _capi.check(_capi.lib().sf_vlm_create(ctypes.byref(c), ctypes.byref(w), ctypes.byref(h)),
+                    "vlm create")
+        self._h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                _capi.lib().sf_vlm_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def prefill(self, x: torch.Tensor, k_pool: torch.Tensor | None = None,
+                vt_pool: torch.Tensor | None = None, stream=None):
+        """x [E, P, W] f32 -> (k_pool [L, E, P, 256], vt_pool [L, E, 256, P]) bf16."""
+        cfg = self.cfg
+        E = x.shape[0]
+        dev = x.device
+        if k_pool is None:
+            k_pool = torch.empty((cfg.layers, E, cfg.prefix_len, cfg.head_dim), dtype=torch.bfloat16,
+                                 device=dev)
+        if vt_pool is None:
+            vt_pool = torch.empty((cfg.layers, E, cfg.head_dim, cfg.prefix_len), dtype=torch.bfloat16,
+                                  device=dev)
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _capi.check(_capi.lib().sf_vlm_prefill(self._h, E, x.contiguous().data_ptr(), k_pool.data_ptr(),
+                                               vt_pool.data_ptr(), s), "vlm prefill")
+        return k_pool, vt_pool
 

@@ -351,3 +351,41 @@ def test_batched_replanner_rounds():
     assert (paths[1] == _capi.SF_PATH_FLASH_ACCEPTED).all()
     assert (paths[2] == _capi.SF_PATH_FLASH_ACCEPTED).all()
     assert (paths[3] == _capi.SF_PATH_PERIODIC).all()  # PF = 2 flash rounds since the refresh
+
+
+def test_vlm_prefill_matches_oracle_and_feeds_the_expert():
+    """Context refresh: prefix encoder K / V written into the
+    pool layout, vs the oracle restatement; the pool then drives a verify."""
+    import dataclasses
+
+    import torch
+
+    from oracle import pi0_oracle as po
+    from paper_2605_13778_b200 import pi0
+    from paper_2605_13778_b200.verifier import VerifierConfig
+
+    vcfg = pi0.VLMConfig(width=512, layers=2, mlp=1024, prefix_len=96)
+    ocfg = po.VLMConfig(width=512, layers=2, mlp=1024, prefix_len=96)
+    vlm = pi0.VLMPrefill(vcfg, seed=7)
+    E = 2
+    rng = np.random.default_rng(8)
+    x = rng.standard_normal((E, vcfg.prefix_len, vcfg.width)).astype(np.float32)
+    kp, vtp = vlm.prefill(torch.from_numpy(x).cuda())
+    layers = po.make_vlm_weights(ocfg, seed=7)
+    for e in range(E):
+        ks, vts = po.prefill_kv(ocfg, layers, x[e])
+        gk = kp[:, e].float().cpu().numpy()
+        gv = vtp[:, e].float().cpu().numpy()
+        np.testing.assert_allclose(gk, ks, rtol=2e-2, atol=2e-2 * np.abs(ks).max())
+        np.testing.assert_allclose(gv, vts, rtol=2e-2, atol=2e-2 * np.abs(vts).max())
+    # the refreshed pool is what the Action Expert attends to
+    _, dcfg = _pair()
+    dcfg = dataclasses.replace(dcfg, prefix_len=vcfg.prefix_len)
+    ae = pi0.ActionExpert(dcfg, seed=0, n_envs=E, kv_seed=1)
+    ae.bind_prefix(kp, vtp)
+    H, D, S = dcfg.horizon, dcfg.action_dim, dcfg.state_dim
+    d = torch.from_numpy(rng.standard_normal((E, H, D)).astype(np.float32)).cuda()
+    e_ = torch.from_numpy(rng.standard_normal((E, H, D)).astype(np.float32)).cuda()
+    s = torch.from_numpy(rng.standard_normal((E, S)).astype(np.float32)).cuda()
+    recon, dist, _, _ = ae.verify_batch(VerifierConfig(timesteps=(0.2, 0.6), delta=0.5), d, e_, s)
+    assert torch.isfinite(recon).all() and torch.isfinite(dist).all()
