@@ -668,6 +668,383 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 }
 
+// ------------------------------------------------ batched: persistent
+//
+// attn_persistent_kernel (one KV split, batched rounds): one CTA per SM walks
+// query tiles t = blockIdx.x, blockIdx.x + gridDim.x, ... with every barrier
+// phase continuing across tiles (global key-block counter g = it * nb + i),
+// so the NEXT tile's Q and first K/V blocks load while the current tile's
+// last blocks and its epilogue run: Q is reloaded once the tile's last S MMA
+// retired (q_empty), and PV(0) of the next tile (which overwrites O) waits for
+// the softmax warps to have read O out of TMEM (o_free). Per block the
+// pipeline is the attn_kernel one (separate K / V^T slots, 8 softmax warps).
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kp,
+                           const __grid_constant__ CUtensorMap tm_vp, const __grid_constant__ CUtensorMap tm_ks,
+                           const __grid_constant__ CUtensorMap tm_vs, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + kQBytes;
+  uint8_t* sP = sKV + 2 * kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kPBytes);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;    // [2]
+  uint64_t* k_empty = bars + 3;   // [2]
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* s_free = bars + 7;    // [2]
+  uint64_t* p_full = bars + 9;    // [2]
+  uint64_t* pv_done = bars + 11;  // [2]
+  uint64_t* v_full = bars + 13;   // [2]
+  uint64_t* v_empty = bars + 15;  // [2]
+  uint64_t* q_empty = bars + 17;  // all S MMAs of a tile retired: Q reusable
+  uint64_t* o_free = bars + 18;   // softmax warps read O out of TMEM: next PV(0) may overwrite
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
+  float* xm = reinterpret_cast<float*>(bars + 32);  // [3 slots][2 half][128]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = p.n_blocks;
+  const int n_tiles = p.tiles;
+  auto tile_geom = [&](int tile, int& m0, int& env, int& env_start, int& sb) {
+    m0 = tile * 16;
+    env = m0 / p.env_rows;
+    env_start = env * p.env_rows;
+    const int seg_first = (m0 - env_start) / p.seg_len;
+    sb = (env_start + seg_first * p.seg_len) & ~(BKEY - 1);
+  };
+
+  if (warp == 0 && lane == 0) {
+    sm100::mbar_init(q_full, 1);
+    sm100::mbar_init(q_empty, 1);
+    sm100::mbar_init(o_free, 256);
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&k_full[s], 1);
+      sm100::mbar_init(&k_empty[s], 1);
+      sm100::mbar_init(&v_full[s], 1);
+      sm100::mbar_init(&v_empty[s], 1);
+      sm100::mbar_init(&s_full[s], 1);
+      sm100::mbar_init(&s_free[s], 256);
+      sm100::mbar_init(&p_full[s], 256);
+      sm100::mbar_init(&pv_done[s], 1);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<kTmemCols>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (sm100::elect_one()) {
+      sm100::tma_prefetch_desc(&tm_q);
+      sm100::tma_prefetch_desc(&tm_kp);
+      sm100::tma_prefetch_desc(&tm_vp);
+      sm100::tma_prefetch_desc(&tm_ks);
+      sm100::tma_prefetch_desc(&tm_vs);
+      const uint64_t pol = sm100::policy_evict_last();
+      // global block g -> (tile, j); K(g) reuses the slot of K(g-2) once S(g-2)
+      // retired, V(g) that of V(g-2) once PV(g-2) retired
+      auto block_src = [&](long long g, int& j, int& slot, int& sb) {
+        const int it = (int)(g / nb);
+        j = (int)(g - (long long)it * nb);
+        int m0, env, env_start;
+        tile_geom(blockIdx.x + it * gridDim.x, m0, env, env_start, sb);
+        slot = p.env_map ? __ldg(p.env_map + env) : env;
+      };
+      auto load_k = [&](long long g) {
+        int j, slot, sb;
+        block_src(g, j, slot, sb);
+        const int s = (int)(g & 1);
+        uint8_t* st = sKV + s * kStageBytes;
+        sm100::mbar_arrive_expect_tx(&k_full[s], kKBytes);
+        if (j < p.n_prefix_blocks && p.k_img) {
+          bulk_load(st, p.k_img + ((size_t)slot * p.img_blocks + j) * kKBytes, kKBytes, &k_full[s], pol);
+        } else if (j < p.n_prefix_blocks) {
+          for (int c = 0; c < 4; ++c)
+            tma_load_3d(&tm_kp, &k_full[s], st + c * (BKEY * 128), c * 64, j * BKEY, slot, pol);
+        } else {
+          const int row0 = sb + (j - p.n_prefix_blocks) * BKEY;
+          for (int c = 0; c < 4; ++c)
+            sm100::tma_load_2d(&tm_ks, &k_full[s], st + c * (BKEY * 128), c * 64, row0, pol);
+        }
+      };
+      auto load_v = [&](long long g) {
+        int j, slot, sb;
+        block_src(g, j, slot, sb);
+        const int s = (int)(g & 1);
+        uint8_t* st = sKV + s * kStageBytes + kKBytes;
+        sm100::mbar_arrive_expect_tx(&v_full[s], kVBytes);
+        if (j < p.n_prefix_blocks && p.v_img) {
+          bulk_load(st, p.v_img + ((size_t)slot * p.img_blocks + j) * kVBytes, kVBytes, &v_full[s], pol);
+        } else if (j < p.n_prefix_blocks) {
+          tma_load_3d(&tm_vp, &v_full[s], st, j * BKEY, 0, slot, pol);
+        } else {
+          const int row0 = sb + (j - p.n_prefix_blocks) * BKEY;
+          sm100::tma_load_2d(&tm_vs, &v_full[s], st, row0, 0, pol);
+        }
+      };
+      const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      const long long total = (long long)my_tiles * nb;
+      long long nk = 0, nv = 0;
+      int nq = 0;  // Q tiles issued
+      // prefix blocks of the first tile before the PDL wait (independent of the previous kernel)
+      while (nk < min(2LL, total) && (int)nk < p.n_prefix_blocks) {
+        load_k(nk);
+        load_v(nk);
+        ++nk;
+        ++nv;
+      }
+      sm100::pdl_wait();
+      const long long t0 = clock64();
+      while (nk < total || nv < total || nq < my_tiles) {
+        // Q of tile nq once every S MMA of tile nq-1 retired
+        if (nq < my_tiles && (nq == 0 || sm100::mbar_test(sm100::smem_u32(q_empty), (nq - 1) & 1))) {
+          int m0, env, env_start, sb;
+          tile_geom(blockIdx.x + nq * gridDim.x, m0, env, env_start, sb);
+          sm100::mbar_arrive_expect_tx(q_full, kQBytes);
+          for (int c = 0; c < 4; ++c)
+            sm100::tma_load_2d(&tm_q, q_full, sQ + c * (BQ * 128), c * 64, m0 * kHeads, pol);
+          ++nq;
+        }
+        if (nk < total && (nk < 2 || sm100::mbar_test(sm100::smem_u32(&k_empty[nk & 1]), ((nk >> 1) & 1) ^ 1))) {
+          load_k(nk);
+          ++nk;
+        }
+        if (nv < total && nv < nk &&
+            (nv < 2 || sm100::mbar_test(sm100::smem_u32(&v_empty[nv & 1]), ((nv >> 1) & 1) ^ 1))) {
+          load_v(nv);
+          ++nv;
+        }
+        if (clock64() - t0 > (1ll << 34)) {
+          printf("sf: attention producer timeout (block %d)\n", blockIdx.x);
+          __trap();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (sm100::elect_one()) {
+      const uint32_t idesc_s = sm100::make_idesc_bf16(BQ, BKEY);
+      const uint32_t idesc_o = sm100::make_idesc_bf16(BQ, HD);
+      const uint32_t q_addr = sm100::smem_u32(sQ);
+      const uint32_t p_addr = sm100::smem_u32(sP);
+      long long g = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+        const long long g0 = g;
+        sm100::mbar_wait(q_full, it & 1);
+        auto issue_pv = [&](long long gg) {
+          const int i = (int)(gg - g0);
+          if (i == 0 && it > 0) {  // PV(0) overwrites O: the previous tile's O must be drained
+            sm100::mbar_wait(o_free, (it - 1) & 1);
+          }
+          sm100::mbar_wait(&p_full[gg & 1], (gg >> 1) & 1);
+          sm100::mbar_wait(&v_full[gg & 1], (gg >> 1) & 1);
+          sm100::tc_fence_after();
+          const uint32_t v_addr = sm100::smem_u32(sKV + (gg & 1) * kStageBytes + kKBytes);
+#pragma unroll
+          for (int kk = 0; kk < BKEY / 16; ++kk)
+            sm100::umma_bf16(tmem + 128, sm100::make_sw128_desc(p_addr + kk * 32),
+                             sm100::make_sw128_desc(v_addr + kk * 32), idesc_o, (i | kk) != 0);
+          sm100::umma_commit(&pv_done[gg & 1]);
+          sm100::umma_commit(&v_empty[gg & 1]);
+        };
+        for (int i = 0; i < nb; ++i, ++g) {
+          const int s = (int)(g & 1);
+          sm100::mbar_wait(&k_full[s], (g >> 1) & 1);
+          if (g >= 2) sm100::mbar_wait(&s_free[s], ((g >> 1) & 1) ^ 1);
+          sm100::tc_fence_after();
+          const uint32_t k_addr = sm100::smem_u32(sKV + s * kStageBytes);
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const int c = kk >> 2, w = kk & 3;
+            sm100::umma_bf16(tmem + s * BKEY, sm100::make_sw128_desc(q_addr + c * (BQ * 128) + w * 32),
+                             sm100::make_sw128_desc(k_addr + c * (BKEY * 128) + w * 32), idesc_s, kk != 0);
+          }
+          sm100::umma_commit(&s_full[s]);
+          sm100::umma_commit(&k_empty[s]);
+          if (i == nb - 1) sm100::umma_commit(q_empty);  // last S of the tile: Q reusable
+          if (i >= 1) issue_pv(g - 1);
+        }
+        if (nb > 0) issue_pv(g - 1);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
+    sm100::pdl_wait();
+    if (threadIdx.x == 64) sm100::pdl_launch_dependents();
+    long long g = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      int m0, env, env_start, sb;
+      tile_geom(tile, m0, env, env_start, sb);
+      const int tok = m0 + (r >> 3);
+      const int head = r & 7;
+      const int local_q = tok - env_start;
+      const int seg_q = local_q / p.seg_len;
+      const int t_q = local_q - seg_q * p.seg_len;
+      const bool real_q = local_q < p.segs * p.seg_len && tok < p.M;
+      const int seg_lo = seg_q * p.seg_len;
+      const int seg_hi = seg_lo + (t_q >= 1 ? p.seg_len : 1);
+      float m_used = -INFINITY, l_sum = 0.f;
+      for (int i = 0; i < nb; ++i, ++g) {
+        const int j = i;
+        const int s = (int)(g & 1);
+        sm100::mbar_wait(&s_full[s], (g >> 1) & 1);
+        sm100::tc_fence_after();
+        uint32_t raw[2][16];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) sm100::tmem_ld16(t_lane + s * BKEY + half * 32 + c * 16, raw[c]);
+        sm100::tmem_ld_wait();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&s_free[s]);
+        int lo = 0, hi;
+        if (j < p.n_prefix_blocks) {
+          hi = p.prefix_len - j * BKEY;
+        } else if (real_q) {
+          const int base = sb + (j - p.n_prefix_blocks) * BKEY - env_start;
+          lo = seg_lo - base;
+          hi = seg_hi - base;
+        } else {
+          hi = 0;
+        }
+        lo -= half * 32;
+        hi -= half * 32;
+        float sv[32];
+        float mb;
+        if (lo <= 0 && hi >= 32) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) sv[c] = __uint_as_float(raw[c >> 4][c & 15]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const float x = __uint_as_float(raw[c >> 4][c & 15]);
+            sv[c] = (c >= lo && c < hi) ? x : -INFINITY;
+          }
+        }
+        {
+          float t[11];
+#pragma unroll
+          for (int c = 0; c < 10; ++c) t[c] = fmax3(sv[3 * c], sv[3 * c + 1], sv[3 * c + 2]);
+          t[10] = fmaxf(sv[30], sv[31]);
+          const float u0 = fmax3(t[0], t[1], t[2]), u1 = fmax3(t[3], t[4], t[5]);
+          const float u2 = fmax3(t[6], t[7], t[8]), u3 = fmaxf(t[9], t[10]);
+          mb = fmaxf(fmax3(u0, u1, u2), u3);
+        }
+        xm[(s * 2 + half) * BQ + r] = mb;
+        asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+        mb = fmaxf(xm[(s * 2) * BQ + r], xm[(s * 2 + 1) * BQ + r]) * p.scale_log2;
+        const float m_new = fmaxf(m_used, mb);
+        bool rescale = false;
+        float alpha = 1.f;
+        if (m_new > -INFINITY) {
+          if (m_used == -INFINITY) {
+            m_used = m_new;
+          } else if (m_new > m_used + 8.f) {
+            alpha = exp2f(m_used - m_new);
+            m_used = m_new;
+            rescale = true;
+          }
+        }
+        const float mu = m_used == -INFINITY ? 0.f : m_used;
+        uint32_t pw[16];
+        float lp = 0.f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float p0 = ex2_approx(fmaf(sv[2 * k], p.scale_log2, -mu));
+          const float p1 = ex2_approx(fmaf(sv[2 * k + 1], p.scale_log2, -mu));
+          lp += p0 + p1;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+          pw[k] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        if (i >= 1) {
+          sm100::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+          sm100::tc_fence_after();
+        }
+        const bool any_rescale = __any_sync(0xffffffffu, rescale);
+        if (any_rescale && i >= 1) {
+          l_sum *= alpha;
+#pragma unroll 1
+          for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 16) {
+            uint32_t o[16];
+            sm100::tmem_ld16(t_lane + 128 + c0, o);
+            sm100::tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 16; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+            sm100::tmem_st16(t_lane + 128 + c0, o);
+          }
+          sm100::tmem_st_wait();
+        } else if (rescale) {
+          l_sum *= alpha;
+        }
+        l_sum += lp;
+        uint8_t* prow = sP + r * 128;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int cc = half * 4 + c;
+          *reinterpret_cast<uint4*>(prow + ((cc ^ (r & 7)) << 4)) =
+              make_uint4(pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
+        }
+        fence_async_smem();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&p_full[s]);
+      }
+      // O final once the tile's last PV retires
+      if (nb > 0) {
+        sm100::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+        sm100::tc_fence_after();
+      }
+      xm[(2 * 2 + half) * BQ + r] = l_sum;  // dedicated slot 2 for the row sums
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+      l_sum = xm[(2 * 2) * BQ + r] + xm[(2 * 2 + 1) * BQ + r];
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");  // slot 2 free for the next tile
+      const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
+      // O -> registers first, then release TMEM (the next tile's PV(0) may
+      // start), then the slow global stores
+      uint32_t ow[4][2][8];
+#pragma unroll
+      for (int u4 = 0; u4 < 4; ++u4) {
+        uint32_t o[2][16];
+        const int c0 = half * 128 + u4 * 32;
+        sm100::tmem_ld16(t_lane + 128 + c0, o[0]);
+        sm100::tmem_ld16(t_lane + 128 + c0 + 16, o[1]);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[u][2 * k]) * inv,
+                                                      __uint_as_float(o[u][2 * k + 1]) * inv);
+            ow[u4][u][k] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+      }
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(o_free);
+      if (tok < p.M) {
+        __nv_bfloat16* dst = p.out + (size_t)tok * (kHeads * HD) + head * HD + half * 128;
+#pragma unroll
+        for (int u4 = 0; u4 < 4; ++u4)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst + u4 * 32 + 16 * u);
+            d4[0] = make_uint4(ow[u4][u][0], ow[u4][u][1], ow[u4][u][2], ow[u4][u][3]);
+            d4[1] = make_uint4(ow[u4][u][4], ow[u4][u][5], ow[u4][u][6], ow[u4][u][7]);
+          }
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
 // ------------------------------------------------ batched: 2-SM CTA pairs
 //
 // attn_pair_kernel: two consecutive query tiles of one env run on a CTA pair

@@ -1104,6 +1104,41 @@ int launch_attn_pair(const Buffers& b, int l, cudaStream_t s, bool pdl) {
 
 int launch_attn(const Buffers& b, int l, cudaStream_t s, bool pdl) {
   if (b.attn_pair) return launch_attn_pair(b, l, s, pdl);
+  if (b.attn_splits == 1 && getenv("SF_NO_ATTN_PERSIST") == nullptr) {
+    // batched: persistent CTAs (one per SM) walk the query tiles
+    static bool pattr = false;
+    static int nsm = 148;
+    if (!pattr) {
+      SF_CHECK_CUDA(cudaFuncSetAttribute(attn::attn_persistent_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)attn::kSmemBytes));
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      pattr = true;
+    }
+    const CUtensorMap* mp = &b.attn_maps[5 * l];
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(b.attn_tiles < nsm ? b.attn_tiles : nsm);
+    cfg.blockDim = dim3(attn::kThreads);
+    cfg.dynamicSmemBytes = attn::kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = a;
+    cfg.numAttrs = 1;
+    attn::Params ap = b.ap;
+    if (b.k_img) {
+      const size_t per_layer = (size_t)b.n_img_envs * b.img_blocks * 32768;
+      ap.k_img = b.k_img + (size_t)l * per_layer;
+      ap.v_img = b.v_img + (size_t)l * per_layer;
+      ap.img_blocks = b.img_blocks;
+    }
+    SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, attn::attn_persistent_kernel, mp[0], mp[1], mp[2], mp[3], mp[4], ap));
+    count_launch();
+    return SF_OK;
+  }
   static bool attr = false;
   if (!attr) {
     SF_CHECK_CUDA(cudaFuncSetAttribute(attn::attn_kernel,
