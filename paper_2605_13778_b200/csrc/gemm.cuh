@@ -164,8 +164,10 @@ __device__ __forceinline__ void epi_swap(const EpiArgs& e, int n, int m0, const 
 template <int KIND>
 __device__ __forceinline__ void epi_normal(const EpiArgs& e, int m, int n0, float (&v)[16], float rs,
                                            float& ssq_acc, __nv_bfloat16* vbuf = nullptr) {
-  // the warp-cooperative V^T transpose needs every lane, valid row or not
-  if (m >= e.M && !(KIND == EPI_QKV && vbuf && n0 >= e.q_features + 256)) return;
+  // the warp-cooperative paths (V^T transpose, staged residual) need every
+  // lane, valid row or not
+  if (m >= e.M && !(KIND == EPI_QKV && vbuf && n0 >= e.q_features + 256) && !(KIND == EPI_RESID && vbuf))
+    return;
   const bool full = n0 + 16 <= e.N;
   if (KIND == EPI_F32 || KIND == EPI_BF16 || KIND == EPI_TANH_BF16) {
 #pragma unroll
@@ -260,6 +262,59 @@ __device__ __forceinline__ void epi_normal(const EpiArgs& e, int m, int n0, floa
       }
     }
   } else if (KIND == EPI_RESID) {
+    if (vbuf) {
+      // Coalesced residual update: the warp's 32 rows x 16 columns go through
+      // a per-warp SMEM scratch so that every load/store instruction covers
+      // 8 rows x 64 contiguous bytes (instead of 32 rows x 16 B).
+      float* sc = reinterpret_cast<float*>(vbuf);  // [32][16], quads XOR-swizzled by row
+      const int lane = threadIdx.x & 31;
+      const int m0w = m - lane;
+#pragma unroll
+      for (int qd = 0; qd < 4; ++qd)
+        reinterpret_cast<float4*>(sc + lane * 16)[qd ^ (lane & 3)] =
+            make_float4(v[4 * qd], v[4 * qd + 1], v[4 * qd + 2], v[4 * qd + 3]);
+      __syncwarp();
+      float rowsq[4];
+      float4 xo[4];
+      const int qd = lane & 3;
+#pragma unroll
+      for (int pass = 0; pass < 4; ++pass) {  // every residual load in flight first
+        const int row = m0w + pass * 8 + (lane >> 2);
+        xo[pass] = row < e.M ? *reinterpret_cast<const float4*>(e.x + (size_t)row * e.N + n0 + qd * 4)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int pass = 0; pass < 4; ++pass) {
+        const int rr = pass * 8 + (lane >> 2);
+        const int row = m0w + rr;
+        const float4 a = reinterpret_cast<const float4*>(sc + rr * 16)[qd ^ (rr & 3)];
+        float4 x4 = xo[pass];
+        x4.x += a.x;
+        x4.y += a.y;
+        x4.z += a.z;
+        x4.w += a.w;
+        float sq = 0.f;
+        if (row < e.M) {
+          *reinterpret_cast<float4*>(e.x + (size_t)row * e.N + n0 + qd * 4) = x4;
+          *reinterpret_cast<uint2*>(e.xb + (size_t)row * e.N + n0 + qd * 4) =
+              make_uint2(pack_bf16(x4.x, x4.y), pack_bf16(x4.z, x4.w));
+          sq = x4.x * x4.x + x4.y * x4.y + x4.z * x4.z + x4.w * x4.w;
+        }
+        sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+        sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+        rowsq[pass] = sq;
+      }
+      // row rr's chunk sum back to its owner lane rr (lane (rr % 8) * 4 of pass rr / 8)
+      float mine = 0.f;
+#pragma unroll
+      for (int pass = 0; pass < 4; ++pass) {
+        const float t = __shfl_sync(0xffffffffu, rowsq[pass], (lane & 7) * 4);
+        if ((lane >> 3) == pass) mine = t;
+      }
+      ssq_acc += mine;
+      __syncwarp();
+      return;
+    }
     float* xr = e.x + (size_t)m * e.N + n0;
     __nv_bfloat16* xbr = e.xb + (size_t)m * e.N + n0;
     uint32_t w[8];
@@ -355,7 +410,7 @@ struct Tail {
   float* rs;             // [256]
   float* red;            // [4][256]
   float* sred;           // [2][2][128] (normal-mode ssq partials per warp group)
-  __nv_bfloat16* vbuf;   // [8 warps][16 x 32] V^T transpose staging (QKV epilogue)
+  __nv_bfloat16* vbuf;   // [8 warps][2 KB] epilogue staging (V^T transpose, residual)
 };
 
 __device__ __forceinline__ Tail carve_tail(uint8_t* smem, const Params& p) {
@@ -373,7 +428,7 @@ __device__ __forceinline__ Tail carve_tail(uint8_t* smem, const Params& p) {
   return t;
 }
 
-constexpr size_t kTailBytes = 8 * (2 * 16 + 4) + 16 + 4 * (256 + 4 * 256 + 2 * 2 * 128) + 8 * 16 * 32 * 2;
+constexpr size_t kTailBytes = 8 * (2 * 16 + 4) + 16 + 4 * (256 + 4 * 256 + 2 * 2 * 128) + 8 * 2048;
 
 // -------------------------------------------------- batch-1: swap + cluster split-K
 
@@ -693,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[u][j]);
           float acc = 0.f;
-          epi_normal<KIND>(e, m, tb * p.bn + c * 16, v, rs, acc, T.vbuf + (warp - 2) * 512);
+          epi_normal<KIND>(e, m, tb * p.bn + c * 16, v, rs, acc, T.vbuf + (warp - 2) * 1024);
           if (c * 16 < 128) ssq0 += acc;
           else ssq1 += acc;
         }
@@ -893,7 +948,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[u][j]);
           float acc = 0.f;
           if (tn * 256 + c * 16 < e.N)
-            epi_normal<KIND>(e, m, tn * 256 + c * 16, v, rs, acc, T.vbuf + (warp - 2) * 512);
+            epi_normal<KIND>(e, m, tn * 256 + c * 16, v, rs, acc, T.vbuf + (warp - 2) * 1024);
           if (c * 16 < 128) ssq0 += acc;
           else ssq1 += acc;
         }
