@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool real_q = local_q < p.segs * p.seg_len && tok < p.M;
     const int seg_lo = seg_q * p.seg_len;                         // local token range of the
     const int seg_hi = seg_lo + (t_q >= 1 ? p.seg_len : 1);       // row's visible suffix keys
-    float* xm = reinterpret_cast<float*>(bars + 32);              // [2 parity][2 half][128]
+    __shared__ float xm[2 * 2 * BQ];                              // [2 parity][2 half][128]
     float m_used = -INFINITY, l_sum = 0.f;
     sm100::pdl_wait();
     if (threadIdx.x == 64) sm100::pdl_launch_dependents();
@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* q_empty = bars + 17;  // all S MMAs of a tile retired: Q reusable
   uint64_t* o_free = bars + 18;   // softmax warps read O out of TMEM: next PV(0) may overwrite
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
-  float* xm = reinterpret_cast<float*>(bars + 32);  // [3 slots][2 half][128]
+  __shared__ float xm[3 * 2 * BQ];  // [3 slots][2 half][128] (static: LDS/STS, not generic)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = p.n_blocks;
