@@ -610,6 +610,7 @@ int build(Handle& h, Buffers& b, int B, int K) {
   if (asplit < 1) asplit = 1;
   if (asplit > n_blocks) asplit = n_blocks;
   if (asplit > attn::kMaxSplitsKV) asplit = attn::kMaxSplitsKV;
+  if (asplit > 8 && !getenv("SF_ATTN_SPLITS")) asplit = 8;  // merge traffic grows with the split count (Euler: 8 beats 16)
   const int bps = (n_blocks + asplit - 1) / asplit;
   asplit = (n_blocks + bps - 1) / bps;
   b.attn_splits = asplit;  // split-KV CTAs of a tile form one cluster (DSMEM merge)
