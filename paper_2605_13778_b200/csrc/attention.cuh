@@ -42,7 +42,16 @@ constexpr uint32_t kStageBytes = kKBytes + kVBytes;
 // control region after P: mbarriers (256 B) + the softmax pair exchange (2 KB)
 constexpr uint32_t kCtlBytes = 4096;
 constexpr uint32_t kSmemBytes = kQBytes + 2 * kStageBytes + kPBytes + kCtlBytes + 1024 /*align*/;
-constexpr int kTmemCols = 512;  // S0 [0,64) S1 [64,128) O [128,384)
+constexpr int kTmemCols = 512;  // S0 [0,64) S1 [64,128) O [128,384) (+ P0/P1 bf16 [384,448))
+// persistent kernel SMEM: Q | 3 K slots | 2 V^T slots | barriers + row-max exchange (2 KB)
+#ifndef SF_ATTN_EXPT
+#define SF_ATTN_EXPT 0
+#endif
+constexpr int kPersistKSlots = 3;
+constexpr uint32_t kPersistSmemUsed = kQBytes + kPersistKSlots * kKBytes + 2 * kVBytes + 256 + 2 * 2 * BQ * 4;
+constexpr uint32_t kPersistSmemBytes = 227 * 1024;  // the 1024 B alignment pad must fit in the slack
+static_assert(kPersistSmemUsed <= kPersistSmemBytes, "persistent attention SMEM");
+constexpr uint32_t kPCol = 384;  // persistent kernel: P(g) for slot s at kPCol + s * BKEY / 2
 constexpr int kPartStride = HD + 2;  // split-KV partial O row stride in SMEM (floats)
 constexpr int kMaxSplitsKV = 16;     // split-KV cluster size limit
 
@@ -686,22 +695,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sKV = smem + kQBytes;
-  uint8_t* sP = sKV + 2 * kStageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kPBytes);
+  uint8_t* sK = smem + kQBytes;               // kPersistKSlots x 32 KB
+  uint8_t* sV = sK + kPersistKSlots * kKBytes;  // 2 x 32 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kVBytes);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;    // [2]
-  uint64_t* k_empty = bars + 3;   // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* s_free = bars + 7;    // [2]
-  uint64_t* p_full = bars + 9;    // [2]
-  uint64_t* pv_done = bars + 11;  // [2]
-  uint64_t* v_full = bars + 13;   // [2]
-  uint64_t* v_empty = bars + 15;  // [2]
-  uint64_t* q_empty = bars + 17;  // all S MMAs of a tile retired: Q reusable
-  uint64_t* o_free = bars + 18;   // softmax warps read O out of TMEM: next PV(0) may overwrite
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
-  __shared__ float xm[3 * 2 * BQ];  // [3 slots][2 half][128] (static: LDS/STS, not generic)
+  uint64_t* k_full = bars + 1;    // [3]
+  uint64_t* k_empty = bars + 4;   // [3]
+  uint64_t* s_full = bars + 7;    // [2]
+  uint64_t* s_free = bars + 9;    // [2]
+  uint64_t* p_full = bars + 11;   // [2]
+  uint64_t* pv_done = bars + 13;  // [2]
+  uint64_t* v_full = bars + 15;   // [2]
+  uint64_t* v_empty = bars + 17;  // [2]
+  uint64_t* q_empty = bars + 19;  // all S MMAs of a tile retired: Q reusable
+  uint64_t* o_free = bars + 20;   // softmax warps read O out of TMEM: next PV(0) may overwrite
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
+  float* xm = reinterpret_cast<float*>(bars + 32);  // [2 slots][2 half][128]
+  if (threadIdx.x == 0 && smem + kPersistSmemUsed > smem_raw + kPersistSmemBytes) __trap();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = p.n_blocks;
@@ -718,9 +728,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::mbar_init(q_full, 1);
     sm100::mbar_init(q_empty, 1);
     sm100::mbar_init(o_free, 256);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kPersistKSlots; ++s) {
       sm100::mbar_init(&k_full[s], 1);
       sm100::mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&v_full[s], 1);
       sm100::mbar_init(&v_empty[s], 1);
       sm100::mbar_init(&s_full[s], 1);
@@ -744,20 +756,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::tma_prefetch_desc(&tm_ks);
       sm100::tma_prefetch_desc(&tm_vs);
       const uint64_t pol = sm100::policy_evict_last();
-      // global block g -> (tile, j); K(g) reuses the slot of K(g-2) once S(g-2)
-      // retired, V(g) that of V(g-2) once PV(g-2) retired
-      auto block_src = [&](long long g, int& j, int& slot, int& sb) {
-        const int it = (int)(g / nb);
-        j = (int)(g - (long long)it * nb);
-        int m0, env, env_start;
-        tile_geom(blockIdx.x + it * gridDim.x, m0, env, env_start, sb);
-        slot = p.env_map ? __ldg(p.env_map + env) : env;
+      // Block cursors (tile it, key block j) for the next K and V loads, advanced
+      // incrementally (no 64-bit divisions on the issuing thread); the tile's
+      // prefix-KV pool slot and first suffix block are looked up once per tile.
+      // K(g) reuses the slot of K(g-3) once S(g-3) retired, V(g) that of V(g-2)
+      // once PV(g-2) retired.
+      struct Cursor {
+        int it = 0, j = 0, slot = 0, sb = 0;
       };
-      auto load_k = [&](long long g) {
-        int j, slot, sb;
-        block_src(g, j, slot, sb);
-        const int s = (int)(g & 1);
-        uint8_t* st = sKV + s * kStageBytes;
+      auto cursor_tile = [&](Cursor& c) {
+        const int tile = blockIdx.x + c.it * gridDim.x;
+        if (tile >= n_tiles) return;  // past this CTA's last tile
+        int m0, env, env_start;
+        tile_geom(tile, m0, env, env_start, c.sb);
+        c.slot = p.env_map ? __ldg(p.env_map + env) : env;
+      };
+      auto cursor_next = [&](Cursor& c) {
+        if (++c.j == nb) {
+          c.j = 0;
+          ++c.it;
+          cursor_tile(c);
+        }
+      };
+      Cursor ck, cv;
+      cursor_tile(ck);
+      cv = ck;
+      int k_s = 0;
+      uint32_t k_ph = 0;  // slot and ring phase of the next K
+      auto load_k = [&]() {
+        const int j = ck.j, slot = ck.slot, sb = ck.sb;
+        const int s = k_s;
+        uint8_t* st = sK + s * kKBytes;
         sm100::mbar_arrive_expect_tx(&k_full[s], kKBytes);
         if (j < p.n_prefix_blocks && p.k_img) {
           bulk_load(st, p.k_img + ((size_t)slot * p.img_blocks + j) * kKBytes, kKBytes, &k_full[s], pol);
@@ -769,12 +798,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < 4; ++c)
             sm100::tma_load_2d(&tm_ks, &k_full[s], st + c * (BKEY * 128), c * 64, row0, pol);
         }
+        if (++k_s == kPersistKSlots) {
+          k_s = 0;
+          k_ph ^= 1;
+        }
+        cursor_next(ck);
       };
       auto load_v = [&](long long g) {
-        int j, slot, sb;
-        block_src(g, j, slot, sb);
+        const int j = cv.j, slot = cv.slot, sb = cv.sb;
         const int s = (int)(g & 1);
-        uint8_t* st = sKV + s * kStageBytes + kKBytes;
+        uint8_t* st = sV + s * kVBytes;
         sm100::mbar_arrive_expect_tx(&v_full[s], kVBytes);
         if (j < p.n_prefix_blocks && p.v_img) {
           bulk_load(st, p.v_img + ((size_t)slot * p.img_blocks + j) * kVBytes, kVBytes, &v_full[s], pol);
@@ -784,6 +817,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int row0 = sb + (j - p.n_prefix_blocks) * BKEY;
           sm100::tma_load_2d(&tm_vs, &v_full[s], st, row0, 0, pol);
         }
+        cursor_next(cv);
       };
       const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
       const long long total = (long long)my_tiles * nb;
@@ -791,7 +825,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int nq = 0;  // Q tiles issued
       // prefix blocks of the first tile before the PDL wait (independent of the previous kernel)
       while (nk < min(2LL, total) && (int)nk < p.n_prefix_blocks) {
-        load_k(nk);
+        load_k();
         load_v(nk);
         ++nk;
         ++nv;
@@ -808,8 +842,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm100::tma_load_2d(&tm_q, q_full, sQ + c * (BQ * 128), c * 64, m0 * kHeads, pol);
           ++nq;
         }
-        if (nk < total && (nk < 2 || sm100::mbar_test(sm100::smem_u32(&k_empty[nk & 1]), ((nk >> 1) & 1) ^ 1))) {
-          load_k(nk);
+        if (nk < total && (nk < kPersistKSlots || sm100::mbar_test(sm100::smem_u32(&k_empty[k_s]), k_ph ^ 1))) {
+          load_k();
           ++nk;
         }
         if (nv < total && nv < nk &&
@@ -828,9 +862,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc_s = sm100::make_idesc_bf16(BQ, BKEY);
       const uint32_t idesc_o = sm100::make_idesc_bf16(BQ, HD);
       const uint32_t q_addr = sm100::smem_u32(sQ);
-      const uint32_t p_addr = sm100::smem_u32(sP);
       long long g = 0;
       int it = 0;
+      int ks = 0;
+      uint32_t kph = 0;  // K ring slot / phase of block g
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
         const long long g0 = g;
         sm100::mbar_wait(q_full, it & 1);
@@ -842,20 +877,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::mbar_wait(&p_full[gg & 1], (gg >> 1) & 1);
           sm100::mbar_wait(&v_full[gg & 1], (gg >> 1) & 1);
           sm100::tc_fence_after();
-          const uint32_t v_addr = sm100::smem_u32(sKV + (gg & 1) * kStageBytes + kKBytes);
+          const uint32_t v_addr = sm100::smem_u32(sV + (gg & 1) * kVBytes);
+          const uint32_t p_tmem = tmem + kPCol + (uint32_t)(gg & 1) * (BKEY / 2);
 #pragma unroll
-          for (int kk = 0; kk < BKEY / 16; ++kk)
-            sm100::umma_bf16(tmem + 128, sm100::make_sw128_desc(p_addr + kk * 32),
-                             sm100::make_sw128_desc(v_addr + kk * 32), idesc_o, (i | kk) != 0);
+          for (int kk = 0; kk < BKEY / 16; ++kk)  // A = P from TMEM: 16 keys = 8 columns per MMA
+            sm100::umma_bf16_ts(tmem + 128, p_tmem + kk * 8, sm100::make_sw128_desc(v_addr + kk * 32),
+                                idesc_o, (i | kk) != 0);
           sm100::umma_commit(&pv_done[gg & 1]);
           sm100::umma_commit(&v_empty[gg & 1]);
         };
         for (int i = 0; i < nb; ++i, ++g) {
           const int s = (int)(g & 1);
-          sm100::mbar_wait(&k_full[s], (g >> 1) & 1);
+          sm100::mbar_wait(&k_full[ks], kph);
           if (g >= 2) sm100::mbar_wait(&s_free[s], ((g >> 1) & 1) ^ 1);
           sm100::tc_fence_after();
-          const uint32_t k_addr = sm100::smem_u32(sKV + s * kStageBytes);
+          const uint32_t k_addr = sm100::smem_u32(sK + ks * kKBytes);
 #pragma unroll
           for (int kk = 0; kk < HD / 16; ++kk) {
             const int c = kk >> 2, w = kk & 3;
@@ -863,7 +899,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                              sm100::make_sw128_desc(k_addr + c * (BKEY * 128) + w * 32), idesc_s, kk != 0);
           }
           sm100::umma_commit(&s_full[s]);
-          sm100::umma_commit(&k_empty[s]);
+          sm100::umma_commit(&k_empty[ks]);
+          if (++ks == kPersistKSlots) {
+            ks = 0;
+            kph ^= 1;
+          }
           if (i == nb - 1) sm100::umma_commit(q_empty);  // last S of the tile: Q reusable
           if (i >= 1) issue_pv(g - 1);
         }
@@ -935,9 +975,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float u2 = fmax3(t[6], t[7], t[8]), u3 = fmaxf(t[9], t[10]);
           mb = fmaxf(fmax3(u0, u1, u2), u3);
         }
+#if SF_ATTN_EXPT >= 1  // timing experiment only (wrong results): no row-max exchange
+        mb *= p.scale_log2;
+#else
         xm[(s * 2 + half) * BQ + r] = mb;
         asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
         mb = fmaxf(xm[(s * 2) * BQ + r], xm[(s * 2 + 1) * BQ + r]) * p.scale_log2;
+#endif
         const float m_new = fmaxf(m_used, mb);
         bool rescale = false;
         float alpha = 1.f;
@@ -955,18 +999,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         float lp = 0.f;
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
+#if SF_ATTN_EXPT >= 2  // timing experiment only: no exponentials
+          const float p0 = fmaf(sv[2 * k], p.scale_log2, -mu);
+          const float p1 = fmaf(sv[2 * k + 1], p.scale_log2, -mu);
+#else
           const float p0 = ex2_approx(fmaf(sv[2 * k], p.scale_log2, -mu));
           const float p1 = ex2_approx(fmaf(sv[2 * k + 1], p.scale_log2, -mu));
+#endif
           lp += p0 + p1;
           __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
           pw[k] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        if (i >= 1) {
-          sm100::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+        // P slot s is free once PV(g-2) retired; PV(g-1) may still run
+        // unless O has to be rescaled
+        if (g >= 2) {
+          sm100::mbar_wait(&pv_done[s], ((g - 2) >> 1) & 1);
           sm100::tc_fence_after();
         }
         const bool any_rescale = __any_sync(0xffffffffu, rescale);
         if (any_rescale && i >= 1) {
+          sm100::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+          sm100::tc_fence_after();
           l_sum *= alpha;
 #pragma unroll 1
           for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 16) {
@@ -982,14 +1035,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           l_sum *= alpha;
         }
         l_sum += lp;
-        uint8_t* prow = sP + r * 128;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int cc = half * 4 + c;
-          *reinterpret_cast<uint4*>(prow + ((cc ^ (r & 7)) << 4)) =
-              make_uint4(pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
-        }
-        fence_async_smem();
+        sm100::tmem_st16(t_lane + kPCol + s * (BKEY / 2) + half * 16, pw);
+        sm100::tmem_st_wait();
         sm100::tc_fence_before();
         sm100::mbar_arrive(&p_full[s]);
       }
@@ -998,10 +1045,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
         sm100::tc_fence_after();
       }
-      xm[(2 * 2 + half) * BQ + r] = l_sum;  // dedicated slot 2 for the row sums
+      // row sums through slot g & 1 (last read for block g - 2, before block g - 1's barrier)
+      const int ls = (int)(g & 1);
+      xm[(ls * 2 + half) * BQ + r] = l_sum;
       asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
-      l_sum = xm[(2 * 2) * BQ + r] + xm[(2 * 2 + 1) * BQ + r];
-      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");  // slot 2 free for the next tile
+      l_sum = xm[(ls * 2) * BQ + r] + xm[(ls * 2 + 1) * BQ + r];
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");  // slot free for the next tile's block g
       const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
       // O -> registers first, then release TMEM (the next tile's PV(0) may
       // start), then the slow global stores

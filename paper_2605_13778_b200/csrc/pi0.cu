@@ -1112,7 +1112,7 @@ int launch_attn(const Buffers& b, int l, cudaStream_t s, bool pdl) {
     if (!pattr) {
       SF_CHECK_CUDA(cudaFuncSetAttribute(attn::attn_persistent_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)attn::kSmemBytes));
+                                         (int)attn::kPersistSmemBytes));
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -1122,7 +1122,7 @@ int launch_attn(const Buffers& b, int l, cudaStream_t s, bool pdl) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(b.attn_tiles < nsm ? b.attn_tiles : nsm);
     cfg.blockDim = dim3(attn::kThreads);
-    cfg.dynamicSmemBytes = attn::kSmemBytes;
+    cfg.dynamicSmemBytes = attn::kPersistSmemBytes;
     cfg.stream = s;
     cudaLaunchAttribute a[1];
     a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
