@@ -43,12 +43,14 @@ constexpr uint32_t kStageBytes = kKBytes + kVBytes;
 constexpr uint32_t kCtlBytes = 4096;
 constexpr uint32_t kSmemBytes = kQBytes + 2 * kStageBytes + kPBytes + kCtlBytes + 1024 /*align*/;
 constexpr int kTmemCols = 512;  // S0 [0,64) S1 [64,128) O [128,384) (+ P0/P1 bf16 [384,448))
-// persistent kernel SMEM: Q | 3 K slots | 2 V^T slots | barriers + row-max exchange (2 KB)
-#ifndef SF_ATTN_EXPT
-#define SF_ATTN_EXPT 0
+// persistent kernel SMEM: Q | K slots | V^T slots (5 x 32 KB together) | barriers + row-max exchange (2 KB)
+#ifndef SF_ATTN_KSLOTS
+#define SF_ATTN_KSLOTS 2
 #endif
-constexpr int kPersistKSlots = 3;
-constexpr uint32_t kPersistSmemUsed = kQBytes + kPersistKSlots * kKBytes + 2 * kVBytes + 256 + 2 * 2 * BQ * 4;
+constexpr int kPersistKSlots = SF_ATTN_KSLOTS;
+constexpr int kPersistVSlots = 5 - SF_ATTN_KSLOTS;
+constexpr uint32_t kPersistSmemUsed =
+    kQBytes + kPersistKSlots * kKBytes + kPersistVSlots * kVBytes + 256 + 2 * 2 * BQ * 4;
 constexpr uint32_t kPersistSmemBytes = 227 * 1024;  // the 1024 B alignment pad must fit in the slack
 static_assert(kPersistSmemUsed <= kPersistSmemBytes, "persistent attention SMEM");
 constexpr uint32_t kPCol = 384;  // persistent kernel: P(g) for slot s at kPCol + s * BKEY / 2
@@ -696,20 +698,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sK = smem + kQBytes;               // kPersistKSlots x 32 KB
-  uint8_t* sV = sK + kPersistKSlots * kKBytes;  // 2 x 32 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kVBytes);
+  uint8_t* sV = sK + kPersistKSlots * kKBytes;  // kPersistVSlots x 32 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kPersistVSlots * kVBytes);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;    // [3]
-  uint64_t* k_empty = bars + 4;   // [3]
-  uint64_t* s_full = bars + 7;    // [2]
-  uint64_t* s_free = bars + 9;    // [2]
-  uint64_t* p_full = bars + 11;   // [2]
-  uint64_t* pv_done = bars + 13;  // [2]
-  uint64_t* v_full = bars + 15;   // [2]
-  uint64_t* v_empty = bars + 17;  // [2]
-  uint64_t* q_empty = bars + 19;  // all S MMAs of a tile retired: Q reusable
-  uint64_t* o_free = bars + 20;   // softmax warps read O out of TMEM: next PV(0) may overwrite
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
+  uint64_t* k_full = bars + 1;    // [<= 4]
+  uint64_t* k_empty = bars + 5;   // [<= 4]
+  uint64_t* s_full = bars + 9;    // [2]
+  uint64_t* s_free = bars + 11;   // [2]
+  uint64_t* p_full = bars + 13;   // [2]
+  uint64_t* pv_done = bars + 15;  // [2]
+  uint64_t* v_full = bars + 17;   // [<= 4]
+  uint64_t* v_empty = bars + 21;  // [<= 4]
+  uint64_t* q_empty = bars + 25;  // all S MMAs of a tile retired: Q reusable
+  uint64_t* o_free = bars + 26;   // softmax warps read O out of TMEM: next PV(0) may overwrite
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 27);
   float* xm = reinterpret_cast<float*>(bars + 32);  // [2 slots][2 half][128]
   if (threadIdx.x == 0 && smem + kPersistSmemUsed > smem_raw + kPersistSmemBytes) __trap();
 
@@ -732,9 +734,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::mbar_init(&k_full[s], 1);
       sm100::mbar_init(&k_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kPersistVSlots; ++s) {
       sm100::mbar_init(&v_full[s], 1);
       sm100::mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&s_full[s], 1);
       sm100::mbar_init(&s_free[s], 256);
       sm100::mbar_init(&p_full[s], 256);
@@ -804,9 +808,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         cursor_next(ck);
       };
-      auto load_v = [&](long long g) {
+      int v_s = 0;
+      uint32_t v_ph = 0;  // slot and ring phase of the next V
+      auto load_v = [&]() {
         const int j = cv.j, slot = cv.slot, sb = cv.sb;
-        const int s = (int)(g & 1);
+        const int s = v_s;
         uint8_t* st = sV + s * kVBytes;
         sm100::mbar_arrive_expect_tx(&v_full[s], kVBytes);
         if (j < p.n_prefix_blocks && p.v_img) {
@@ -817,6 +823,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int row0 = sb + (j - p.n_prefix_blocks) * BKEY;
           sm100::tma_load_2d(&tm_vs, &v_full[s], st, row0, 0, pol);
         }
+        if (++v_s == kPersistVSlots) {
+          v_s = 0;
+          v_ph ^= 1;
+        }
         cursor_next(cv);
       };
       const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -826,7 +836,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // prefix blocks of the first tile before the PDL wait (independent of the previous kernel)
       while (nk < min(2LL, total) && (int)nk < p.n_prefix_blocks) {
         load_k();
-        load_v(nk);
+        load_v();
         ++nk;
         ++nv;
       }
@@ -847,8 +857,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++nk;
         }
         if (nv < total && nv < nk &&
-            (nv < 2 || sm100::mbar_test(sm100::smem_u32(&v_empty[nv & 1]), ((nv >> 1) & 1) ^ 1))) {
-          load_v(nv);
+            (nv < kPersistVSlots || sm100::mbar_test(sm100::smem_u32(&v_empty[v_s]), v_ph ^ 1))) {
+          load_v();
           ++nv;
         }
         if (clock64() - t0 > (1ll << 34)) {
@@ -864,8 +874,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t q_addr = sm100::smem_u32(sQ);
       long long g = 0;
       int it = 0;
-      int ks = 0;
-      uint32_t kph = 0;  // K ring slot / phase of block g
+      int ks = 0, vs = 0;
+      uint32_t kph = 0, vph = 0;  // K ring slot / phase of block g, V ring of the next PV
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
         const long long g0 = g;
         sm100::mbar_wait(q_full, it & 1);
@@ -875,16 +885,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm100::mbar_wait(o_free, (it - 1) & 1);
           }
           sm100::mbar_wait(&p_full[gg & 1], (gg >> 1) & 1);
-          sm100::mbar_wait(&v_full[gg & 1], (gg >> 1) & 1);
+          sm100::mbar_wait(&v_full[vs], vph);
           sm100::tc_fence_after();
-          const uint32_t v_addr = sm100::smem_u32(sV + (gg & 1) * kVBytes);
+          const uint32_t v_addr = sm100::smem_u32(sV + vs * kVBytes);
           const uint32_t p_tmem = tmem + kPCol + (uint32_t)(gg & 1) * (BKEY / 2);
 #pragma unroll
           for (int kk = 0; kk < BKEY / 16; ++kk)  // A = P from TMEM: 16 keys = 8 columns per MMA
             sm100::umma_bf16_ts(tmem + 128, p_tmem + kk * 8, sm100::make_sw128_desc(v_addr + kk * 32),
                                 idesc_o, (i | kk) != 0);
           sm100::umma_commit(&pv_done[gg & 1]);
-          sm100::umma_commit(&v_empty[gg & 1]);
+          sm100::umma_commit(&v_empty[vs]);
+          if (++vs == kPersistVSlots) {
+            vs = 0;
+            vph ^= 1;
+          }
         };
         for (int i = 0; i < nb; ++i, ++g) {
           const int s = (int)(g & 1);
@@ -975,13 +989,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float u2 = fmax3(t[6], t[7], t[8]), u3 = fmaxf(t[9], t[10]);
           mb = fmaxf(fmax3(u0, u1, u2), u3);
         }
-#if SF_ATTN_EXPT >= 1  // timing experiment only (wrong results): no row-max exchange
-        mb *= p.scale_log2;
-#else
         xm[(s * 2 + half) * BQ + r] = mb;
         asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
         mb = fmaxf(xm[(s * 2) * BQ + r], xm[(s * 2 + 1) * BQ + r]) * p.scale_log2;
-#endif
         const float m_new = fmaxf(m_used, mb);
         bool rescale = false;
         float alpha = 1.f;
@@ -999,13 +1009,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float lp = 0.f;
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-#if SF_ATTN_EXPT >= 2  // timing experiment only: no exponentials
-          const float p0 = fmaf(sv[2 * k], p.scale_log2, -mu);
-          const float p1 = fmaf(sv[2 * k + 1], p.scale_log2, -mu);
-#else
           const float p0 = ex2_approx(fmaf(sv[2 * k], p.scale_log2, -mu));
           const float p1 = ex2_approx(fmaf(sv[2 * k + 1], p.scale_log2, -mu));
-#endif
           lp += p0 + p1;
           __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
           pw[k] = *reinterpret_cast<uint32_t*>(&b2);

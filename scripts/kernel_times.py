@@ -22,6 +22,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--envs", type=int, nargs="+", default=[1])
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--per-layer", action="store_true")
     args = ap.parse_args()
     cfg = PI0
     ae = ActionExpert(cfg, n_envs=max(args.envs))
@@ -47,6 +48,8 @@ def main():
             agg[name.split(".")[-1]].append(t)
         total = sum(best)
         print(f"envs={E}: {len(best)} kernels, {total:.1f} us total (eager, warm, no PDL)")
+        if args.per_layer:
+            print("  attn per layer:", " ".join(f"{t:.0f}" for t in agg["attn"]))
         for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
             print(f"  {k:10s} n={len(v):3d} sum {sum(v):9.1f} us ({100 * sum(v) / total:4.1f}%)  "
                   f"avg {sum(v) / len(v):8.2f} us  min {min(v):7.2f}  max {max(v):7.2f}")
