@@ -716,14 +716,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0 && smem + kPersistSmemUsed > smem_raw + kPersistSmemBytes) __trap();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nb = p.n_blocks;
   const int n_tiles = p.tiles;
-  auto tile_geom = [&](int tile, int& m0, int& env, int& env_start, int& sb) {
+  // tile -> first token, env, first suffix key block (sb) and the number of key
+  // blocks the tile visits: the prefix blocks plus the suffix blocks covering
+  // the segments of its 16 tokens (p.n_blocks is the bound over all tiles)
+  auto tile_geom = [&](int tile, int& m0, int& env, int& env_start, int& sb, int& nbt) {
     m0 = tile * 16;
     env = m0 / p.env_rows;
     env_start = env * p.env_rows;
-    const int seg_first = (m0 - env_start) / p.seg_len;
+    const int lo = m0 - env_start;
+    const int seg_first = lo / p.seg_len;
+    int hi = min(lo + 15, p.segs * p.seg_len - 1);
+    hi = hi < lo ? lo : hi;
+    const int seg_last = hi / p.seg_len;
     sb = (env_start + seg_first * p.seg_len) & ~(BKEY - 1);
+    const int n_suf = (env_start + (seg_last + 1) * p.seg_len - sb + BKEY - 1) / BKEY;
+    nbt = p.n_prefix_blocks + min(n_suf, p.n_blocks - p.n_prefix_blocks);
   };
 
   if (warp == 0 && lane == 0) {
@@ -766,17 +774,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       // K(g) reuses the slot of K(g-3) once S(g-3) retired, V(g) that of V(g-2)
       // once PV(g-2) retired.
       struct Cursor {
-        int it = 0, j = 0, slot = 0, sb = 0;
+        int it = 0, j = 0, slot = 0, sb = 0, nb = 0;
       };
       auto cursor_tile = [&](Cursor& c) {
         const int tile = blockIdx.x + c.it * gridDim.x;
         if (tile >= n_tiles) return;  // past this CTA's last tile
         int m0, env, env_start;
-        tile_geom(tile, m0, env, env_start, c.sb);
+        tile_geom(tile, m0, env, env_start, c.sb, c.nb);
         c.slot = p.env_map ? __ldg(p.env_map + env) : env;
       };
       auto cursor_next = [&](Cursor& c) {
-        if (++c.j == nb) {
+        if (++c.j == c.nb) {
           c.j = 0;
           ++c.it;
           cursor_tile(c);
@@ -830,11 +838,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         cursor_next(cv);
       };
       const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-      const long long total = (long long)my_tiles * nb;
       long long nk = 0, nv = 0;
       int nq = 0;  // Q tiles issued
       // prefix blocks of the first tile before the PDL wait (independent of the previous kernel)
-      while (nk < min(2LL, total) && (int)nk < p.n_prefix_blocks) {
+      while (my_tiles > 0 && nk < 2 && (int)nk < p.n_prefix_blocks) {
         load_k();
         load_v();
         ++nk;
@@ -842,21 +849,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       sm100::pdl_wait();
       const long long t0 = clock64();
-      while (nk < total || nv < total || nq < my_tiles) {
+      while (ck.it < my_tiles || cv.it < my_tiles || nq < my_tiles) {
         // Q of tile nq once every S MMA of tile nq-1 retired
         if (nq < my_tiles && (nq == 0 || sm100::mbar_test(sm100::smem_u32(q_empty), (nq - 1) & 1))) {
-          int m0, env, env_start, sb;
-          tile_geom(blockIdx.x + nq * gridDim.x, m0, env, env_start, sb);
+          int m0, env, env_start, sb, nbt;
+          tile_geom(blockIdx.x + nq * gridDim.x, m0, env, env_start, sb, nbt);
           sm100::mbar_arrive_expect_tx(q_full, kQBytes);
           for (int c = 0; c < 4; ++c)
             sm100::tma_load_2d(&tm_q, q_full, sQ + c * (BQ * 128), c * 64, m0 * kHeads, pol);
           ++nq;
         }
-        if (nk < total && (nk < kPersistKSlots || sm100::mbar_test(sm100::smem_u32(&k_empty[k_s]), k_ph ^ 1))) {
+        if (ck.it < my_tiles && (nk < kPersistKSlots || sm100::mbar_test(sm100::smem_u32(&k_empty[k_s]), k_ph ^ 1))) {
           load_k();
           ++nk;
         }
-        if (nv < total && nv < nk &&
+        if (cv.it < my_tiles && nv < nk &&
             (nv < kPersistVSlots || sm100::mbar_test(sm100::smem_u32(&v_empty[v_s]), v_ph ^ 1))) {
           load_v();
           ++nv;
@@ -900,6 +907,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             vph ^= 1;
           }
         };
+        int m0, env, env_start, sb, nb;
+        tile_geom(tile, m0, env, env_start, sb, nb);
         for (int i = 0; i < nb; ++i, ++g) {
           const int s = (int)(g & 1);
           sm100::mbar_wait(&k_full[ks], kph);
@@ -934,8 +943,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 64) sm100::pdl_launch_dependents();
     long long g = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      int m0, env, env_start, sb;
-      tile_geom(tile, m0, env, env_start, sb);
+      int m0, env, env_start, sb, nb;
+      tile_geom(tile, m0, env, env_start, sb, nb);
       const int tok = m0 + (r >> 3);
       const int head = r & 7;
       const int local_q = tok - env_start;
