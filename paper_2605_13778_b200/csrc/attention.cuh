@@ -1110,23 +1110,31 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ------------------------------------------------ batched: 2-SM CTA pairs
 //
-// attn_pair_kernel: two consecutive query tiles of one env run on a CTA pair
-// (cluster of 2) with tcgen05.mma.cta_group::2: S = Q K^T is one 256 x 64
-// MMA per key block and O += P V one 256 x 256 MMA, each CTA holding its own
-// 128 query rows (Q, P, S and O in its TMEM) but only HALF of every key block
-// (32 keys of K, 128 dims of V^T): 32 KB per block per SM instead of 64 KB,
-// so the same SMEM holds a 4-deep K/V ring. The K/V stream (L2 -> SMEM,
-// ~93 GB/s per SM) and its latency, not the tensor pipe, bound the 1-SM
-// kernel. The leader (rank 0) issues every MMA; its barriers count both
-// CTAs' TMA bytes and both CTAs' softmax arrivals; commits are multicast.
-// Splits == 1 only (batched rounds). Tiles pair up inside an env; an odd last
-// tile is paired with a dummy partner whose rows are computed and dropped.
+// attn_pair_kernel (persistent, one KV split, batched rounds): the two CTAs
+// of a cluster run two consecutive query tiles of one env ("pair tile", 32
+// tokens x 8 heads) with tcgen05.mma.cta_group::2: S = Q K^T is one 256 x 64
+// MMA per key block and O += P V one 256 x 256 MMA. Each CTA keeps its own
+// 128 query rows (Q in SMEM; S, P and O in its TMEM) but loads only HALF of
+// every key block (32 keys of K, 128 dims of V^T): 32 KB per block per SM
+// instead of 64 KB, which halves the L2 -> SMEM stream (~93 GB/s per SM) that
+// bounds the 1-SM kernel, and doubles the ring depth in blocks. The leader
+// (rank 0) issues every MMA; its full-barriers count both CTAs' TMA bytes
+// (.cta_group::2 loads signal the leader) and its s_free / p_full / o_free
+// barriers one arrival per softmax warp of both CTAs (one elected lane after
+// __syncwarp); MMA commits are multicast to both.
+// Pair tiles are walked persistently (cluster c: c, c + clusters, ...), every
+// barrier phase continuing across pair tiles as in attn_persistent_kernel.
+// Tiles pair up inside an env; an odd last tile gets a dummy partner whose
+// rows are computed and dropped.
 
-constexpr int kPairStages = 4;
-constexpr uint32_t kPairKBytes = 32 * HD * 2;     // 16 KB: 32 keys x 256 dims (4 chunks of 32 x 64)
+constexpr int kPairKSlots = 4;
+constexpr int kPairVSlots = 6;
+constexpr uint32_t kPairKBytes = 32 * HD * 2;          // 16 KB: 32 keys x 256 dims (4 chunks of 32 x 64)
 constexpr uint32_t kPairVBytes = (HD / 2) * BKEY * 2;  // 16 KB: 128 dims x 64 keys
-constexpr uint32_t kPairStageBytes = kPairKBytes + kPairVBytes;
-constexpr uint32_t kPairSmemBytes = kQBytes + kPairStages * kPairStageBytes + kPBytes + kCtlBytes + 1024;
+constexpr uint32_t kPairSmemUsed =
+    kQBytes + kPairKSlots * kPairKBytes + kPairVSlots * kPairVBytes + 256 + 2 * 2 * BQ * 4;
+constexpr uint32_t kPairSmemBytes = 227 * 1024;
+static_assert(kPairSmemUsed <= kPairSmemBytes, "pair attention SMEM");
 
 __device__ __forceinline__ uint32_t pair_rank() {
   uint32_t r;
@@ -1162,6 +1170,15 @@ __device__ __forceinline__ void pair_mma(uint32_t tmem_d, uint64_t adesc, uint64
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// A from each CTA's own TMEM (its 128 rows), B halves from the two SMEMs.
+__device__ __forceinline__ void pair_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void pair_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -1169,8 +1186,12 @@ __device__ __forceinline__ void pair_commit(uint64_t* bar) {
       "h"((uint16_t)3)
       : "memory");
 }
+// Remote (or local, via mapa) arrive with the default .release.cta semantics
+// (the CUTLASS cluster-barrier form): the data it publishes lives in TMEM and
+// is ordered by tcgen05 fences; a .release.cluster arrive would emit a
+// GPU-scope MEMBAR per call.
 __device__ __forceinline__ void pair_arrive(uint32_t bar_cluster) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -1181,18 +1202,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sKV = smem + kQBytes;  // kPairStages x [K half 16 KB | V^T half 16 KB]
-  uint8_t* sP = sKV + kPairStages * kPairStageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kPBytes);
-  uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;    // [4]
-  uint64_t* kv_empty = bars + 5;   // [4]
-  uint64_t* s_full = bars + 9;     // [2]
-  uint64_t* s_free = bars + 11;    // [2]
-  uint64_t* p_full = bars + 13;    // [2]
-  uint64_t* pv_done = bars + 15;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
-  float* xm = reinterpret_cast<float*>(bars + 32);  // softmax pair exchange [2][2][128]
+  uint8_t* sK = smem + kQBytes;                    // kPairKSlots x 16 KB
+  uint8_t* sV = sK + kPairKSlots * kPairKBytes;    // kPairVSlots x 16 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kPairVSlots * kPairVBytes);
+  uint64_t* q_full = bars + 0;    // leader: both Q tiles landed
+  uint64_t* k_full = bars + 1;    // [4] leader: both K halves landed
+  uint64_t* k_empty = bars + 5;   // [4] both: S of the block retired
+  uint64_t* s_full = bars + 9;    // [2] both
+  uint64_t* s_free = bars + 11;   // [2] leader: both CTAs read S
+  uint64_t* p_full = bars + 13;   // [2] leader: both CTAs wrote P
+  uint64_t* pv_done = bars + 15;  // [2] both
+  uint64_t* v_full = bars + 17;   // [6] leader: both V^T halves landed
+  uint64_t* v_empty = bars + 23;  // [6] both: PV of the block retired
+  uint64_t* q_empty = bars + 29;  // both: every S of the pair tile retired
+  uint64_t* o_free = bars + 30;   // leader: both CTAs drained O
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 31);
+  float* xm = reinterpret_cast<float*>(bars + 32);  // [2 slots][2 half][128]
+  if (threadIdx.x == 0 && smem + kPairSmemUsed > smem_raw + kPairSmemBytes) __trap();
   cg::cluster_group cluster = cg::this_cluster();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1200,29 +1226,45 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool leader = rank == 0;
   const int tiles_env = p.env_rows / 16;
   const int pairs_env = (tiles_env + 1) / 2;
-  const int pr = blockIdx.x >> 1;
-  const int env = pr / pairs_env, jp = pr - env * pairs_env;
-  const int tloc = 2 * jp + (int)rank;  // tile inside the env
-  const bool valid = tloc < tiles_env;
-  const int env_start = env * p.env_rows;
-  const int m0 = env_start + tloc * 16;  // first token of this CTA's tile (dummy: next env)
-  // shared key blocks: suffix blocks cover the segments of the pair's 32 tokens
-  const int pair_m0 = env_start + 2 * jp * 16;
-  const int seg_first = (pair_m0 - env_start) / p.seg_len;
-  const int sb = (env_start + seg_first * p.seg_len) & ~(BKEY - 1);
-  const int nb = p.n_blocks;
+  const int n_pairs = (p.M / p.env_rows) * pairs_env;
+  const int cl = blockIdx.x >> 1, n_cl = gridDim.x >> 1;
+  const int my_pairs = cl < n_pairs ? (n_pairs - 1 - cl) / n_cl + 1 : 0;
+  // pair tile -> env, this CTA's first token, validity, first suffix key block
+  // and key-block count (prefix + suffix blocks covering the pair's segments)
+  auto pair_geom = [&](int pt, int& env, int& env_start, int& m0, bool& valid, int& sb, int& nbt) {
+    env = pt / pairs_env;
+    const int jp = pt - env * pairs_env;
+    env_start = env * p.env_rows;
+    const int tloc = 2 * jp + (int)rank;
+    valid = tloc < tiles_env;
+    m0 = env_start + tloc * 16;
+    const int lo = 32 * jp;
+    const int seg_first = lo / p.seg_len;
+    int hi = min(lo + 31, p.segs * p.seg_len - 1);
+    hi = hi < lo ? lo : hi;
+    const int seg_last = hi / p.seg_len;
+    sb = (env_start + seg_first * p.seg_len) & ~(BKEY - 1);
+    const int n_suf = (env_start + (seg_last + 1) * p.seg_len - sb + BKEY - 1) / BKEY;
+    nbt = p.n_prefix_blocks + min(n_suf, p.n_blocks - p.n_prefix_blocks);
+  };
 
   if (warp == 0 && lane == 0) {
     sm100::mbar_init(q_full, 1);
-    for (int s = 0; s < kPairStages; ++s) {
-      sm100::mbar_init(&kv_full[s], 1);
-      sm100::mbar_init(&kv_empty[s], 1);
+    sm100::mbar_init(q_empty, 1);
+    sm100::mbar_init(o_free, 2 * 8);  // one arrival per softmax warp
+    for (int s = 0; s < kPairKSlots; ++s) {
+      sm100::mbar_init(&k_full[s], 1);
+      sm100::mbar_init(&k_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      sm100::mbar_init(&s_full[b], 1);
-      sm100::mbar_init(&s_free[b], 2 * 256);
-      sm100::mbar_init(&p_full[b], 2 * 256);
-      sm100::mbar_init(&pv_done[b], 1);
+    for (int s = 0; s < kPairVSlots; ++s) {
+      sm100::mbar_init(&v_full[s], 1);
+      sm100::mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&s_full[s], 1);
+      sm100::mbar_init(&s_free[s], 2 * 8);
+      sm100::mbar_init(&p_full[s], 2 * 8);
+      sm100::mbar_init(&pv_done[s], 1);
     }
     sm100::fence_barrier_init();
   }
@@ -1244,37 +1286,101 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::tma_prefetch_desc(&tm_ks);
       sm100::tma_prefetch_desc(&tm_vs);
       const uint64_t pol = sm100::policy_evict_last();
-      const int slot = p.env_map ? __ldg(p.env_map + env) : env;  // prefix-KV pool slot
-      auto load_block = [&](int i, bool prefix_only) -> bool {
-        const int j = i;
-        const bool is_prefix = j < p.n_prefix_blocks;
-        if (prefix_only && !is_prefix) return false;
-        const int s = i % kPairStages;
-        uint8_t* st = sKV + s * kPairStageBytes;
-        const uint32_t fb = pair_mapa(sm100::smem_u32(&kv_full[s]), 0);
-        if (leader) sm100::mbar_arrive_expect_tx(&kv_full[s], 2 * kPairStageBytes);
-        if (is_prefix) {
-          for (int c = 0; c < 4; ++c)
-            pair_load_3d(&tm_kp, fb, st + c * (32 * 128), c * 64, j * BKEY + rank * 32, slot, pol);
-          pair_load_3d(&tm_vp, fb, st + kPairKBytes, j * BKEY, rank * (HD / 2), slot, pol);
-        } else {
-          const int row0 = sb + (j - p.n_prefix_blocks) * BKEY;
-          for (int c = 0; c < 4; ++c)
-            pair_load_2d(&tm_ks, fb, st + c * (32 * 128), c * 64, row0 + rank * 32, pol);
-          pair_load_2d(&tm_vs, fb, st + kPairKBytes, row0, rank * (HD / 2), pol);
-        }
-        return true;
+      struct Cursor {
+        int it = 0, j = 0, slot = 0, sb = 0, nb = 0;
       };
-      int issued = 0;
-      while (issued < min(kPairStages, nb) && load_block(issued, true)) ++issued;
-      sm100::pdl_wait();
+      auto cursor_tile = [&](Cursor& c) {
+        if (c.it >= my_pairs) return;
+        int env, env_start, m0, sb, nbt;
+        bool valid;
+        pair_geom(cl + c.it * n_cl, env, env_start, m0, valid, sb, nbt);
+        c.sb = sb;
+        c.nb = nbt;
+        c.slot = p.env_map ? __ldg(p.env_map + env) : env;
+      };
+      auto cursor_next = [&](Cursor& c) {
+        if (++c.j == c.nb) {
+          c.j = 0;
+          ++c.it;
+          cursor_tile(c);
+        }
+      };
+      Cursor ck, cv;
+      cursor_tile(ck);
+      cv = ck;
+      int k_s = 0, v_s = 0;
+      uint32_t k_ph = 0, v_ph = 0;
+      auto load_k = [&]() {
+        const int s = k_s;
+        uint8_t* st = sK + s * kPairKBytes;
+        const uint32_t fb = pair_mapa(sm100::smem_u32(&k_full[s]), 0);
+        if (leader) sm100::mbar_arrive_expect_tx(&k_full[s], 2 * kPairKBytes);
+        if (ck.j < p.n_prefix_blocks) {
+          for (int c = 0; c < 4; ++c)
+            pair_load_3d(&tm_kp, fb, st + c * (32 * 128), c * 64, ck.j * BKEY + (int)rank * 32, ck.slot, pol);
+        } else {
+          const int row0 = ck.sb + (ck.j - p.n_prefix_blocks) * BKEY;
+          for (int c = 0; c < 4; ++c)
+            pair_load_2d(&tm_ks, fb, st + c * (32 * 128), c * 64, row0 + (int)rank * 32, pol);
+        }
+        if (++k_s == kPairKSlots) {
+          k_s = 0;
+          k_ph ^= 1;
+        }
+        cursor_next(ck);
+      };
+      auto load_v = [&]() {
+        const int s = v_s;
+        uint8_t* st = sV + s * kPairVBytes;
+        const uint32_t fb = pair_mapa(sm100::smem_u32(&v_full[s]), 0);
+        if (leader) sm100::mbar_arrive_expect_tx(&v_full[s], 2 * kPairVBytes);
+        if (cv.j < p.n_prefix_blocks) {
+          pair_load_3d(&tm_vp, fb, st, cv.j * BKEY, (int)rank * (HD / 2), cv.slot, pol);
+        } else {
+          const int row0 = cv.sb + (cv.j - p.n_prefix_blocks) * BKEY;
+          pair_load_2d(&tm_vs, fb, st, row0, (int)rank * (HD / 2), pol);
+        }
+        if (++v_s == kPairVSlots) {
+          v_s = 0;
+          v_ph ^= 1;
+        }
+        cursor_next(cv);
+      };
+      long long nk = 0, nv = 0;
+      int nq = 0;
       const uint32_t qb = pair_mapa(sm100::smem_u32(q_full), 0);
-      if (leader) sm100::mbar_arrive_expect_tx(q_full, 2 * kQBytes);
-      for (int c = 0; c < 4; ++c)
-        pair_load_2d(&tm_q, qb, sQ + c * (BQ * 128), c * 64, m0 * kHeads, pol);
-      for (int i = issued; i < nb; ++i) {
-        if (i >= kPairStages) sm100::mbar_wait(&kv_empty[i % kPairStages], ((i / kPairStages) & 1) ^ 1);
-        load_block(i, false);
+      // prefix blocks of the first pair tile before the PDL wait
+      while (my_pairs > 0 && nk < 2 && (int)nk < p.n_prefix_blocks) {
+        load_k();
+        load_v();
+        ++nk;
+        ++nv;
+      }
+      sm100::pdl_wait();
+      const long long t0 = clock64();
+      while (ck.it < my_pairs || cv.it < my_pairs || nq < my_pairs) {
+        if (nq < my_pairs && (nq == 0 || sm100::mbar_test(sm100::smem_u32(q_empty), (nq - 1) & 1))) {
+          int env, env_start, m0, sb, nbt;
+          bool valid;
+          pair_geom(cl + nq * n_cl, env, env_start, m0, valid, sb, nbt);
+          if (leader) sm100::mbar_arrive_expect_tx(q_full, 2 * kQBytes);
+          for (int c = 0; c < 4; ++c) pair_load_2d(&tm_q, qb, sQ + c * (BQ * 128), c * 64, m0 * kHeads, pol);
+          ++nq;
+        }
+        if (ck.it < my_pairs &&
+            (nk < kPairKSlots || sm100::mbar_test(sm100::smem_u32(&k_empty[k_s]), k_ph ^ 1))) {
+          load_k();
+          ++nk;
+        }
+        if (cv.it < my_pairs && nv < nk &&
+            (nv < kPairVSlots || sm100::mbar_test(sm100::smem_u32(&v_empty[v_s]), v_ph ^ 1))) {
+          load_v();
+          ++nv;
+        }
+        if (clock64() - t0 > (1ll << 34)) {
+          printf("sf: pair attention producer timeout (block %d)\n", blockIdx.x);
+          __trap();
+        }
       }
     }
   } else if (warp == 1) {
@@ -1282,191 +1388,225 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc_s = sm100::make_idesc_bf16(256, BKEY);
       const uint32_t idesc_o = sm100::make_idesc_bf16(256, HD);
       const uint32_t q_addr = sm100::smem_u32(sQ);
-      const uint32_t p_addr = sm100::smem_u32(sP);
-      sm100::mbar_wait(q_full, 0);
-      auto issue_pv = [&](int i) {
-        sm100::mbar_wait(&p_full[i & 1], (i >> 1) & 1);
-        sm100::tc_fence_after();
-        const uint32_t v_addr = sm100::smem_u32(sKV + (i % kPairStages) * kPairStageBytes + kPairKBytes);
+      long long g = 0;
+      int ks = 0, vs = 0;
+      uint32_t kph = 0, vph = 0;
+      for (int it = 0; it < my_pairs; ++it) {
+        int env, env_start, m0, sb, nb;
+        bool valid;
+        pair_geom(cl + it * n_cl, env, env_start, m0, valid, sb, nb);
+        const long long g0 = g;
+        sm100::mbar_wait(q_full, it & 1);
+        auto issue_pv = [&](long long gg) {
+          const int i = (int)(gg - g0);
+          if (i == 0 && it > 0) sm100::mbar_wait(o_free, (it - 1) & 1);
+          sm100::mbar_wait(&p_full[gg & 1], (gg >> 1) & 1);
+          sm100::mbar_wait(&v_full[vs], vph);
+          sm100::tc_fence_after();
+          const uint32_t v_addr = sm100::smem_u32(sV + vs * kPairVBytes);
+          const uint32_t p_tmem = tmem + kPCol + (uint32_t)(gg & 1) * (BKEY / 2);
 #pragma unroll
-        for (int kk = 0; kk < BKEY / 16; ++kk)
-          pair_mma(tmem + 128, sm100::make_sw128_desc(p_addr + kk * 32),
-                   sm100::make_sw128_desc(v_addr + kk * 32), idesc_o, (i | kk) != 0);
-        pair_commit(&pv_done[i & 1]);
-        pair_commit(&kv_empty[i % kPairStages]);
-      };
-      for (int i = 0; i < nb; ++i) {
-        const int s = i % kPairStages, b = i & 1;
-        sm100::mbar_wait(&kv_full[s], (i / kPairStages) & 1);
-        if (i >= 2) sm100::mbar_wait(&s_free[b], ((i >> 1) & 1) ^ 1);
-        sm100::tc_fence_after();
-        const uint32_t k_addr = sm100::smem_u32(sKV + s * kPairStageBytes);
+          for (int kk = 0; kk < BKEY / 16; ++kk)
+            pair_mma_ts(tmem + 128, p_tmem + kk * 8, sm100::make_sw128_desc(v_addr + kk * 32), idesc_o,
+                        (i | kk) != 0);
+          pair_commit(&pv_done[gg & 1]);
+          pair_commit(&v_empty[vs]);
+          if (++vs == kPairVSlots) {
+            vs = 0;
+            vph ^= 1;
+          }
+        };
+        for (int i = 0; i < nb; ++i, ++g) {
+          const int s = (int)(g & 1);
+          sm100::mbar_wait(&k_full[ks], kph);
+          if (g >= 2) sm100::mbar_wait(&s_free[s], ((g >> 1) & 1) ^ 1);
+          sm100::tc_fence_after();
+          const uint32_t k_addr = sm100::smem_u32(sK + ks * kPairKBytes);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const int c = kk >> 2, w = kk & 3;
-          pair_mma(tmem + b * BKEY, sm100::make_sw128_desc(q_addr + c * (BQ * 128) + w * 32),
-                   sm100::make_sw128_desc(k_addr + c * (32 * 128) + w * 32), idesc_s, kk != 0);
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const int c = kk >> 2, w = kk & 3;
+            pair_mma(tmem + s * BKEY, sm100::make_sw128_desc(q_addr + c * (BQ * 128) + w * 32),
+                     sm100::make_sw128_desc(k_addr + c * (32 * 128) + w * 32), idesc_s, kk != 0);
+          }
+          pair_commit(&s_full[s]);
+          pair_commit(&k_empty[ks]);
+          if (++ks == kPairKSlots) {
+            ks = 0;
+            kph ^= 1;
+          }
+          if (i == nb - 1) pair_commit(q_empty);
+          if (i >= 1) issue_pv(g - 1);
         }
-        pair_commit(&s_full[b]);
-        if (i >= 1) issue_pv(i - 1);
+        if (nb > 0) issue_pv(g - 1);
       }
-      if (nb > 0) issue_pv(nb - 1);
     }
     __syncwarp();
   } else {
-    // softmax (as attn_kernel: 2 warps per TMEM lane quarter, column halves)
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const int r = q * 32 + lane;
     const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
-    const int tok = m0 + (r >> 3);
-    const int head = r & 7;
-    const int local_q = tok - env_start;
-    const int seg_q = local_q / p.seg_len;
-    const int t_q = local_q - seg_q * p.seg_len;
-    const bool real_q = valid && local_q < p.segs * p.seg_len && tok < p.M;
-    const int seg_lo = seg_q * p.seg_len;
-    const int seg_hi = seg_lo + (t_q >= 1 ? p.seg_len : 1);
     const uint32_t sfree_l = pair_mapa(sm100::smem_u32(s_free), 0);
     const uint32_t pfull_l = pair_mapa(sm100::smem_u32(p_full), 0);
-    float m_used = -INFINITY, l_sum = 0.f;
+    const uint32_t ofree_l = pair_mapa(sm100::smem_u32(o_free), 0);
     sm100::pdl_wait();
     if (threadIdx.x == 64) sm100::pdl_launch_dependents();
-    for (int i = 0; i < nb; ++i) {
-      const int j = i;
-      const int b = i & 1;
-      sm100::mbar_wait(&s_full[b], (i >> 1) & 1);
-      sm100::tc_fence_after();
-      uint32_t raw[2][16];
+    long long g = 0;
+    for (int it = 0; it < my_pairs; ++it) {
+      int env, env_start, m0, sb, nb;
+      bool valid;
+      pair_geom(cl + it * n_cl, env, env_start, m0, valid, sb, nb);
+      const int tok = m0 + (r >> 3);
+      const int head = r & 7;
+      const int local_q = tok - env_start;
+      const int seg_q = local_q / p.seg_len;
+      const int t_q = local_q - seg_q * p.seg_len;
+      const bool real_q = valid && local_q < p.segs * p.seg_len && tok < p.M;
+      const int seg_lo = seg_q * p.seg_len;
+      const int seg_hi = seg_lo + (t_q >= 1 ? p.seg_len : 1);
+      float m_used = -INFINITY, l_sum = 0.f;
+      for (int i = 0; i < nb; ++i, ++g) {
+        const int j = i;
+        const int s = (int)(g & 1);
+        sm100::mbar_wait(&s_full[s], (g >> 1) & 1);
+        sm100::tc_fence_after();
+        uint32_t raw[2][16];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) sm100::tmem_ld16(t_lane + b * BKEY + half * 32 + c * 16, raw[c]);
-      sm100::tmem_ld_wait();
-      sm100::tc_fence_before();
-      pair_arrive(sfree_l + b * 8);
-      int lo = 0, hi;
-      if (j < p.n_prefix_blocks) {
-        hi = p.prefix_len - j * BKEY;
-      } else if (real_q) {
-        const int base = sb + (j - p.n_prefix_blocks) * BKEY - env_start;
-        lo = seg_lo - base;
-        hi = seg_hi - base;
-      } else {
-        hi = 0;
-      }
-      lo -= half * 32;
-      hi -= half * 32;
-      float sv[32];
-      float mb;
-      if (lo <= 0 && hi >= 32) {  // fully visible half-block (every prefix block but the last)
-#pragma unroll
-        for (int c = 0; c < 32; ++c) sv[c] = __uint_as_float(raw[c >> 4][c & 15]);
-      } else {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const float x = __uint_as_float(raw[c >> 4][c & 15]);
-          sv[c] = (c >= lo && c < hi) ? x : -INFINITY;
+        for (int c = 0; c < 2; ++c) sm100::tmem_ld16(t_lane + s * BKEY + half * 32 + c * 16, raw[c]);
+        sm100::tmem_ld_wait();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) pair_arrive(sfree_l + s * 8);
+        int lo = 0, hi;
+        if (j < p.n_prefix_blocks) {
+          hi = p.prefix_len - j * BKEY;
+        } else if (real_q) {
+          const int base = sb + (j - p.n_prefix_blocks) * BKEY - env_start;
+          lo = seg_lo - base;
+          hi = seg_hi - base;
+        } else {
+          hi = 0;
         }
-      }
-      {  // 3-input max tree
-        float t[11];
+        lo -= half * 32;
+        hi -= half * 32;
+        float sv[32];
+        float mb;
+        if (lo <= 0 && hi >= 32) {
 #pragma unroll
-        for (int c = 0; c < 10; ++c) t[c] = fmax3(sv[3 * c], sv[3 * c + 1], sv[3 * c + 2]);
-        t[10] = fmaxf(sv[30], sv[31]);
-        const float u0 = fmax3(t[0], t[1], t[2]), u1 = fmax3(t[3], t[4], t[5]);
-        const float u2 = fmax3(t[6], t[7], t[8]), u3 = fmaxf(t[9], t[10]);
-        mb = fmaxf(fmax3(u0, u1, u2), u3);
-      }
-      xm[(b * 2 + half) * BQ + r] = mb;
-      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
-      mb = fmaxf(xm[(b * 2) * BQ + r], xm[(b * 2 + 1) * BQ + r]) * p.scale_log2;
-      const float m_new = fmaxf(m_used, mb);
-      bool rescale = false;
-      float alpha = 1.f;
-      if (m_new > -INFINITY) {
-        if (m_used == -INFINITY) {
-          m_used = m_new;
-        } else if (m_new > m_used + 8.f) {
-          alpha = exp2f(m_used - m_new);
-          m_used = m_new;
-          rescale = true;
+          for (int c = 0; c < 32; ++c) sv[c] = __uint_as_float(raw[c >> 4][c & 15]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const float x = __uint_as_float(raw[c >> 4][c & 15]);
+            sv[c] = (c >= lo && c < hi) ? x : -INFINITY;
+          }
         }
-      }
-      // exponentials first (registers): only the P store and an O rescale
-      // have to wait for PV(i-1), so the MUFU work overlaps it
-      const float mu = m_used == -INFINITY ? 0.f : m_used;
-      uint32_t pw[16];
-      float lp = 0.f;
+        {
+          float t[11];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const float p0 = ex2_approx(fmaf(sv[2 * k], p.scale_log2, -mu));
-        const float p1 = ex2_approx(fmaf(sv[2 * k + 1], p.scale_log2, -mu));
-        lp += p0 + p1;
-        __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-        pw[k] = *reinterpret_cast<uint32_t*>(&b2);
+          for (int c = 0; c < 10; ++c) t[c] = fmax3(sv[3 * c], sv[3 * c + 1], sv[3 * c + 2]);
+          t[10] = fmaxf(sv[30], sv[31]);
+          const float u0 = fmax3(t[0], t[1], t[2]), u1 = fmax3(t[3], t[4], t[5]);
+          const float u2 = fmax3(t[6], t[7], t[8]), u3 = fmaxf(t[9], t[10]);
+          mb = fmaxf(fmax3(u0, u1, u2), u3);
+        }
+        xm[(s * 2 + half) * BQ + r] = mb;
+        asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+        mb = fmaxf(xm[(s * 2) * BQ + r], xm[(s * 2 + 1) * BQ + r]) * p.scale_log2;
+        const float m_new = fmaxf(m_used, mb);
+        bool rescale = false;
+        float alpha = 1.f;
+        if (m_new > -INFINITY) {
+          if (m_used == -INFINITY) {
+            m_used = m_new;
+          } else if (m_new > m_used + 8.f) {
+            alpha = exp2f(m_used - m_new);
+            m_used = m_new;
+            rescale = true;
+          }
+        }
+        const float mu = m_used == -INFINITY ? 0.f : m_used;
+        uint32_t pw[16];
+        float lp = 0.f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float p0 = ex2_approx(fmaf(sv[2 * k], p.scale_log2, -mu));
+          const float p1 = ex2_approx(fmaf(sv[2 * k + 1], p.scale_log2, -mu));
+          lp += p0 + p1;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+          pw[k] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        // P slot s is free once PV(g-2) retired; PV(g-1) may still run
+        // unless O has to be rescaled
+        if (g >= 2) {
+          sm100::mbar_wait(&pv_done[s], ((g - 2) >> 1) & 1);
+          sm100::tc_fence_after();
+        }
+        const bool any_rescale = __any_sync(0xffffffffu, rescale);
+        if (any_rescale && i >= 1) {
+          sm100::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+          sm100::tc_fence_after();
+          l_sum *= alpha;
+#pragma unroll 1
+          for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 16) {
+            uint32_t o[16];
+            sm100::tmem_ld16(t_lane + 128 + c0, o);
+            sm100::tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 16; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+            sm100::tmem_st16(t_lane + 128 + c0, o);
+          }
+          sm100::tmem_st_wait();
+        } else if (rescale) {
+          l_sum *= alpha;
+        }
+        l_sum += lp;
+        sm100::tmem_st16(t_lane + kPCol + s * (BKEY / 2) + half * 16, pw);
+        sm100::tmem_st_wait();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) pair_arrive(pfull_l + s * 8);
       }
-      if (i >= 1) {
-        sm100::mbar_wait(&pv_done[(i - 1) & 1], ((i - 1) >> 1) & 1);
+      if (nb > 0) {
+        sm100::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
         sm100::tc_fence_after();
       }
-      const bool any_rescale = __any_sync(0xffffffffu, rescale);
-      if (any_rescale && i >= 1) {
-        l_sum *= alpha;
-#pragma unroll 1
-        for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 16) {
-          uint32_t o[16];
-          sm100::tmem_ld16(t_lane + 128 + c0, o);
-          sm100::tmem_ld_wait();
-#pragma unroll
-          for (int k = 0; k < 16; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
-          sm100::tmem_st16(t_lane + 128 + c0, o);
-        }
-        sm100::tmem_st_wait();
-      } else if (rescale) {
-        l_sum *= alpha;
-      }
-      uint8_t* prow = sP + r * 128;
-      l_sum += lp;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int cc = half * 4 + c;
-        *reinterpret_cast<uint4*>(prow + ((cc ^ (r & 7)) << 4)) =
-            make_uint4(pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
-      }
-      fence_async_smem();
-      sm100::tc_fence_before();
-      pair_arrive(pfull_l + b * 8);
-    }
-    if (nb > 0) {
-      sm100::mbar_wait(&pv_done[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
-      sm100::tc_fence_after();
-    }
-    {
-      const int ps = nb & 1;
-      xm[(ps * 2 + half) * BQ + r] = l_sum;
+      const int ls = (int)(g & 1);
+      xm[(ls * 2 + half) * BQ + r] = l_sum;
       asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
-      l_sum = xm[(ps * 2) * BQ + r] + xm[(ps * 2 + 1) * BQ + r];
-    }
-    const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
-    __nv_bfloat16* dst = p.out + (size_t)tok * (kHeads * HD) + head * HD;
-    for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 32) {
-      uint32_t o[2][16];
-      sm100::tmem_ld16(t_lane + 128 + c0, o[0]);
-      sm100::tmem_ld16(t_lane + 128 + c0 + 16, o[1]);
-      sm100::tmem_ld_wait();
+      l_sum = xm[(ls * 2) * BQ + r] + xm[(ls * 2 + 1) * BQ + r];
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+      const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
+      uint32_t ow[4][2][8];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        uint32_t w[8];
+      for (int u4 = 0; u4 < 4; ++u4) {
+        uint32_t o[2][16];
+        const int c0 = half * 128 + u4 * 32;
+        sm100::tmem_ld16(t_lane + 128 + c0, o[0]);
+        sm100::tmem_ld16(t_lane + 128 + c0 + 16, o[1]);
+        sm100::tmem_ld_wait();
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[u][2 * k]) * inv,
-                                                    __uint_as_float(o[u][2 * k + 1]) * inv);
-          w[k] = *reinterpret_cast<uint32_t*>(&b2);
-        }
-        if (valid && tok < p.M) {
-          uint4* d4 = reinterpret_cast<uint4*>(dst + c0 + 16 * u);
-          d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
-          d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
-        }
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[u][2 * k]) * inv,
+                                                      __uint_as_float(o[u][2 * k + 1]) * inv);
+            ow[u4][u][k] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) pair_arrive(ofree_l);
+      if (valid && tok < p.M) {
+        __nv_bfloat16* dst = p.out + (size_t)tok * (kHeads * HD) + head * HD + half * 128;
+#pragma unroll
+        for (int u4 = 0; u4 < 4; ++u4)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst + u4 * 32 + 16 * u);
+            d4[0] = make_uint4(ow[u4][u][0], ow[u4][u][1], ow[u4][u][2], ow[u4][u][3]);
+            d4[1] = make_uint4(ow[u4][u][4], ow[u4][u][5], ow[u4][u][6], ow[u4][u][7]);
+          }
       }
     }
   }

@@ -1081,11 +1081,17 @@ int launch_attn_pair(const Buffers& b, int l, cudaStream_t s, bool pdl) {
                                        (int)attn::kPairSmemBytes));
     attr = true;
   }
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
   const CUtensorMap* mp = &b.attn_pair_maps[5 * l];
   const int tiles_env = b.env_rows / 16;
   const int pairs = b.B * ((tiles_env + 1) / 2);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * pairs);
+  cfg.gridDim = dim3(2 * (pairs < nsm / 2 ? pairs : nsm / 2));  // persistent: one CTA pair per 2 SMs
   cfg.blockDim = dim3(attn::kThreads);
   cfg.dynamicSmemBytes = attn::kPairSmemBytes;
   cfg.stream = s;
