@@ -94,24 +94,6 @@ struct Params {
   } while (0)
 #endif
 
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, int rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void st_async_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
-                                            uint32_t d, uint32_t bar) {
-  asm volatile(
-      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
-      "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uint32_t bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr),
-               "f"(a), "f"(b), "r"(bar)
-               : "memory");
-}
-
 // MUFU ex2 (flush-to-zero; ex2(-inf) = +0 for masked keys)
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
