@@ -1094,29 +1094,33 @@ __global__ void __launch_bounds__(kThreads, 1)
 //
 // attn_pair_kernel (persistent, one KV split, batched rounds): the two CTAs
 // of a cluster run two consecutive query tiles of one env ("pair tile", 32
-// tokens x 8 heads) with tcgen05.mma.cta_group::2: S = Q K^T is one 256 x 64
-// MMA per key block and O += P V one 256 x 256 MMA. Each CTA keeps its own
-// 128 query rows (Q in SMEM; S, P and O in its TMEM) but loads only HALF of
-// every key block (32 keys of K, 128 dims of V^T): 32 KB per block per SM
-// instead of 64 KB, which halves the L2 -> SMEM stream (~93 GB/s per SM) that
-// bounds the 1-SM kernel, and doubles the ring depth in blocks. The leader
-// (rank 0) issues every MMA; its full-barriers count both CTAs' TMA bytes
-// (.cta_group::2 loads signal the leader) and its s_free / p_full / o_free
-// barriers one arrival per softmax warp of both CTAs (one elected lane after
-// __syncwarp); MMA commits are multicast to both.
-// Pair tiles are walked persistently (cluster c: c, c + clusters, ...), every
-// barrier phase continuing across pair tiles as in attn_persistent_kernel.
-// Tiles pair up inside an env; an odd last tile gets a dummy partner whose
-// rows are computed and dropped.
+// tokens x 8 heads = 256 query rows) with tcgen05.mma.cta_group::2 over
+// 128-key superblocks (two 64-key blocks; CTA r loads block 2G + r):
+//   S(G) = Q K^T   one 256 x 128 MMA group (N = 128 halves the number of S
+//                  MMAs per key, the costliest part of the 1-SM kernel);
+//                  each CTA holds its 128 query rows of S in TMEM;
+//   P(G)           written by the softmax (bf16) over the first 64 columns of
+//                  S(G)'s TMEM slot;
+//   O += P V       one 256 x 256 MMA group with A = P from each CTA's TMEM and
+//                  V^T split by dims (CTA r holds dims [128 r, 128 r + 128)).
+// Per superblock each SM loads 32 KB of K and 32 KB of V^T (the 1-SM kernel
+// loads 64 KB per 64 keys). S(G+2) reuses P(G)'s slot: it is issued after
+// PV(G) and tcgen05 MMAs of one issuer execute in order. The leader (rank 0)
+// issues every MMA; its full-barriers count both CTAs' TMA bytes
+// (.cta_group::2 loads signal the leader), its p_full / o_free barriers one
+// arrival per softmax warp of both CTAs; MMA commits are multicast. Pair
+// tiles are walked persistently with barrier phases continuing across them;
+// an odd last tile of an env gets a dummy partner whose rows are dropped.
 
-constexpr int kPairKSlots = 4;
-constexpr int kPairVSlots = 6;
-constexpr uint32_t kPairKBytes = 32 * HD * 2;          // 16 KB: 32 keys x 256 dims (4 chunks of 32 x 64)
-constexpr uint32_t kPairVBytes = (HD / 2) * BKEY * 2;  // 16 KB: 128 dims x 64 keys
+constexpr int kPairKSlots = 2;
+constexpr int kPairVSlots = 3;
+constexpr uint32_t kPairKBytes = BKEY * HD * 2;        // 32 KB: this CTA's 64-key block (4 chunks of 64 x 64)
+constexpr uint32_t kPairVBytes = (HD / 2) * 128 * 2;   // 32 KB: 128 dims x 128 keys (2 chunks of 128 x 64)
 constexpr uint32_t kPairSmemUsed =
     kQBytes + kPairKSlots * kPairKBytes + kPairVSlots * kPairVBytes + 256 + 2 * 2 * BQ * 4;
 constexpr uint32_t kPairSmemBytes = 227 * 1024;
 static_assert(kPairSmemUsed <= kPairSmemBytes, "pair attention SMEM");
+constexpr uint32_t kPairOCol = 256;  // TMEM: S/P slots [0,128) [128,256), O [256,512)
 
 __device__ __forceinline__ uint32_t pair_rank() {
   uint32_t r;
@@ -1184,21 +1188,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = smem + kQBytes;                    // kPairKSlots x 16 KB
-  uint8_t* sV = sK + kPairKSlots * kPairKBytes;    // kPairVSlots x 16 KB
+  uint8_t* sK = smem + kQBytes;                  // kPairKSlots x 32 KB
+  uint8_t* sV = sK + kPairKSlots * kPairKBytes;  // kPairVSlots x 32 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kPairVSlots * kPairVBytes);
   uint64_t* q_full = bars + 0;    // leader: both Q tiles landed
-  uint64_t* k_full = bars + 1;    // [4] leader: both K halves landed
-  uint64_t* k_empty = bars + 5;   // [4] both: S of the block retired
-  uint64_t* s_full = bars + 9;    // [2] both
-  uint64_t* s_free = bars + 11;   // [2] leader: both CTAs read S
-  uint64_t* p_full = bars + 13;   // [2] leader: both CTAs wrote P
-  uint64_t* pv_done = bars + 15;  // [2] both
-  uint64_t* v_full = bars + 17;   // [6] leader: both V^T halves landed
-  uint64_t* v_empty = bars + 23;  // [6] both: PV of the block retired
-  uint64_t* q_empty = bars + 29;  // both: every S of the pair tile retired
-  uint64_t* o_free = bars + 30;   // leader: both CTAs drained O
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 31);
+  uint64_t* k_full = bars + 1;    // [2] leader: both K blocks landed
+  uint64_t* k_empty = bars + 3;   // [2] both: S of the superblock retired
+  uint64_t* s_full = bars + 5;    // [2] both
+  uint64_t* p_full = bars + 7;    // [2] leader: both CTAs wrote P
+  uint64_t* pv_done = bars + 9;   // [2] both
+  uint64_t* v_full = bars + 11;   // [3] leader: both V^T halves landed
+  uint64_t* v_empty = bars + 14;  // [3] both: PV of the superblock retired
+  uint64_t* q_empty = bars + 17;  // both: every S of the pair tile retired
+  uint64_t* o_free = bars + 18;   // leader: both CTAs drained O
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
   float* xm = reinterpret_cast<float*>(bars + 32);  // [2 slots][2 half][128]
   if (threadIdx.x == 0 && smem + kPairSmemUsed > smem_raw + kPairSmemBytes) __trap();
   cg::cluster_group cluster = cg::this_cluster();
@@ -1244,7 +1247,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&s_full[s], 1);
-      sm100::mbar_init(&s_free[s], 2 * 8);
       sm100::mbar_init(&p_full[s], 2 * 8);
       sm100::mbar_init(&pv_done[s], 1);
     }
@@ -1268,21 +1270,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::tma_prefetch_desc(&tm_ks);
       sm100::tma_prefetch_desc(&tm_vs);
       const uint64_t pol = sm100::policy_evict_last();
+      // superblock cursors (pair tile it, superblock G) for the next K and V loads
       struct Cursor {
-        int it = 0, j = 0, slot = 0, sb = 0, nb = 0;
+        int it = 0, G = 0, slot = 0, sb = 0, nb = 0;
       };
       auto cursor_tile = [&](Cursor& c) {
         if (c.it >= my_pairs) return;
-        int env, env_start, m0, sb, nbt;
+        int env, env_start, m0;
         bool valid;
-        pair_geom(cl + c.it * n_cl, env, env_start, m0, valid, sb, nbt);
-        c.sb = sb;
-        c.nb = nbt;
+        pair_geom(cl + c.it * n_cl, env, env_start, m0, valid, c.sb, c.nb);
         c.slot = p.env_map ? __ldg(p.env_map + env) : env;
       };
       auto cursor_next = [&](Cursor& c) {
-        if (++c.j == c.nb) {
-          c.j = 0;
+        if (++c.G == (c.nb + 1) / 2) {
+          c.G = 0;
           ++c.it;
           cursor_tile(c);
         }
@@ -1292,18 +1293,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       cv = ck;
       int k_s = 0, v_s = 0;
       uint32_t k_ph = 0, v_ph = 0;
+      // a block past the tile's last one (odd count) re-reads prefix block 0:
+      // finite data, fully masked by the softmax
       auto load_k = [&]() {
         const int s = k_s;
         uint8_t* st = sK + s * kPairKBytes;
         const uint32_t fb = pair_mapa(sm100::smem_u32(&k_full[s]), 0);
         if (leader) sm100::mbar_arrive_expect_tx(&k_full[s], 2 * kPairKBytes);
-        if (ck.j < p.n_prefix_blocks) {
+        int j = 2 * ck.G + (int)rank;
+        j = j < ck.nb ? j : 0;
+        if (j < p.n_prefix_blocks) {
           for (int c = 0; c < 4; ++c)
-            pair_load_3d(&tm_kp, fb, st + c * (32 * 128), c * 64, ck.j * BKEY + (int)rank * 32, ck.slot, pol);
+            pair_load_3d(&tm_kp, fb, st + c * (BKEY * 128), c * 64, j * BKEY, ck.slot, pol);
         } else {
-          const int row0 = ck.sb + (ck.j - p.n_prefix_blocks) * BKEY;
-          for (int c = 0; c < 4; ++c)
-            pair_load_2d(&tm_ks, fb, st + c * (32 * 128), c * 64, row0 + (int)rank * 32, pol);
+          const int row0 = ck.sb + (j - p.n_prefix_blocks) * BKEY;
+          for (int c = 0; c < 4; ++c) pair_load_2d(&tm_ks, fb, st + c * (BKEY * 128), c * 64, row0, pol);
         }
         if (++k_s == kPairKSlots) {
           k_s = 0;
@@ -1316,11 +1320,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* st = sV + s * kPairVBytes;
         const uint32_t fb = pair_mapa(sm100::smem_u32(&v_full[s]), 0);
         if (leader) sm100::mbar_arrive_expect_tx(&v_full[s], 2 * kPairVBytes);
-        if (cv.j < p.n_prefix_blocks) {
-          pair_load_3d(&tm_vp, fb, st, cv.j * BKEY, (int)rank * (HD / 2), cv.slot, pol);
-        } else {
-          const int row0 = cv.sb + (cv.j - p.n_prefix_blocks) * BKEY;
-          pair_load_2d(&tm_vs, fb, st, row0, (int)rank * (HD / 2), pol);
+        for (int h = 0; h < 2; ++h) {  // chunk h: keys of block 2G + h, this CTA's 128 dims
+          int j = 2 * cv.G + h;
+          j = j < cv.nb ? j : 0;
+          uint8_t* dst = st + h * (kPairVBytes / 2);
+          if (j < p.n_prefix_blocks) {
+            pair_load_3d(&tm_vp, fb, dst, j * BKEY, (int)rank * (HD / 2), cv.slot, pol);
+          } else {
+            const int row0 = cv.sb + (j - p.n_prefix_blocks) * BKEY;
+            pair_load_2d(&tm_vs, fb, dst, row0, (int)rank * (HD / 2), pol);
+          }
         }
         if (++v_s == kPairVSlots) {
           v_s = 0;
@@ -1331,8 +1340,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       long long nk = 0, nv = 0;
       int nq = 0;
       const uint32_t qb = pair_mapa(sm100::smem_u32(q_full), 0);
-      // prefix blocks of the first pair tile before the PDL wait
-      while (my_pairs > 0 && nk < 2 && (int)nk < p.n_prefix_blocks) {
+      // prefix superblock 0 of the first pair tile before the PDL wait
+      if (my_pairs > 0 && 2 <= p.n_prefix_blocks) {
         load_k();
         load_v();
         ++nk;
@@ -1367,16 +1376,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (leader && sm100::elect_one()) {
-      const uint32_t idesc_s = sm100::make_idesc_bf16(256, BKEY);
+      const uint32_t idesc_s = sm100::make_idesc_bf16(256, 2 * BKEY);
       const uint32_t idesc_o = sm100::make_idesc_bf16(256, HD);
       const uint32_t q_addr = sm100::smem_u32(sQ);
-      long long g = 0;
+      long long g = 0;  // global superblock counter
       int ks = 0, vs = 0;
       uint32_t kph = 0, vph = 0;
       for (int it = 0; it < my_pairs; ++it) {
-        int env, env_start, m0, sb, nb;
+        int env, env_start, m0, sb, nbt;
         bool valid;
-        pair_geom(cl + it * n_cl, env, env_start, m0, valid, sb, nb);
+        pair_geom(cl + it * n_cl, env, env_start, m0, valid, sb, nbt);
+        const int nsb = (nbt + 1) / 2;
         const long long g0 = g;
         sm100::mbar_wait(q_full, it & 1);
         auto issue_pv = [&](long long gg) {
@@ -1386,10 +1396,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::mbar_wait(&v_full[vs], vph);
           sm100::tc_fence_after();
           const uint32_t v_addr = sm100::smem_u32(sV + vs * kPairVBytes);
-          const uint32_t p_tmem = tmem + kPCol + (uint32_t)(gg & 1) * (BKEY / 2);
+          const uint32_t p_tmem = tmem + (uint32_t)(gg & 1) * (2 * BKEY);
 #pragma unroll
-          for (int kk = 0; kk < BKEY / 16; ++kk)
-            pair_mma_ts(tmem + 128, p_tmem + kk * 8, sm100::make_sw128_desc(v_addr + kk * 32), idesc_o,
+          for (int kk = 0; kk < 2 * BKEY / 16; ++kk)  // 16 keys per MMA: 8 P columns, V^T chunk kk / 4
+            pair_mma_ts(tmem + kPairOCol, p_tmem + kk * 8,
+                        sm100::make_sw128_desc(v_addr + (kk >> 2) * (kPairVBytes / 2) + (kk & 3) * 32), idesc_o,
                         (i | kk) != 0);
           pair_commit(&pv_done[gg & 1]);
           pair_commit(&v_empty[vs]);
@@ -1398,46 +1409,44 @@ __global__ void __launch_bounds__(kThreads, 1)
             vph ^= 1;
           }
         };
-        for (int i = 0; i < nb; ++i, ++g) {
-          const int s = (int)(g & 1);
+        for (int i = 0; i < nsb; ++i, ++g) {
           sm100::mbar_wait(&k_full[ks], kph);
-          if (g >= 2) sm100::mbar_wait(&s_free[s], ((g >> 1) & 1) ^ 1);
           sm100::tc_fence_after();
           const uint32_t k_addr = sm100::smem_u32(sK + ks * kPairKBytes);
 #pragma unroll
           for (int kk = 0; kk < HD / 16; ++kk) {
             const int c = kk >> 2, w = kk & 3;
-            pair_mma(tmem + s * BKEY, sm100::make_sw128_desc(q_addr + c * (BQ * 128) + w * 32),
-                     sm100::make_sw128_desc(k_addr + c * (32 * 128) + w * 32), idesc_s, kk != 0);
+            pair_mma(tmem + (uint32_t)(g & 1) * (2 * BKEY), sm100::make_sw128_desc(q_addr + c * (BQ * 128) + w * 32),
+                     sm100::make_sw128_desc(k_addr + c * (BKEY * 128) + w * 32), idesc_s, kk != 0);
           }
-          pair_commit(&s_full[s]);
+          pair_commit(&s_full[g & 1]);
           pair_commit(&k_empty[ks]);
           if (++ks == kPairKSlots) {
             ks = 0;
             kph ^= 1;
           }
-          if (i == nb - 1) pair_commit(q_empty);
+          if (i == nsb - 1) pair_commit(q_empty);
           if (i >= 1) issue_pv(g - 1);
         }
-        if (nb > 0) issue_pv(g - 1);
+        if (nsb > 0) issue_pv(g - 1);
       }
     }
     __syncwarp();
   } else {
     const int q = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int half = (warp - 2) >> 2;  // keys [64 half, 64 half + 64) of a superblock = block 2G + half
     const int r = q * 32 + lane;
     const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t sfree_l = pair_mapa(sm100::smem_u32(s_free), 0);
     const uint32_t pfull_l = pair_mapa(sm100::smem_u32(p_full), 0);
     const uint32_t ofree_l = pair_mapa(sm100::smem_u32(o_free), 0);
     sm100::pdl_wait();
     if (threadIdx.x == 64) sm100::pdl_launch_dependents();
     long long g = 0;
     for (int it = 0; it < my_pairs; ++it) {
-      int env, env_start, m0, sb, nb;
+      int env, env_start, m0, sb, nbt;
       bool valid;
-      pair_geom(cl + it * n_cl, env, env_start, m0, valid, sb, nb);
+      pair_geom(cl + it * n_cl, env, env_start, m0, valid, sb, nbt);
+      const int nsb = (nbt + 1) / 2;
       const int tok = m0 + (r >> 3);
       const int head = r & 7;
       const int local_q = tok - env_start;
@@ -1447,51 +1456,55 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int seg_lo = seg_q * p.seg_len;
       const int seg_hi = seg_lo + (t_q >= 1 ? p.seg_len : 1);
       float m_used = -INFINITY, l_sum = 0.f;
-      for (int i = 0; i < nb; ++i, ++g) {
-        const int j = i;
+      for (int i = 0; i < nsb; ++i, ++g) {
         const int s = (int)(g & 1);
+        const uint32_t t_s = t_lane + (uint32_t)s * (2 * BKEY);
         sm100::mbar_wait(&s_full[s], (g >> 1) & 1);
         sm100::tc_fence_after();
-        uint32_t raw[2][16];
+        float sv[64];
+        {
+          uint32_t raw[4][16];
 #pragma unroll
-        for (int c = 0; c < 2; ++c) sm100::tmem_ld16(t_lane + s * BKEY + half * 32 + c * 16, raw[c]);
-        sm100::tmem_ld_wait();
-        sm100::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) pair_arrive(sfree_l + s * 8);
-        int lo = 0, hi;
-        if (j < p.n_prefix_blocks) {
-          hi = p.prefix_len - j * BKEY;
-        } else if (real_q) {
-          const int base = sb + (j - p.n_prefix_blocks) * BKEY - env_start;
-          lo = seg_lo - base;
-          hi = seg_hi - base;
-        } else {
-          hi = 0;
-        }
-        lo -= half * 32;
-        hi -= half * 32;
-        float sv[32];
-        float mb;
-        if (lo <= 0 && hi >= 32) {
+          for (int c = 0; c < 4; ++c) sm100::tmem_ld16(t_s + half * BKEY + c * 16, raw[c]);
+          sm100::tmem_ld_wait();
+          const int j = 2 * i + half;
+          int lo = 0, hi;
+          if (j >= nbt) {
+            hi = 0;
+          } else if (j < p.n_prefix_blocks) {
+            hi = p.prefix_len - j * BKEY;
+          } else if (real_q) {
+            const int base = sb + (j - p.n_prefix_blocks) * BKEY - env_start;
+            lo = seg_lo - base;
+            hi = seg_hi - base;
+          } else {
+            hi = 0;
+          }
+          if (lo <= 0 && hi >= BKEY) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) sv[c] = __uint_as_float(raw[c >> 4][c & 15]);
-        } else {
+            for (int c = 0; c < 64; ++c) sv[c] = __uint_as_float(raw[c >> 4][c & 15]);
+          } else {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const float x = __uint_as_float(raw[c >> 4][c & 15]);
-            sv[c] = (c >= lo && c < hi) ? x : -INFINITY;
+            for (int c = 0; c < 64; ++c) {
+              const float x = __uint_as_float(raw[c >> 4][c & 15]);
+              sv[c] = (c >= lo && c < hi) ? x : -INFINITY;
+            }
           }
         }
+        float mb;
         {
-          float t[11];
+          float t[22];
 #pragma unroll
-          for (int c = 0; c < 10; ++c) t[c] = fmax3(sv[3 * c], sv[3 * c + 1], sv[3 * c + 2]);
-          t[10] = fmaxf(sv[30], sv[31]);
-          const float u0 = fmax3(t[0], t[1], t[2]), u1 = fmax3(t[3], t[4], t[5]);
-          const float u2 = fmax3(t[6], t[7], t[8]), u3 = fmaxf(t[9], t[10]);
-          mb = fmaxf(fmax3(u0, u1, u2), u3);
+          for (int c = 0; c < 21; ++c) t[c] = fmax3(sv[3 * c], sv[3 * c + 1], sv[3 * c + 2]);
+          t[21] = sv[63];
+          float u[8];
+#pragma unroll
+          for (int c = 0; c < 7; ++c) u[c] = fmax3(t[3 * c], t[3 * c + 1], t[3 * c + 2]);
+          u[7] = t[21];
+          mb = fmaxf(fmax3(u[0], u[1], u[2]), fmaxf(fmax3(u[3], u[4], u[5]), fmaxf(u[6], u[7])));
         }
+        // both halves of the row finished reading S (their tcgen05.ld waited)
+        // before anyone overwrites the slot's first 64 columns with P
         xm[(s * 2 + half) * BQ + r] = mb;
         asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
         mb = fmaxf(xm[(s * 2) * BQ + r], xm[(s * 2 + 1) * BQ + r]) * p.scale_log2;
@@ -1508,21 +1521,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         const float mu = m_used == -INFINITY ? 0.f : m_used;
-        uint32_t pw[16];
+        uint32_t pw[32];
         float lp = 0.f;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < 32; ++k) {
           const float p0 = ex2_approx(fmaf(sv[2 * k], p.scale_log2, -mu));
           const float p1 = ex2_approx(fmaf(sv[2 * k + 1], p.scale_log2, -mu));
           lp += p0 + p1;
           __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
           pw[k] = *reinterpret_cast<uint32_t*>(&b2);
-        }
-        // P slot s is free once PV(g-2) retired; PV(g-1) may still run
-        // unless O has to be rescaled
-        if (g >= 2) {
-          sm100::mbar_wait(&pv_done[s], ((g - 2) >> 1) & 1);
-          sm100::tc_fence_after();
         }
         const bool any_rescale = __any_sync(0xffffffffu, rescale);
         if (any_rescale && i >= 1) {
@@ -1532,24 +1539,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
           for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 16) {
             uint32_t o[16];
-            sm100::tmem_ld16(t_lane + 128 + c0, o);
+            sm100::tmem_ld16(t_lane + kPairOCol + c0, o);
             sm100::tmem_ld_wait();
 #pragma unroll
             for (int k = 0; k < 16; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
-            sm100::tmem_st16(t_lane + 128 + c0, o);
+            sm100::tmem_st16(t_lane + kPairOCol + c0, o);
           }
           sm100::tmem_st_wait();
         } else if (rescale) {
           l_sum *= alpha;
         }
         l_sum += lp;
-        sm100::tmem_st16(t_lane + kPCol + s * (BKEY / 2) + half * 16, pw);
+        // P(G) keys [64 half, +64) -> columns [32 half, 32 half + 32) of the slot
+        sm100::tmem_st16(t_s + half * 32, *reinterpret_cast<const uint32_t(*)[16]>(&pw[0]));
+        sm100::tmem_st16(t_s + half * 32 + 16, *reinterpret_cast<const uint32_t(*)[16]>(&pw[16]));
         sm100::tmem_st_wait();
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) pair_arrive(pfull_l + s * 8);
       }
-      if (nb > 0) {
+      if (nsb > 0) {
         sm100::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
         sm100::tc_fence_after();
       }
@@ -1564,8 +1573,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u4 = 0; u4 < 4; ++u4) {
         uint32_t o[2][16];
         const int c0 = half * 128 + u4 * 32;
-        sm100::tmem_ld16(t_lane + 128 + c0, o[0]);
-        sm100::tmem_ld16(t_lane + 128 + c0 + 16, o[1]);
+        sm100::tmem_ld16(t_lane + kPairOCol + c0, o[0]);
+        sm100::tmem_ld16(t_lane + kPairOCol + c0 + 16, o[1]);
         sm100::tmem_ld_wait();
 #pragma unroll
         for (int u = 0; u < 2; ++u)

@@ -907,11 +907,10 @@ int build(Handle& h, Buffers& b, int B, int K) {
     if ((rc = gemm::make_map(&mp[3], b.ks, b.M, c.head_dim, c.head_dim, attn::BKEY))) return rc;
     if ((rc = gemm::make_map(&mp[4], b.vt, c.head_dim, b.m_ld, b.m_ld, c.head_dim))) return rc;
   }
-  // 2-SM attention for batched rounds (one split): each CTA of a pair loads
-  // half of every key block (32 keys of K, 128 dims of V^T)
-  // (opt-in, SF_ATTN_PAIR=1: measured slower than the 1-SM kernel with split
-  // K/V slots -- the key-block chain is latency-, not ingress-bound)
-  b.attn_pair = b.attn_splits == 1 && b.env_rows / 16 >= 2 && getenv("SF_ATTN_PAIR") != nullptr;
+  // 2-SM attention for batched rounds (one split): 128-key superblocks, CTA r
+  // of a pair loads key block 2G + r and dims [128 r, 128 r + 128) of V^T
+  // (default; SF_ATTN_SINGLE=1 selects the 1-SM persistent kernel)
+  b.attn_pair = b.attn_splits == 1 && b.env_rows / 16 >= 2 && getenv("SF_ATTN_SINGLE") == nullptr;
   if (b.attn_pair) {
     b.attn_pair_maps.resize(5 * L);
     for (int l = 0; l < L; ++l) {
@@ -920,12 +919,12 @@ int build(Handle& h, Buffers& b, int B, int K) {
       const bf16* kp = h.k_prefix + (size_t)l * E * c.prefix_len * c.head_dim;
       const bf16* vp = h.vt_prefix + (size_t)l * E * c.head_dim * c.prefix_len;
       if ((rc = make_map_3d(&mp[1], kp, c.head_dim, c.prefix_len, E, (uint64_t)c.head_dim * 2,
-                            (uint64_t)c.prefix_len * c.head_dim * 2, 64, 32)))
+                            (uint64_t)c.prefix_len * c.head_dim * 2, 64, attn::BKEY)))
         return rc;
       if ((rc = make_map_3d(&mp[2], vp, c.prefix_len, c.head_dim, E, (uint64_t)c.prefix_len * 2,
                             (uint64_t)c.prefix_len * c.head_dim * 2, attn::BKEY, c.head_dim / 2)))
         return rc;
-      if ((rc = gemm::make_map(&mp[3], b.ks, b.M, c.head_dim, c.head_dim, 32))) return rc;
+      if ((rc = gemm::make_map(&mp[3], b.ks, b.M, c.head_dim, c.head_dim, attn::BKEY))) return rc;
       if ((rc = gemm::make_map(&mp[4], b.vt, c.head_dim, b.m_ld, b.m_ld, c.head_dim / 2))) return rc;
     }
   }

@@ -220,9 +220,10 @@ def test_full_size_cfg3_verify_vs_oracle():
 
 
 def test_attention_pair_kernel_matches_single_sm():
-    """Batched rounds (one KV split) run attention on 2-SM CTA pairs
-    (attn_pair_kernel, odd tile counts paired with a dummy partner); it must
-    agree with the 1-SM kernel on the same inputs."""
+    """Batched rounds (one KV split) run attention on 2-SM CTA pairs by default
+    (attn_pair_kernel: 128-key superblocks, odd tile counts paired with a dummy
+    partner); it must agree with the 1-SM persistent kernel (SF_ATTN_SINGLE=1)
+    on the same inputs."""
     import os
 
     import torch
@@ -239,14 +240,14 @@ def test_attention_pair_kernel_matches_single_sm():
     s = torch.from_numpy(rng.standard_normal((E, S)).astype(np.float32)).cuda()
     cfg = VerifierConfig(timesteps=(0.2, 0.4, 0.6, 0.8), delta=0.5)
     outs = []
-    for flag in (None, "1"):
+    for flag in ("1", None):
         if flag:
-            os.environ["SF_ATTN_PAIR"] = flag
+            os.environ["SF_ATTN_SINGLE"] = flag
         else:
-            os.environ.pop("SF_ATTN_PAIR", None)
+            os.environ.pop("SF_ATTN_SINGLE", None)
         ae = pi0.ActionExpert(dcfg, seed=0, n_envs=E, kv_seed=1)
         outs.append([t.clone() for t in ae.verify_batch(cfg, d, e, s)])
-    os.environ.pop("SF_ATTN_PAIR", None)
+    os.environ.pop("SF_ATTN_SINGLE", None)
     (r0, d0, _, _), (r1, d1, _, _) = outs
     torch.testing.assert_close(r1, r0, rtol=2e-3, atol=2e-3 * r0.abs().max().item())
     torch.testing.assert_close(d1, d0, rtol=2e-3, atol=2e-3 * d0.abs().max().item())
