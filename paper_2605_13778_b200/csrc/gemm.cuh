@@ -874,7 +874,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::tma_prefetch_desc(&tma_a);
       sm100::tma_prefetch_desc(&tma_b);
       const uint64_t pol_w = sm100::policy_evict_last();
-      const uint64_t pol_x = sm100::policy_evict_first();
+      // activations too: the tiles_n pairs sharing an A row block run at about
+      // the same time, and evict_first let lagging readers miss to HBM
+      // (QKV read 4x its A bytes from DRAM); evict_last: -3 % on the batched
+      // GEMMs (evict_normal: -1.5 %)
+      const uint64_t pol_x = sm100::policy_evict_last();
       int kiter = 0;
       bool first = true;
       for (int t = pair; t < p.total_tiles; t += n_pairs) {
