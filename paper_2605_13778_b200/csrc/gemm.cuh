@@ -826,8 +826,13 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       "h"((uint16_t)3)
       : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
+// Release of a TMEM accumulator to the leader: only the epilogue's tcgen05.ld
+// (waited, then tcgen05.fence::before_thread_sync) must precede it, not its
+// global stores, so the arrive is relaxed (a .release.cluster arrive makes
+// every thread wait for its stores: MEMBAR + ERRBAR, 10 % of the QKV
+// kernel's stall samples) and issued once per warp.
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
                : "memory");
 }
 
@@ -855,7 +860,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       sm100::mbar_init(&T.tmem_full[a], 1);
-      sm100::mbar_init(&T.tmem_empty[a], 2 * kEpiThreads);
+      sm100::mbar_init(&T.tmem_empty[a], 2 * kEpiWarps);
     }
     sm100::fence_barrier_init();
   }
@@ -958,7 +963,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       sm100::tc_fence_before();
-      mbar_arrive_remote(te + a * 8);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote_relaxed(te + a * 8);
       if (KIND == EPI_RESID) {
         T.sred[(g * 2 + 0) * 128 + lane_row] = ssq0;
         T.sred[(g * 2 + 1) * 128 + lane_row] = ssq1;
