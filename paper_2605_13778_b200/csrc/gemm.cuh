@@ -67,6 +67,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+// 32-byte global store (one STG.256: a full L2 sector per lane)
+__device__ __forceinline__ void st_global_v8(void* p, const uint32_t (&w)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+               "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
 
 // ------------------------------------------------------------- epilogues
 //
@@ -944,6 +950,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::tc_fence_after();
       const uint32_t t_lane = tmem + a * 256 + ((uint32_t)(q * 32) << 16);
       float ssq0 = 0.f, ssq1 = 0.f;
+      if (KIND == EPI_QKV && tn * 256 < e.q_features + 256) {
+        // q / k head tile with RoPE: adjacent chunks (c, c+1) per pass, so each
+        // row's rotated halves leave as 32 B runs (dims [8c, 8c+16) and
+        // [128+8c, 128+8c+16)) -- full L2 sectors instead of 16 B pieces
+        const int pos = m < e.M ? e.pos0 + ((m % e.env_rows) % e.seg_len) : 0;
+        __nv_bfloat16* base = tn * 256 < e.q_features ? e.q + (size_t)m * e.q_features + tn * 256
+                                                      : e.k + (size_t)m * 256;
+        for (int c = 2 * g; c < 16; c += 4) {
+          uint32_t r[2][16];
+          sm100::tmem_ld16(t_lane + c * 16, r[0]);
+          sm100::tmem_ld16(t_lane + (c + 1) * 16, r[1]);
+          sm100::tmem_ld_wait();
+          uint32_t wa[8], wb[8];
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int pp = 0; pp < 8; pp += 2) {
+              float ya[2], yb[2];
+#pragma unroll
+              for (int w2 = 0; w2 < 2; ++w2) {
+                const int pr = pp + w2;  // pair index inside the chunk
+                const float x0 = __uint_as_float(r[u][2 * pr]) * rs, x1 = __uint_as_float(r[u][2 * pr + 1]) * rs;
+                const float2 cs = __ldg(e.rope + (size_t)((c + u) * 8 + pr) * e.rope_ld + pos);
+                ya[w2] = x0 * cs.x - x1 * cs.y;
+                yb[w2] = x1 * cs.x + x0 * cs.y;
+              }
+              wa[u * 4 + (pp >> 1)] = pack_bf16(ya[0], ya[1]);
+              wb[u * 4 + (pp >> 1)] = pack_bf16(yb[0], yb[1]);
+            }
+          if (m < e.M) {
+            st_global_v8(base + c * 8, wa);
+            st_global_v8(base + 128 + c * 8, wb);
+          }
+        }
+      } else
       for (int ch = g; ch < 16; ch += 4) {  // two TMEM loads in flight per wait
         uint32_t r[2][16];
         sm100::tmem_ld16(t_lane + ch * 16, r[0]);
