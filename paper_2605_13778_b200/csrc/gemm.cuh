@@ -984,6 +984,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             st_global_v8(base + 128 + c * 8, wb);
           }
         }
+      } else if (KIND == EPI_GEGLU && (e.ld_bf16 % 16) == 0 && tn * 256 + 256 <= e.N) {
+        // adjacent chunk pairs: 16 consecutive outputs h[128 tn + 8c, +16) per
+        // row leave as one 32 B store (full L2 sector)
+        __nv_bfloat16* hrow = e.out_bf16 + (size_t)m * e.ld_bf16 + tn * 128;
+        for (int c = 2 * g; c < 16; c += 4) {
+          uint32_t r[2][16];
+          sm100::tmem_ld16(t_lane + c * 16, r[0]);
+          sm100::tmem_ld16(t_lane + (c + 1) * 16, r[1]);
+          sm100::tmem_ld_wait();
+          uint32_t w[8];
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int pp = 0; pp < 8; pp += 2) {
+              const float h0 = gelu_tanh(__uint_as_float(r[u][2 * pp]) * rs) * (__uint_as_float(r[u][2 * pp + 1]) * rs);
+              const float h1 =
+                  gelu_tanh(__uint_as_float(r[u][2 * pp + 2]) * rs) * (__uint_as_float(r[u][2 * pp + 3]) * rs);
+              w[u * 4 + (pp >> 1)] = pack_bf16(h0, h1);
+            }
+          if (m < e.M) st_global_v8(hrow + c * 8, w);
+        }
       } else
       for (int ch = g; ch < 16; ch += 4) {  // two TMEM loads in flight per wait
         uint32_t r[2][16];
