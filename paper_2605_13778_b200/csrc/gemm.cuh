@@ -251,15 +251,16 @@ __device__ __forceinline__ void epi_normal(const EpiArgs& e, int m, int n0, floa
         __syncwarp();
         const int m0w = m - lane;  // first token of the warp
         const int d = lane >> 1;
-#pragma unroll
-        for (int o2 = 0; o2 < 2; ++o2) {
-          const int o = (lane & 1) * 2 + o2;  // token octet
-          const uint4 val = *reinterpret_cast<const uint4*>(vbuf + d * 32 + o * 8);
-          if (m0w + o * 8 + 7 < e.M)
-            *reinterpret_cast<uint4*>(e.vt + (size_t)(d0 + d) * e.vt_ld + m0w + o * 8) = val;
-          else
-            for (int z = 0; z < 8; ++z)
-              if (m0w + o * 8 + z < e.M) e.vt[(size_t)(d0 + d) * e.vt_ld + m0w + o * 8 + z] = vbuf[d * 32 + o * 8 + z];
+        const int t0 = (lane & 1) * 16;  // 16 consecutive tokens of feature d: one 32 B store
+        __nv_bfloat16* dst = e.vt + (size_t)(d0 + d) * e.vt_ld + m0w + t0;
+        if (m0w + t0 + 15 < e.M && (e.vt_ld % 16) == 0) {
+          const uint4 v0 = *reinterpret_cast<const uint4*>(vbuf + d * 32 + t0);
+          const uint4 v1 = *reinterpret_cast<const uint4*>(vbuf + d * 32 + t0 + 8);
+          const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+          st_global_v8(dst, w);
+        } else {
+          for (int z = 0; z < 16; ++z)
+            if (m0w + t0 + z < e.M) dst[z] = vbuf[d * 32 + t0 + z];
         }
         __syncwarp();
       } else {
