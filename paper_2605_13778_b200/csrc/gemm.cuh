@@ -271,8 +271,9 @@ __device__ __forceinline__ void epi_normal(const EpiArgs& e, int m, int n0, floa
   } else if (KIND == EPI_RESID) {
     if (vbuf) {
       // Coalesced residual update: the warp's 32 rows x 16 columns go through
-      // a per-warp SMEM scratch so that every load/store instruction covers
-      // 8 rows x 64 contiguous bytes (instead of 32 rows x 16 B).
+      // a per-warp SMEM scratch so that every lane moves 32 contiguous bytes of
+      // one row per instruction (LDG/STG.256 for x, 16 B for xb): 16 rows x
+      // 64 B per x instruction, 16 rows x 32 B per xb instruction.
       float* sc = reinterpret_cast<float*>(vbuf);  // [32][16], quads XOR-swizzled by row
       const int lane = threadIdx.x & 31;
       const int m0w = m - lane;
@@ -281,42 +282,50 @@ __device__ __forceinline__ void epi_normal(const EpiArgs& e, int m, int n0, floa
         reinterpret_cast<float4*>(sc + lane * 16)[qd ^ (lane & 3)] =
             make_float4(v[4 * qd], v[4 * qd + 1], v[4 * qd + 2], v[4 * qd + 3]);
       __syncwarp();
-      float rowsq[4];
-      float4 xo[4];
-      const int qd = lane & 3;
+      float rowsq[2];
+      float xo[2][8];
+      const int hq = lane & 1;  // columns [8 hq, 8 hq + 8) of the chunk
 #pragma unroll
-      for (int pass = 0; pass < 4; ++pass) {  // every residual load in flight first
-        const int row = m0w + pass * 8 + (lane >> 2);
-        xo[pass] = row < e.M ? *reinterpret_cast<const float4*>(e.x + (size_t)row * e.N + n0 + qd * 4)
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int pass = 0; pass < 2; ++pass) {  // every residual load in flight first
+        const int row = m0w + pass * 16 + (lane >> 1);
+        if (row < e.M) {
+          asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=f"(xo[pass][0]), "=f"(xo[pass][1]), "=f"(xo[pass][2]), "=f"(xo[pass][3]),
+                         "=f"(xo[pass][4]), "=f"(xo[pass][5]), "=f"(xo[pass][6]), "=f"(xo[pass][7])
+                       : "l"(e.x + (size_t)row * e.N + n0 + hq * 8));
+        } else {
+#pragma unroll
+          for (int z = 0; z < 8; ++z) xo[pass][z] = 0.f;
+        }
       }
 #pragma unroll
-      for (int pass = 0; pass < 4; ++pass) {
-        const int rr = pass * 8 + (lane >> 2);
+      for (int pass = 0; pass < 2; ++pass) {
+        const int rr = pass * 16 + (lane >> 1);
         const int row = m0w + rr;
-        const float4 a = reinterpret_cast<const float4*>(sc + rr * 16)[qd ^ (rr & 3)];
-        float4 x4 = xo[pass];
-        x4.x += a.x;
-        x4.y += a.y;
-        x4.z += a.z;
-        x4.w += a.w;
+        const float4 a0 = reinterpret_cast<const float4*>(sc + rr * 16)[(2 * hq) ^ (rr & 3)];
+        const float4 a1 = reinterpret_cast<const float4*>(sc + rr * 16)[(2 * hq + 1) ^ (rr & 3)];
+        float y[8] = {xo[pass][0] + a0.x, xo[pass][1] + a0.y, xo[pass][2] + a0.z, xo[pass][3] + a0.w,
+                      xo[pass][4] + a1.x, xo[pass][5] + a1.y, xo[pass][6] + a1.z, xo[pass][7] + a1.w};
         float sq = 0.f;
         if (row < e.M) {
-          *reinterpret_cast<float4*>(e.x + (size_t)row * e.N + n0 + qd * 4) = x4;
-          *reinterpret_cast<uint2*>(e.xb + (size_t)row * e.N + n0 + qd * 4) =
-              make_uint2(pack_bf16(x4.x, x4.y), pack_bf16(x4.z, x4.w));
-          sq = x4.x * x4.x + x4.y * x4.y + x4.z * x4.z + x4.w * x4.w;
+          const uint32_t w[8] = {__float_as_uint(y[0]), __float_as_uint(y[1]), __float_as_uint(y[2]),
+                                 __float_as_uint(y[3]), __float_as_uint(y[4]), __float_as_uint(y[5]),
+                                 __float_as_uint(y[6]), __float_as_uint(y[7])};
+          st_global_v8(e.x + (size_t)row * e.N + n0 + hq * 8, w);
+          *reinterpret_cast<uint4*>(e.xb + (size_t)row * e.N + n0 + hq * 8) =
+              make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
+#pragma unroll
+          for (int z = 0; z < 8; ++z) sq += y[z] * y[z];
         }
         sq += __shfl_xor_sync(0xffffffffu, sq, 1);
-        sq += __shfl_xor_sync(0xffffffffu, sq, 2);
         rowsq[pass] = sq;
       }
-      // row rr's chunk sum back to its owner lane rr (lane (rr % 8) * 4 of pass rr / 8)
+      // row rr's chunk sum back to its owner lane rr (lane (rr % 16) * 2 of pass rr / 16)
       float mine = 0.f;
 #pragma unroll
-      for (int pass = 0; pass < 4; ++pass) {
-        const float t = __shfl_sync(0xffffffffu, rowsq[pass], (lane & 7) * 4);
-        if ((lane >> 3) == pass) mine = t;
+      for (int pass = 0; pass < 2; ++pass) {
+        const float t = __shfl_sync(0xffffffffu, rowsq[pass], (lane & 15) * 2);
+        if ((lane >> 4) == pass) mine = t;
       }
       ssq_acc += mine;
       __syncwarp();
