@@ -1074,11 +1074,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int u4 = 0; u4 < 4; ++u4)
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst + u4 * 32 + 16 * u);
-            d4[0] = make_uint4(ow[u4][u][0], ow[u4][u][1], ow[u4][u][2], ow[u4][u][3]);
-            d4[1] = make_uint4(ow[u4][u][4], ow[u4][u][5], ow[u4][u][6], ow[u4][u][7]);
-          }
+          for (int u = 0; u < 2; ++u)  // 16 dims = one full 32 B sector per store
+            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + u4 * 32 + 16 * u),
+                         "r"(ow[u4][u][0]), "r"(ow[u4][u][1]), "r"(ow[u4][u][2]), "r"(ow[u4][u][3]),
+                         "r"(ow[u4][u][4]), "r"(ow[u4][u][5]), "r"(ow[u4][u][6]), "r"(ow[u4][u][7])
+                         : "memory");
       }
     }
   }
@@ -1593,11 +1593,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int u4 = 0; u4 < 4; ++u4)
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst + u4 * 32 + 16 * u);
-            d4[0] = make_uint4(ow[u4][u][0], ow[u4][u][1], ow[u4][u][2], ow[u4][u][3]);
-            d4[1] = make_uint4(ow[u4][u][4], ow[u4][u][5], ow[u4][u][6], ow[u4][u][7]);
-          }
+          for (int u = 0; u < 2; ++u)  // 16 dims = one full 32 B sector per store
+            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + u4 * 32 + 16 * u),
+                         "r"(ow[u4][u][0]), "r"(ow[u4][u][1]), "r"(ow[u4][u][2]), "r"(ow[u4][u][3]),
+                         "r"(ow[u4][u][4]), "r"(ow[u4][u][5]), "r"(ow[u4][u][6]), "r"(ow[u4][u][7])
+                         : "memory");
       }
     }
   }
