@@ -113,6 +113,19 @@ def test_verify_matches_oracle_small(n_envs, k):
     assert flips <= max(1, n_envs // 3)
 
 
+@pytest.mark.parametrize("attn", ["pair", "single"])
+def test_verify_matches_oracle_batched_attention(attn, monkeypatch):
+    """The batched (one KV split) attention kernels against the oracle: the
+    default 2-SM pair kernel (128-key superblocks, 3 query tiles per env so the
+    last pair has a dummy partner) and the 1-SM persistent kernel."""
+    monkeypatch.setenv("SF_ATTN_SPLITS", "1")
+    if attn == "single":
+        monkeypatch.setenv("SF_ATTN_SINGLE", "1")
+    else:
+        monkeypatch.delenv("SF_ATTN_SINGLE", raising=False)
+    test_verify_matches_oracle_small(6, 4)
+
+
 @pytest.mark.parametrize("n_envs", [1, 300])
 def test_flash_round_draft_matches_oracle(n_envs):
     """propose (draft MLP) fused into the verify graph: draft vs oracle, and the
