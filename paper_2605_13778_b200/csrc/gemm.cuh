@@ -67,6 +67,24 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+// Residual rows of one 16-column chunk in the staged layout (lane: row
+// pass * 16 + lane / 2, columns 8 (lane & 1) .. +8): two 32 B loads per lane.
+__device__ __forceinline__ void resid_load(const float* x, int M, int N, int m0w, int n0, int lane,
+                                           float (&xo)[2][8]) {
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+    const int row = m0w + pass * 16 + (lane >> 1);
+    if (row < M) {
+      asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=f"(xo[pass][0]), "=f"(xo[pass][1]), "=f"(xo[pass][2]), "=f"(xo[pass][3]),
+                     "=f"(xo[pass][4]), "=f"(xo[pass][5]), "=f"(xo[pass][6]), "=f"(xo[pass][7])
+                   : "l"(x + (size_t)row * N + n0 + (lane & 1) * 8));
+    } else {
+#pragma unroll
+      for (int z = 0; z < 8; ++z) xo[pass][z] = 0.f;
+    }
+  }
+}
 // 32-byte global store (one STG.256: a full L2 sector per lane)
 __device__ __forceinline__ void st_global_v8(void* p, const uint32_t (&w)[8]) {
   asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
@@ -992,6 +1010,78 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (m < e.M) {
             st_global_v8(base + c * 8, wa);
             st_global_v8(base + 128 + c * 8, wb);
+          }
+        }
+      } else if (KIND == EPI_RESID && tn * 256 + 256 <= e.N) {
+        // residual chunks: the next pass's x rows are loaded before this pass's
+        // TMEM loads are consumed (two chunk pairs of loads in flight)
+        float* sc = reinterpret_cast<float*>(T.vbuf + (warp - 2) * 1024);  // [32][16] staging
+        const int m0w = m - lane;
+        float xo[2][2][8];
+        resid_load(e.x, e.M, e.N, m0w, tn * 256 + g * 16, lane, xo[0]);
+        resid_load(e.x, e.M, e.N, m0w, tn * 256 + (g + 2) * 16, lane, xo[1]);
+        for (int ch = g; ch < 16; ch += 4) {
+          uint32_t r[2][16];
+          sm100::tmem_ld16(t_lane + ch * 16, r[0]);
+          sm100::tmem_ld16(t_lane + (ch + 2) * 16, r[1]);
+          sm100::tmem_ld_wait();
+          float xn[2][2][8];
+          if (ch + 4 < 16) {
+            resid_load(e.x, e.M, e.N, m0w, tn * 256 + (ch + 4) * 16, lane, xn[0]);
+            resid_load(e.x, e.M, e.N, m0w, tn * 256 + (ch + 6) * 16, lane, xn[1]);
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int n0 = tn * 256 + (ch + 2 * u) * 16;
+#pragma unroll
+            for (int qd = 0; qd < 4; ++qd)
+              reinterpret_cast<float4*>(sc + lane * 16)[qd ^ (lane & 3)] =
+                  make_float4(__uint_as_float(r[u][4 * qd]), __uint_as_float(r[u][4 * qd + 1]),
+                              __uint_as_float(r[u][4 * qd + 2]), __uint_as_float(r[u][4 * qd + 3]));
+            __syncwarp();
+            const int hq = lane & 1;
+            float rowsq[2];
+#pragma unroll
+            for (int pass = 0; pass < 2; ++pass) {
+              const int rr = pass * 16 + (lane >> 1);
+              const int row = m0w + rr;
+              const float4 a0 = reinterpret_cast<const float4*>(sc + rr * 16)[(2 * hq) ^ (rr & 3)];
+              const float4 a1 = reinterpret_cast<const float4*>(sc + rr * 16)[(2 * hq + 1) ^ (rr & 3)];
+              const float* xv = xo[u][pass];
+              const float y[8] = {xv[0] + a0.x, xv[1] + a0.y, xv[2] + a0.z, xv[3] + a0.w,
+                                  xv[4] + a1.x, xv[5] + a1.y, xv[6] + a1.z, xv[7] + a1.w};
+              float sq = 0.f;
+              if (row < e.M) {
+                const uint32_t w[8] = {__float_as_uint(y[0]), __float_as_uint(y[1]), __float_as_uint(y[2]),
+                                       __float_as_uint(y[3]), __float_as_uint(y[4]), __float_as_uint(y[5]),
+                                       __float_as_uint(y[6]), __float_as_uint(y[7])};
+                st_global_v8(e.x + (size_t)row * e.N + n0 + hq * 8, w);
+                *reinterpret_cast<uint4*>(e.xb + (size_t)row * e.N + n0 + hq * 8) =
+                    make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]),
+                               pack_bf16(y[6], y[7]));
+#pragma unroll
+                for (int z = 0; z < 8; ++z) sq += y[z] * y[z];
+              }
+              sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+              rowsq[pass] = sq;
+            }
+            float mine = 0.f;
+#pragma unroll
+            for (int pass = 0; pass < 2; ++pass) {
+              const float t2 = __shfl_sync(0xffffffffu, rowsq[pass], (lane & 15) * 2);
+              if ((lane >> 4) == pass) mine = t2;
+            }
+            if ((ch + 2 * u) * 16 < 128) ssq0 += mine;
+            else ssq1 += mine;
+            __syncwarp();
+          }
+          if (ch + 4 < 16) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+              for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+                for (int z = 0; z < 8; ++z) xo[u][pass][z] = xn[u][pass][z];
           }
         }
       } else if (KIND == EPI_GEGLU && (e.ld_bf16 % 16) == 0 && tn * 256 + 256 <= e.N) {
