@@ -1379,36 +1379,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc_s = sm100::make_idesc_bf16(256, 2 * BKEY);
       const uint32_t idesc_o = sm100::make_idesc_bf16(256, HD);
       const uint32_t q_addr = sm100::smem_u32(sQ);
+      // One global superblock stream across pair tiles: S(g) then PV(g-1), so
+      // the first S of the next tile is issued before the previous tile's
+      // last PV and its softmax overlaps that PV; PV of a tile's first
+      // superblock waits until the softmax warps drained the previous O.
       long long g = 0;  // global superblock counter
       int ks = 0, vs = 0;
       uint32_t kph = 0, vph = 0;
-      for (int it = 0; it < my_pairs; ++it) {
+      int pv_it = 0, pv_i = 0, pv_nsb = 0;  // tile / index of the next PV
+      auto tile_nsb = [&](int t) {
         int env, env_start, m0, sb, nbt;
         bool valid;
-        pair_geom(cl + it * n_cl, env, env_start, m0, valid, sb, nbt);
-        const int nsb = (nbt + 1) / 2;
-        const long long g0 = g;
-        sm100::mbar_wait(q_full, it & 1);
-        auto issue_pv = [&](long long gg) {
-          const int i = (int)(gg - g0);
-          if (i == 0 && it > 0) sm100::mbar_wait(o_free, (it - 1) & 1);
-          sm100::mbar_wait(&p_full[gg & 1], (gg >> 1) & 1);
-          sm100::mbar_wait(&v_full[vs], vph);
-          sm100::tc_fence_after();
-          const uint32_t v_addr = sm100::smem_u32(sV + vs * kPairVBytes);
-          const uint32_t p_tmem = tmem + (uint32_t)(gg & 1) * (2 * BKEY);
+        pair_geom(cl + t * n_cl, env, env_start, m0, valid, sb, nbt);
+        return (nbt + 1) / 2;
+      };
+      auto issue_pv = [&](long long gg) {
+        if (pv_i == 0 && pv_it > 0) sm100::mbar_wait(o_free, (pv_it - 1) & 1);
+        sm100::mbar_wait(&p_full[gg & 1], (gg >> 1) & 1);
+        sm100::mbar_wait(&v_full[vs], vph);
+        sm100::tc_fence_after();
+        const uint32_t v_addr = sm100::smem_u32(sV + vs * kPairVBytes);
+        const uint32_t p_tmem = tmem + (uint32_t)(gg & 1) * (2 * BKEY);
 #pragma unroll
-          for (int kk = 0; kk < 2 * BKEY / 16; ++kk)  // 16 keys per MMA: 8 P columns, V^T chunk kk / 4
-            pair_mma_ts(tmem + kPairOCol, p_tmem + kk * 8,
-                        sm100::make_sw128_desc(v_addr + (kk >> 2) * (kPairVBytes / 2) + (kk & 3) * 32), idesc_o,
-                        (i | kk) != 0);
-          pair_commit(&pv_done[gg & 1]);
-          pair_commit(&v_empty[vs]);
-          if (++vs == kPairVSlots) {
-            vs = 0;
-            vph ^= 1;
-          }
-        };
+        for (int kk = 0; kk < 2 * BKEY / 16; ++kk)  // 16 keys per MMA: 8 P columns, V^T chunk kk / 4
+          pair_mma_ts(tmem + kPairOCol, p_tmem + kk * 8,
+                      sm100::make_sw128_desc(v_addr + (kk >> 2) * (kPairVBytes / 2) + (kk & 3) * 32), idesc_o,
+                      (pv_i | kk) != 0);
+        pair_commit(&pv_done[gg & 1]);
+        pair_commit(&v_empty[vs]);
+        if (++vs == kPairVSlots) {
+          vs = 0;
+          vph ^= 1;
+        }
+        if (++pv_i == pv_nsb) {
+          pv_i = 0;
+          ++pv_it;
+          if (pv_it < my_pairs) pv_nsb = tile_nsb(pv_it);
+        }
+      };
+      if (my_pairs > 0) pv_nsb = tile_nsb(0);
+      for (int it = 0; it < my_pairs; ++it) {
+        const int nsb = tile_nsb(it);
+        sm100::mbar_wait(q_full, it & 1);
         for (int i = 0; i < nsb; ++i, ++g) {
           sm100::mbar_wait(&k_full[ks], kph);
           sm100::tc_fence_after();
@@ -1426,10 +1438,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             kph ^= 1;
           }
           if (i == nsb - 1) pair_commit(q_empty);
-          if (i >= 1) issue_pv(g - 1);
+          if (g >= 1) issue_pv(g - 1);
         }
-        if (nsb > 0) issue_pv(g - 1);
       }
+      if (g > 0) issue_pv(g - 1);
     }
     __syncwarp();
   } else {
@@ -1442,6 +1454,55 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::pdl_wait();
     if (threadIdx.x == 64) sm100::pdl_launch_dependents();
     long long g = 0;
+    // A tile's O is drained after the NEXT tile's first superblock (whose S
+    // the MMA issues before this tile's last PV), so that PV overlaps softmax.
+    // xm slot for the row-sum exchange: glast & 1 when deferred (softmax of
+    // glast + 1 synchronised in between), else the other slot.
+    auto epilogue = [&](float lsum, int etok, bool estore, long long glast, bool deferred) {
+      sm100::mbar_wait(&pv_done[glast & 1], (glast >> 1) & 1);
+      sm100::tc_fence_after();
+      const int ls = (int)((deferred ? glast : glast + 1) & 1);
+      xm[(ls * 2 + half) * BQ + r] = lsum;
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+      lsum = xm[(ls * 2) * BQ + r] + xm[(ls * 2 + 1) * BQ + r];
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+      uint32_t ow[4][2][8];
+#pragma unroll
+      for (int u4 = 0; u4 < 4; ++u4) {
+        uint32_t o[2][16];
+        const int c0 = half * 128 + u4 * 32;
+        sm100::tmem_ld16(t_lane + kPairOCol + c0, o[0]);
+        sm100::tmem_ld16(t_lane + kPairOCol + c0 + 16, o[1]);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int kq = 0; kq < 8; ++kq) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[u][2 * kq]) * inv,
+                                                      __uint_as_float(o[u][2 * kq + 1]) * inv);
+            ow[u4][u][kq] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) pair_arrive(ofree_l);
+      if (estore) {
+        __nv_bfloat16* dst = p.out + (size_t)etok * (kHeads * HD) + (r & 7) * HD + half * 128;
+#pragma unroll
+        for (int u4 = 0; u4 < 4; ++u4)
+#pragma unroll
+          for (int u = 0; u < 2; ++u)  // 16 dims = one full 32 B sector per store
+            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + u4 * 32 + 16 * u),
+                         "r"(ow[u4][u][0]), "r"(ow[u4][u][1]), "r"(ow[u4][u][2]), "r"(ow[u4][u][3]),
+                         "r"(ow[u4][u][4]), "r"(ow[u4][u][5]), "r"(ow[u4][u][6]), "r"(ow[u4][u][7])
+                         : "memory");
+      }
+    };
+    bool pend = false, pend_store = false;
+    float pend_lsum = 0.f;
+    int pend_tok = 0;
+    long long pend_glast = 0;
     for (int it = 0; it < my_pairs; ++it) {
       int env, env_start, m0, sb, nbt;
       bool valid;
@@ -1557,49 +1618,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) pair_arrive(pfull_l + s * 8);
+        if (i == 0 && pend) {
+          epilogue(pend_lsum, pend_tok, pend_store, pend_glast, true);
+          pend = false;
+        }
       }
-      if (nsb > 0) {
-        sm100::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
-        sm100::tc_fence_after();
-      }
-      const int ls = (int)(g & 1);
-      xm[(ls * 2 + half) * BQ + r] = l_sum;
-      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
-      l_sum = xm[(ls * 2) * BQ + r] + xm[(ls * 2 + 1) * BQ + r];
-      asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
-      const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
-      uint32_t ow[4][2][8];
-#pragma unroll
-      for (int u4 = 0; u4 < 4; ++u4) {
-        uint32_t o[2][16];
-        const int c0 = half * 128 + u4 * 32;
-        sm100::tmem_ld16(t_lane + kPairOCol + c0, o[0]);
-        sm100::tmem_ld16(t_lane + kPairOCol + c0 + 16, o[1]);
-        sm100::tmem_ld_wait();
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[u][2 * k]) * inv,
-                                                      __uint_as_float(o[u][2 * k + 1]) * inv);
-            ow[u4][u][k] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-      }
-      sm100::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) pair_arrive(ofree_l);
-      if (valid && tok < p.M) {
-        __nv_bfloat16* dst = p.out + (size_t)tok * (kHeads * HD) + head * HD + half * 128;
-#pragma unroll
-        for (int u4 = 0; u4 < 4; ++u4)
-#pragma unroll
-          for (int u = 0; u < 2; ++u)  // 16 dims = one full 32 B sector per store
-            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + u4 * 32 + 16 * u),
-                         "r"(ow[u4][u][0]), "r"(ow[u4][u][1]), "r"(ow[u4][u][2]), "r"(ow[u4][u][3]),
-                         "r"(ow[u4][u][4]), "r"(ow[u4][u][5]), "r"(ow[u4][u][6]), "r"(ow[u4][u][7])
-                         : "memory");
-      }
+      pend = nsb > 0;
+      pend_lsum = l_sum;
+      pend_tok = tok;
+      pend_store = valid && tok < p.M;
+      pend_glast = g - 1;
     }
+    if (pend) epilogue(pend_lsum, pend_tok, pend_store, pend_glast, false);
   }
   sm100::tc_fence_before();
   cluster.sync();  // the peer's barriers / TMEM are no longer referenced
