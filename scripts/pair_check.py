@@ -1,3 +1,8 @@
+"""pi0-scale verify outputs of the 1-SM persistent attention kernel
+(SF_ATTN_SINGLE=1) vs the default 2-SM pair kernel on the same inputs.
+
+usage: python scripts/pair_check.py
+"""
 import os, sys, torch
 sys.path.insert(0, os.getcwd())
 from paper_2605_13778_b200.pi0 import PI0, ActionExpert
