@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int hi = min(lo + 15, p.segs * p.seg_len - 1);
     hi = hi < lo ? lo : hi;
     const int seg_last = hi / p.seg_len;
-    sb = (env_start + seg_first * p.seg_len) & ~(BKEY - 1);
+    sb = (env_start + seg_first * p.seg_len) & ~7;  // 8-key (16 B) aligned start of the tile's suffix keys
     const int n_suf = (env_start + (seg_last + 1) * p.seg_len - sb + BKEY - 1) / BKEY;
     nbt = p.n_prefix_blocks + min(n_suf, p.n_blocks - p.n_prefix_blocks);
   };
@@ -1228,7 +1228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int hi = min(lo + 31, p.segs * p.seg_len - 1);
     hi = hi < lo ? lo : hi;
     const int seg_last = hi / p.seg_len;
-    sb = (env_start + seg_first * p.seg_len) & ~(BKEY - 1);
+    sb = (env_start + seg_first * p.seg_len) & ~7;  // 8-key (16 B) aligned: V^T boxes start on the key axis
     const int n_suf = (env_start + (seg_last + 1) * p.seg_len - sb + BKEY - 1) / BKEY;
     nbt = p.n_prefix_blocks + min(n_suf, p.n_blocks - p.n_prefix_blocks);
   };
