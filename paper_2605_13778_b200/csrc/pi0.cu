@@ -130,19 +130,20 @@ struct EmbedParams {
 // blockIdx.y * 256 + t. The embedding weights are read through transposed
 // copies ([D][W], [S][W], made once at sf_ae_create) so every weight load is
 // a coalesced 1 KB warp access, and each is reused for all 16 tokens.
-constexpr int kEmbedTok = 16;
+constexpr int kEmbedTok = 16;  // token rows per CTA (8 for batched rounds, see launch_embed)
 
+template <int TOK>
 __global__ void __launch_bounds__(256) embed_kernel(const EmbedParams p) {
   sm100::pdl_wait();
-  const int m0 = blockIdx.x * kEmbedTok;
-  __shared__ float in[kEmbedTok][65];
-  __shared__ int kind[kEmbedTok];  // 0 padding, 1 state token, 2 action token
-  __shared__ int kbr[kEmbedTok];   // branch of the token
-  __shared__ float red[8][kEmbedTok];
+  const int m0 = blockIdx.x * TOK;
+  __shared__ float in[TOK][65];
+  __shared__ int kind[TOK];  // 0 padding, 1 state token, 2 action token
+  __shared__ int kbr[TOK];   // branch of the token
+  __shared__ float red[8][TOK];
   __shared__ int has_state;
   if (threadIdx.x == 0) has_state = 0;
   __syncthreads();
-  for (int idx = threadIdx.x; idx < kEmbedTok * 64; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < TOK * 64; idx += blockDim.x) {
     const int tk = idx >> 6, c = idx & 63;
     const int m = m0 + tk;
     const int e = m / p.env_rows;
@@ -175,33 +176,33 @@ __global__ void __launch_bounds__(256) embed_kernel(const EmbedParams p) {
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = blockIdx.y * 256 + threadIdx.x;
-  float acc[kEmbedTok];
+  float acc[TOK];
   const float ab = p.a_b[n];
 #pragma unroll
-  for (int tk = 0; tk < kEmbedTok; ++tk) acc[tk] = ab;
+  for (int tk = 0; tk < TOK; ++tk) acc[tk] = ab;
 #pragma unroll 8
   for (int c = 0; c < p.D; ++c) {
     const float w = __ldg(p.a_wt + c * p.W + n);
 #pragma unroll
-    for (int tk = 0; tk < kEmbedTok; ++tk) acc[tk] = fmaf(w, in[tk][c], acc[tk]);
+    for (int tk = 0; tk < TOK; ++tk) acc[tk] = fmaf(w, in[tk][c], acc[tk]);
   }
   if (has_state) {
-    float sacc[kEmbedTok];
+    float sacc[TOK];
     const float sb = p.s_b[n];
 #pragma unroll
-    for (int tk = 0; tk < kEmbedTok; ++tk) sacc[tk] = sb;
+    for (int tk = 0; tk < TOK; ++tk) sacc[tk] = sb;
 #pragma unroll 8
     for (int c = 0; c < p.S; ++c) {
       const float w = __ldg(p.s_wt + c * p.W + n);
 #pragma unroll
-      for (int tk = 0; tk < kEmbedTok; ++tk) sacc[tk] = fmaf(w, in[tk][c], sacc[tk]);
+      for (int tk = 0; tk < TOK; ++tk) sacc[tk] = fmaf(w, in[tk][c], sacc[tk]);
     }
 #pragma unroll
-    for (int tk = 0; tk < kEmbedTok; ++tk)
+    for (int tk = 0; tk < TOK; ++tk)
       if (kind[tk] == 1) acc[tk] = sacc[tk];
   }
 #pragma unroll
-  for (int tk = 0; tk < kEmbedTok; ++tk) {
+  for (int tk = 0; tk < TOK; ++tk) {
     const int m = m0 + tk;
     float v = 0.f;
     if (kind[tk] == 2) v = acc[tk] + p.temb[kbr[tk] * p.W + n];
@@ -214,8 +215,8 @@ __global__ void __launch_bounds__(256) embed_kernel(const EmbedParams p) {
   }
   __syncthreads();
   // per-128-feature-group sum of squares: warps 0-3 cover group 2y, 4-7 group 2y+1
-  if (threadIdx.x < 2 * kEmbedTok) {
-    const int half = threadIdx.x / kEmbedTok, tk = threadIdx.x % kEmbedTok;
+  if (threadIdx.x < 2 * TOK) {
+    const int half = threadIdx.x / TOK, tk = threadIdx.x % TOK;
     const float s = ((red[4 * half][tk] + red[4 * half + 1][tk]) + red[4 * half + 2][tk]) +
                     red[4 * half + 3][tk];
     p.ssq[(size_t)(2 * blockIdx.y + half) * p.ssq_ld + m0 + tk] = s;
@@ -492,6 +493,12 @@ int launch_pdl(void (*kern)(P), dim3 grid, dim3 block, size_t smem, cudaStream_t
   SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
   count_launch();
   return SF_OK;
+}
+
+// 8 token rows per CTA for batched rounds (lighter CTAs: 48 registers, more resident), else 16
+int launch_embed(int M, int W, cudaStream_t s, const EmbedParams& ep, bool pdl) {
+  if (M % 8 == 0 && M >= 148 * 64) return launch_pdl(embed_kernel<8>, dim3(M / 8, W / 256), dim3(256), 0, s, ep, pdl);
+  return launch_pdl(embed_kernel<kEmbedTok>, dim3(M / kEmbedTok, W / 256), dim3(256), 0, s, ep, pdl);
 }
 
 int compute_temb(Handle& h, const float* taus_host, int R, float* out, cudaStream_t s) {
@@ -1258,7 +1265,7 @@ int enqueue_verify(Handle& h, Buffers& b, const sf_verify_cfg_t* cfg, cudaStream
       if ((rc = gemm::launch(b.dops[i], s, pdl))) return rc;
   }
   EmbedParams ep = embed_params(h, b, 0, h.temb);
-  if ((rc = launch_pdl(embed_kernel, dim3(b.M / kEmbedTok, h.cfg.width / 256), dim3(256), 0, s, ep, with_draft && pdl))) return rc;
+  if ((rc = launch_embed(b.M, h.cfg.width, s, ep, with_draft && pdl))) return rc;
   trace_mark(s);
   if ((rc = run_stack(h, b, s, pdl))) return rc;
   VerifyEpiParams vp{};
@@ -1304,7 +1311,7 @@ int enqueue_denoise(Handle& h, Buffers& b, int n_steps, cudaStream_t s, bool pdl
   if ((rc = launch_pdl(status_init_kernel, dim3(1), dim3(256), 0, s, sp, false))) return rc;
   for (int i = 0; i < n_steps; ++i) {
     EmbedParams ep = embed_params(h, b, 1, h.temb_euler + (size_t)i * W);
-    if ((rc = launch_pdl(embed_kernel, dim3(b.M / kEmbedTok, h.cfg.width / 256), dim3(256), 0, s, ep, pdl))) return rc;
+    if ((rc = launch_embed(b.M, h.cfg.width, s, ep, pdl))) return rc;
     if ((rc = run_stack(h, b, s, pdl))) return rc;
     const int total = b.B * h.cfg.horizon * h.cfg.action_dim;
     EulerParams up{b.draft, b.vel, b.B, h.cfg.horizon, h.cfg.action_dim, b.env_rows, n_steps, i,
@@ -1738,7 +1745,7 @@ extern "C" int sf_ae_velocity(void* handle, int n_envs, int rows, const float* x
                                 cudaMemcpyDeviceToDevice, s));
   EmbedParams ep = embed_params(*h, *b, 1, h->temb);
   ep.draft = actions;
-  if ((rc = launch_pdl(embed_kernel, dim3(b->M / kEmbedTok, h->cfg.width / 256), dim3(256), 0, s, ep, false))) return rc;
+  if ((rc = launch_embed(b->M, h->cfg.width, s, ep, false))) return rc;
   if ((rc = run_stack(*h, *b, s, false))) return rc;
   GatherParams gp{b->vel, v_out, n_envs, rows, cf.horizon, cf.action_dim, T_of(*h), b->env_rows};
   gather_vel_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(gp);
