@@ -64,9 +64,10 @@ def test_velocity_matches_oracle_small(k):
 
 
 @pytest.mark.parametrize("n_envs,k", [(1, 4), (3, 2), (6, 4)])
-def test_verify_matches_oracle_small(n_envs, k):
+def test_verify_matches_oracle_small(n_envs, k, check_envs=None):
     """Whole verify chain vs the pinned specflow oracle driven by the pi0 oracle
-    field; n_envs * env_rows > 256 exercises the batched (normal) GEMM path."""
+    field; n_envs * env_rows > 256 exercises the batched (normal) GEMM path.
+    check_envs: the envs compared against the (slow) oracle (default: all)."""
     import torch
 
     from oracle import pi0_oracle as po
@@ -91,7 +92,7 @@ def test_verify_matches_oracle_small(n_envs, k):
     recon, dist = recon.cpu().numpy(), dist.cpu().numpy()
     branch, result = branch.cpu().numpy(), result.cpu().numpy()
     flips = 0
-    for e in range(n_envs):
+    for e in (range(n_envs) if check_envs is None else check_envs):
         kv = po.make_prefix_kv(ocfg, 1, e)
 
         def vel(x, tau):
@@ -111,6 +112,13 @@ def test_verify_matches_oracle_small(n_envs, k):
         assert ("flash_accepted", "flash_rejected_fallback", "flash_phase_fallback")[result[e, 2]] == path
         assert result[e, 3] == planned
     assert flips <= max(1, n_envs // 3)
+
+
+def test_verify_matches_oracle_large_batch():
+    """200 envs (9600 token rows): the batched kernels' large-M paths (2-SM
+    pair attention with one KV split, 8-row embedding CTAs) vs the oracle on a
+    few envs."""
+    test_verify_matches_oracle_small(200, 4, check_envs=(0, 117, 199))
 
 
 @pytest.mark.parametrize("attn", ["pair", "single"])
