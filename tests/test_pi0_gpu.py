@@ -181,6 +181,32 @@ def test_denoise_matches_oracle_small():
     np.testing.assert_allclose(got, want, rtol=2e-2, atol=2e-2 * np.abs(want).max())
 
 
+def test_denoise_matches_oracle_large_batch():
+    """Euler full path over 300 envs (one 16-row query tile per env: the 1-SM
+    persistent attention kernel with one KV split, 8-row embedding CTAs) vs
+    the oracle on a few envs."""
+    import torch
+
+    from oracle import pi0_oracle as po
+    from oracle import specflow_oracle as so
+    from paper_2605_13778_b200 import pi0
+
+    ocfg, dcfg = _pair()
+    E = 300
+    w = po.make_weights(ocfg, 0)
+    ae = pi0.ActionExpert(dcfg, seed=0, n_envs=E, kv_seed=1)
+    rng = np.random.default_rng(4)
+    start = rng.standard_normal((E, dcfg.horizon, dcfg.action_dim)).astype(np.float32)
+    state = rng.standard_normal((E, dcfg.state_dim)).astype(np.float32)
+    chunk, status = ae.denoise_batch(torch.from_numpy(start).cuda(), torch.from_numpy(state).cuda(), 4)
+    chunk = chunk.cpu().numpy()
+    for e in (0, 151, 299):
+        kv = po.make_prefix_kv(ocfg, 1, e)
+        want = so.integrate_flow(
+            lambda x, t: po.field_velocity(ocfg, w, kv, [(x.astype(np.float32), t)], state[e])[0], start[e], 4)
+        np.testing.assert_allclose(chunk[e], want, rtol=2e-2, atol=2e-2 * np.abs(want).max())
+
+
 def test_graph_pdl_matches_eager_and_is_deterministic():
     import torch
 
