@@ -116,12 +116,15 @@ def embed_tokens(cfg, w, actions, tau, state):
     return x
 
 
-def field_velocity(cfg, w, kv, branches, state):
+def field_velocity(cfg, w, kv, branches, state, bf16_points=True):
     """Velocity for several branches that share the prefix KV.
 
     branches: list of (actions [H, D], tau); kv: (K [L][P, 256], Vt [L][256, P])
     bf16-valued float32 arrays. Returns v [len(branches), H, D] float32.
+    bf16_points=False is the unrounded fp32 model: same (bf16-valued) weights
+    and prefix KV, activations never rounded (the north-star fp32 reference).
     """
+    bf16 = globals()["bf16"] if bf16_points else (lambda a: np.asarray(a, np.float32))
     cs = rope_table(cfg, cfg.prefix_len + cfg.seg_len)
     kp, vtp = kv
     P = cfg.prefix_len

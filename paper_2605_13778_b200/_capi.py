@@ -17,6 +17,7 @@ SF_OK, SF_EINVAL, SF_ENONFINITE, SF_ERUNTIME, SF_ECUDA = 0, 1, 2, 3, 4
 SF_F32, SF_F64 = 0, 1
 SF_MAX_LAYERS = 8
 SF_MAX_K = 16
+TINY_MAX_K = 8  # branch rows of one fused tiny-field launch (csrc/tiny.cu kMaxRows)
 SF_METRIC = {"l2": 0, "linf": 1}
 SF_RESULT_WORDS = 8
 RES_PREFIX, RES_SWITCH, RES_PATH, RES_PLANNED, RES_NONFINITE = 0, 1, 2, 3, 4

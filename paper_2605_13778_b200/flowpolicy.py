@@ -238,6 +238,12 @@ def integrate_flow(field, cache: ConditioningCache, state, cfg: DenoiseConfig,
     if hasattr(field, "device_denoise"):
         return field.device_denoise(cache, state, start, n)
     if isinstance(field, VelocityField):
+        emb = np.asarray(cache.embedding, np.float64)
+        st_in = np.asarray(state, np.float64)
+        if emb.size != field.emb_dim or st_in.size != field.state_dim:
+            # the reference's nets.forward rejects the mis-sized pack (nets.py:94-99)
+            n_in = field.horizon * field.dim + 1 + emb.size + st_in.size
+            raise ValueError(f"input has shape ({n_in},), expected ({field.net.in_dim},)")
         field.eval_count += n
         out, _, st = _run_full(None, cache.embedding if cache.embedding.size else np.zeros(0),
                                field.emb_dim, field.net, np.asarray(state, np.float64), start,

@@ -137,7 +137,8 @@ class ActionExpert:
 
     def __init__(self, cfg: AEConfig = PI0, seed: int = 0, n_envs: int = 1, kv_seed: int = 1,
                  layout: ChannelLayout | None = None, std: float = 0.02,
-                 flags: int = SF_AE_GRAPH | SF_AE_PDL, env_offset: int = 0):
+                 flags: int = SF_AE_GRAPH | SF_AE_PDL, env_offset: int = 0,
+                 draft_gripper_bias: float = 0.0):
         self.cfg = cfg
         self.horizon = cfg.horizon
         self.dim = cfg.action_dim
@@ -197,7 +198,13 @@ class ActionExpert:
             shapes = ((hid, cfg.draft_in), (hid, hid), (hdd, hid))
             for i, shp in enumerate(shapes):
                 w.draft_w[i] = mk(shp, b16, TID_DRAFT_BASE + i, float(np.sqrt(1.0 / shp[1]))).data_ptr()
-                w.draft_b[i] = zeros(shp[0]).data_ptr()
+                bias = zeros(shp[0])
+                if i == 2 and draft_gripper_bias:
+                    # one-signed gripper column (last channel of every row): a
+                    # draft that holds the gripper state, so phase fallbacks come
+                    # from the current sign, not from random draft signs
+                    bias.view(cfg.horizon, cfg.action_dim)[:, -1] = draft_gripper_bias
+                w.draft_b[i] = bias.data_ptr()
         c = _AeConfigC(cfg.width, cfg.layers, cfg.q_heads, cfg.head_dim, cfg.mlp, cfg.action_dim,
                        cfg.state_dim, cfg.horizon, cfg.prefix_len, cfg.eps, cfg.temb_min_period,
                        cfg.temb_max_period, cfg.draft_in, cfg.draft_hidden)

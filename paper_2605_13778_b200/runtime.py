@@ -19,6 +19,7 @@ from .actions import ActionChunk, ChannelLayout, Standardizer, gripper_switch
 from .draft import DraftModel, propose
 from .flowpolicy import (ConditioningCache, ContextEncoder, DenoiseConfig, VelocityField, denoise,
                          encode_context, _run_full)
+from . import _capi
 from .actions import STANDARDIZED
 from .verifier import VerifierConfig, VerifierReport, tiny_flash_round, verify
 
@@ -161,7 +162,7 @@ def flash_attempt(obs, models: Models, policy: RuntimePolicy, state: RunnerState
     rng = np.random.default_rng(seed)
     field = models.field
     norm_state = models.norm_state(obs.robot_state)
-    if isinstance(field, VelocityField):
+    if isinstance(field, VelocityField) and len(policy.verifier_cfg.timesteps) <= _capi.TINY_MAX_K:
         draft = models.draft
         feats = draft.features(obs)
         eps = rng.standard_normal((draft.horizon, draft.layout.dim))

@@ -8,9 +8,9 @@ Mirrors:
     ``read_trace``                           bench/reports.py:96-114
   * ``episode_stats``                        bench/metrics.py:45-75
 
-``records_from_device`` turns the device decision words of a batched flash
-round (``ActionExpert.flash_batch`` / ``sf_ae_flash_round``: prefix L, switch,
-path code, planned) into per-env records, so batched GPU runs produce the same
+``records_from_device`` turns a batched replanning round
+(``BatchedReplanner.round``: post-bookkeeping path codes and planned prefixes,
+plus the flash attempt's prefix / branch / switch words) into per-env records, so batched GPU runs produce the same
 trace schema as the reference's sequential episode loop.
 """
 
@@ -24,7 +24,7 @@ from typing import Iterable, Mapping, Sequence
 import numpy as np
 
 from ._capi import (SF_PATH_FLASH_ACCEPTED, SF_PATH_FLASH_PHASE, SF_PATH_FLASH_REJECTED,
-                    SF_RES_PATH, SF_RES_PLANNED, SF_RES_PREFIX, SF_RES_SWITCH)
+                    SF_PATH_FULL, SF_PATH_PERIODIC, SF_RES_PREFIX, SF_RES_SWITCH)
 from .runtime import (PATH_FLASH_ACCEPTED, PATH_FLASH_PHASE, PATH_FLASH_REJECTED, PATH_FULL,
                       PATH_PERIODIC)
 
@@ -32,6 +32,8 @@ _DEVICE_PATH = {
     SF_PATH_FLASH_ACCEPTED: PATH_FLASH_ACCEPTED,
     SF_PATH_FLASH_REJECTED: PATH_FLASH_REJECTED,
     SF_PATH_FLASH_PHASE: PATH_FLASH_PHASE,
+    SF_PATH_FULL: PATH_FULL,
+    SF_PATH_PERIODIC: PATH_PERIODIC,
 }
 
 
@@ -135,31 +137,48 @@ def episode_stats(records: Sequence[Mapping], success: bool, replan_size: int,
                         speedup=baseline_full_ms / lat if lat > 0 else float("nan"))
 
 
-def records_from_device(result: np.ndarray, branch: np.ndarray | None, round_index: int,
-                        latency_ms: float, start_ticks: Sequence[int] | None = None,
+def records_from_device(path: np.ndarray, planned: np.ndarray, result: np.ndarray,
+                        branch: np.ndarray | None, round_index: int, latency_ms: float,
+                        start_ticks: Sequence[int] | None = None,
                         verify_seeds: Sequence[int] | None = None,
-                        cache_rounds: Sequence[int] | None = None) -> list[RoundRecord]:
-    """Per-env records of one batched flash round from the device decision
-    words ``result [B, 8]`` (and branch prefixes ``[B, K]``). ``executed`` is
-    the planned prefix (the conveyor stepping that would clip it is out of
-    scope); fallback rounds carry the path label and ``planned = replan_size``
-    as the reference does before its full round (runtime.py:289-309)."""
-    result = np.asarray(result)
+                        cache_rounds: Sequence[int] | None = None,
+                        switch_in_executed: np.ndarray | None = None) -> list[RoundRecord]:
+    """Per-env records of one batched replanning round.
+
+    ``path`` / ``planned`` [B] are the round's POST-bookkeeping values
+    (``BatchedReplanner.round``: ``sf_replan_update``), so full rounds (no
+    context yet) and periodic refreshes get their own labels and planned =
+    replan_size, exactly as ``run_episode`` records them (runtime.py:262-276).
+    ``result [B, 8]`` / ``branch [B, K]`` are the flash attempt's decision
+    words; as in the reference they are recorded only for rounds that made a
+    flash attempt (accepted and both fallbacks, runtime.py:279-282).
+    ``executed`` = planned for every path (the conveyor stepping that could
+    clip it at episode end is out of scope; runtime.py:325-326).
+    ``switch_in_executed`` [B] (optional, ``BatchedReplanner``'s device
+    flag) is recorded for accepted rounds only (runtime.py:321-323)."""
+    path, planned, result = np.asarray(path), np.asarray(planned), np.asarray(result)
     recs = []
-    for e in range(result.shape[0]):
+    for e in range(path.shape[0]):
+        code = int(path[e])
+        label = _DEVICE_PATH.get(code)
+        if label is None:
+            raise ValueError(f"env {e}: unknown device path code {code}")
+        flash = code in (SF_PATH_FLASH_ACCEPTED, SF_PATH_FLASH_REJECTED, SF_PATH_FLASH_PHASE)
         w = result[e]
-        path = _DEVICE_PATH.get(int(w[SF_RES_PATH]))
-        if path is None:
-            raise ValueError(f"env {e}: unknown device path code {int(w[SF_RES_PATH])}")
-        planned = int(w[SF_RES_PLANNED])
+        sie = None
+        if code == SF_PATH_FLASH_ACCEPTED and switch_in_executed is not None:
+            sie = bool(switch_in_executed[e])
         recs.append(RoundRecord(
-            index=round_index, path=path, executed=planned if path == PATH_FLASH_ACCEPTED else 0,
-            latency_ms=float(latency_ms), start_tick=int(start_ticks[e]) if start_ticks is not None else 0,
-            stall_ticks=0, planned=planned, prefix=int(w[SF_RES_PREFIX]),
-            branch_prefixes=tuple(int(x) for x in branch[e]) if branch is not None else None,
-            gripper_switch=bool(w[SF_RES_SWITCH]),
-            cache_round=int(cache_rounds[e]) if cache_rounds is not None else None,
-            verify_seed=int(verify_seeds[e]) if verify_seeds is not None else None))
+            index=round_index, path=label, executed=int(planned[e]), latency_ms=float(latency_ms),
+            start_tick=int(start_ticks[e]) if start_ticks is not None else 0, stall_ticks=0,
+            planned=int(planned[e]),
+            prefix=int(w[SF_RES_PREFIX]) if flash else None,
+            branch_prefixes=(tuple(int(x) for x in branch[e]) if flash and branch is not None
+                             else None),
+            gripper_switch=bool(w[SF_RES_SWITCH]) if flash else None,
+            switch_in_executed=sie,
+            cache_round=int(cache_rounds[e]) if flash and cache_rounds is not None else None,
+            verify_seed=int(verify_seeds[e]) if flash and verify_seeds is not None else None))
     return recs
 
 

@@ -160,6 +160,24 @@ def _report(recon, dist, branch, res, seed) -> VerifierReport:
         planned=int(res[_capi.RES_PLANNED]))
 
 
+def _check_tiny_inputs(field: VelocityField, draft_net, din, eps, emb, st) -> None:
+    """The fused kernel packs its inputs back to back, so every size is checked
+    before the launch with the reference's exceptions (flowpolicy.py:253-257
+    ``velocity``; nets.py:94-99 ``forward`` for a mis-sized pack or draft
+    feature vector)."""
+    h, d = field.horizon, field.dim
+    if draft_net is None:
+        if din.shape != (h, d):
+            raise ValueError(f"chunk shape {din.shape} does not match field")
+    elif din.size != draft_net.in_dim:
+        raise ValueError(f"input has shape {din.shape}, expected ({draft_net.in_dim},)")
+    if eps.shape != (h, d):
+        raise ValueError("draft and noise shapes differ")
+    if emb.size != field.emb_dim or st.size != field.state_dim:
+        n = h * d + 1 + emb.size + st.size
+        raise ValueError(f"input has shape ({n},), expected ({field.net.in_dim},)")
+
+
 def tiny_flash_round(field: VelocityField, draft_net, draft_in, cache: ConditioningCache, state,
                      eps, cfg: VerifierConfig, current_sign: float, layout, seed=None,
                      phase_fallback=True, prefix_cap=True, replan_size=12):
@@ -168,11 +186,13 @@ def tiny_flash_round(field: VelocityField, draft_net, draft_in, cache: Condition
     Returns (draft values, VerifierReport)."""
     h, d = field.horizon, field.dim
     k = len(cfg.timesteps)
-    emb = cache.embedding
+    emb = np.asarray(cache.embedding, dtype=np.float64)
     st = np.asarray(state, dtype=np.float64)
+    din = np.asarray(draft_in, dtype=np.float64)
+    eps = np.asarray(eps, dtype=np.float64)
+    _check_tiny_inputs(field, draft_net, din, eps, emb, st)
     n_out = h * d + k * h * d + k * h
     n_words = _capi.SF_RESULT_WORDS + k
-    din = np.asarray(draft_in, dtype=np.float64)
     stg = _device.Staging.get("flash", din.size + eps.size + emb.size + st.size + 3, n_out, n_words)
     p_draft, p_eps, p_emb, p_state = stg.upload([din, eps, emb, st])
     out = _capi.SfVerifyOut(stg.out_ptr(0), stg.out_ptr(h * d), stg.out_ptr(h * d + k * h * d),
@@ -222,13 +242,14 @@ def verify(field, draft: ActionChunk, cache: ConditioningCache, state, cfg: Veri
     if hasattr(field, "device_verify"):
         field.eval_count += k
         return field.device_verify(draft, cache, state, cfg, eps, current_gripper_sign, noise_seed)
-    if isinstance(field, VelocityField):
+    if isinstance(field, VelocityField) and k <= _capi.TINY_MAX_K:
         field.eval_count += k
         _, rep = tiny_flash_round(field, None, draft.values, cache, state, eps, cfg,
                                   current_gripper_sign, draft.layout, noise_seed)
         return rep
-    # generic field protocol: device interpolation, field evaluated where it
-    # lives (branch by branch, as the reference schedules them), device epilogue
+    # generic field protocol (and MLP fields with K > TINY_MAX_K): device
+    # interpolation, field evaluated where it lives (branch by branch, as the
+    # reference schedules them), device epilogue
     vals = draft.values
     xs = np.empty((k,) + vals.shape)
     da, de = _device.to_dev(vals), _device.to_dev(eps)

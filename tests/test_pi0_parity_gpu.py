@@ -1,0 +1,276 @@
+"""Full-size pi0-scale parity (cfg3 batch 1 and the cfg4 batched path) against
+the vectorised torch oracle (oracle/pi0_torch.py, pinned to the numpy oracle
+by tests/test_oracle_torch_cpu.py) driving the reference's verify / decision
+restatement (oracle/specflow_oracle.py, pinned to the reference's goldens).
+
+Workload (SURVEY §7 hard part 5 / VERDICT r1 item 1): seeded rounds with a
+one-signed draft gripper column (+20) and alternating current gripper sign,
+so phase fallbacks come from the sign flip; delta per round at the 25/50/75 %
+quantiles of the deciding distance (max over branches of the first row), so
+accepted, rejected and phase-fallback rounds all occur.
+
+Checks:
+  * endpoints (recon) vs the UNROUNDED fp32 model, element-wise: the north
+    star asks rtol 1e-2 for bf16 activations / fp32 accumulation; the test
+    asserts rtol 1e-2 on every element of typical magnitude (|ref| >= rms)
+    and |dev - ref| <= 2e-2 rms on all elements (near-zero elements cannot
+    meet a pure rtol in any bf16 implementation), and reports the measured
+    bound next to the bf16-mirroring oracle's own distance from fp32;
+  * branch prefixes / switch / path / planned vs the bf16-MIRRORING oracle,
+    identical except rounds whose deciding distance lies within the measured
+    numerical band of delta; flips are counted with their margins and written
+    to $SF_PARITY_OUT (JSON) when set.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs CUDA")]
+
+TAUS = (0.2, 0.4, 0.6, 0.8)
+WINDOW = 24
+GRIP = 20.0
+_REPORT = {}
+
+
+def _report(key, value):
+    _REPORT[key] = value
+    path = os.environ.get("SF_PARITY_OUT")
+    if path:
+        with open(path, "w") as f:
+            json.dump(_REPORT, f, indent=1, sort_keys=True)
+    print(f"[parity] {key}: {json.dumps(value)}")
+
+
+@pytest.fixture(scope="module")
+def models():
+    import torch
+
+    from oracle import pi0_oracle as po
+    from oracle import pi0_torch as pt
+    from paper_2605_13778_b200 import pi0
+
+    n_env = 64
+    ae = pi0.ActionExpert(pi0.PI0, seed=0, n_envs=n_env, kv_seed=1)
+    ref = pt.Pi0Torch(po.AEConfig(), seed=0, kv_seed=1, env_ids=range(n_env), device="cuda")
+    torch.cuda.synchronize()
+    return ae, ref
+
+
+def _inputs(n, seed, H=50, D=32, S=32):
+    rng = np.random.default_rng(seed)
+    draft = rng.standard_normal((n, H, D)).astype(np.float32)
+    draft[:, :, -1] = GRIP                           # one-signed gripper column
+    eps = rng.standard_normal((n, H, D)).astype(np.float32)
+    state = rng.standard_normal((n, S)).astype(np.float32)
+    signs = np.where(np.arange(n) % 2 == 0, 1.0, -1.0).astype(np.float32)  # odd: phase fallback
+    return draft, eps, state, signs
+
+
+def _oracle_velocities(ref, draft, eps, state, env_index, mirror):
+    """v at the K interpolated states of every round: [n, K, H, D] (float64)."""
+    import torch
+
+    from oracle import specflow_oracle as so
+
+    n = draft.shape[0]
+    xs = np.stack([[so.interpolate(draft[i].astype(np.float64), eps[i].astype(np.float64), t)
+                    for t in TAUS] for i in range(n)]).astype(np.float32)
+    out = []
+    for c in range(0, n, 16):
+        v = ref.velocity(torch.from_numpy(xs[c:c + 16]).cuda(), TAUS,
+                         torch.from_numpy(state[c:c + 16]).cuda(), mirror_bf16=mirror,
+                         env_index=env_index[c:c + 16])
+        out.append(v.double().cpu().numpy())
+    return np.concatenate(out)
+
+
+def _oracle_verify(v, draft, eps, delta, sign):
+    from oracle import specflow_oracle as so
+
+    lut = {t: v[k] for k, t in enumerate(TAUS)}
+    return so.verify(lambda x, t: lut[t], draft.astype(np.float64), eps.astype(np.float64), TAUS, delta,
+                     draft.shape[1] - 1, "l2", WINDOW, float(sign))
+
+
+def _deltas(v, draft, eps, signs):
+    """delta per round at the 25/50/75 % quantiles of the deciding distance."""
+    from oracle import specflow_oracle as so
+
+    n = draft.shape[0]
+    m = np.array([_oracle_verify(v[i], draft[i], eps[i], 0.0, signs[i])["distances"][:, 0].max()
+                  for i in range(n)])
+    q = np.quantile(m[signs > 0], [0.25, 0.5, 0.75])
+    return np.array([q[(i // 2) % 3] for i in range(n)])
+
+
+def _margin(dist, branch, delta, H):
+    """Distance of the decision-relevant rows (each branch's accepted rows and
+    the first rejected one) to delta."""
+    rows = [dist[k, : min(branch[k] + 1, H)] for k in range(dist.shape[0])]
+    return float(np.abs(np.concatenate(rows) - delta).min())
+
+
+def _compare(tag, recon, dist, branch, result, draft, eps, signs, deltas, v32, vmir):
+    from oracle import specflow_oracle as so
+
+    n, H = draft.shape[0], draft.shape[1]
+    errs, refs, merrs = [], [], []
+    flips, near, paths = [], 0, [0, 0, 0]
+    dist_err = 0.0
+    for i in range(n):
+        r32 = _oracle_verify(v32[i], draft[i], eps[i], deltas[i], signs[i])
+        rm = _oracle_verify(vmir[i], draft[i], eps[i], deltas[i], signs[i])
+        errs.append(recon[i] - r32["reconstructed"])
+        refs.append(r32["reconstructed"])
+        merrs.append(rm["reconstructed"] - r32["reconstructed"])
+        dist_err = max(dist_err, float(np.abs(dist[i] - rm["distances"]).max()))
+        path, planned = so.fallback_decision(rm["prefix"], rm["gripper_switch_detected"], H)
+        code = ("flash_accepted", "flash_rejected_fallback", "flash_phase_fallback").index(path)
+        paths[code] += 1
+        same = (tuple(int(x) for x in branch[i]) == rm["branch_prefixes"]
+                and bool(result[i, 1]) == rm["gripper_switch_detected"]
+                and int(result[i, 2]) == code and int(result[i, 3]) == planned)
+        m = _margin(rm["distances"], rm["branch_prefixes"], deltas[i], H)
+        if m < 1e-4:
+            near += 1
+        if not same:
+            flips.append({"round": i, "margin": m, "dev_branch": [int(x) for x in branch[i]],
+                          "oracle_branch": list(rm["branch_prefixes"])})
+    err, ref, merr = np.stack(errs), np.stack(refs), np.stack(merrs)
+    rms = float(np.sqrt((ref ** 2).mean()))
+    rel = np.abs(err) / np.maximum(np.abs(ref), 1e-30)
+    big = np.abs(ref) >= 0.1 * rms
+    typical = np.abs(ref) >= rms
+    stats = {
+        "rounds": n, "paths_oracle": {"accepted": paths[0], "rejected": paths[1], "phase": paths[2]},
+        "recon_vs_fp32": {
+            "max_abs_err": float(np.abs(err).max()), "max_abs_ref": float(np.abs(ref).max()),
+            "rms_ref": rms, "max_err_over_rms": float(np.abs(err).max() / rms),
+            "frac_within_pure_rtol_1e-2": float((rel <= 1e-2).mean()),
+            "rel_err_p99_where_ref_ge_0.1rms": float(np.quantile(rel[big], 0.99)),
+            "rel_err_p999_where_ref_ge_0.1rms": float(np.quantile(rel[big], 0.999)),
+            "max_rel_err_where_ref_ge_rms": float(rel[typical].max()),
+        },
+        # the intrinsic bf16-activation floor: the bf16-mirroring oracle vs fp32
+        "mirror_oracle_vs_fp32": {
+            "max_err_over_rms": float(np.abs(merr).max() / rms),
+            "max_rel_err_where_ref_ge_rms": float((np.abs(merr) / np.abs(ref))[typical].max()),
+        },
+        "dist_vs_bf16_oracle_max_abs": dist_err,
+        "decision_flips": len(flips), "flip_detail": flips,
+        "rounds_within_1e-4_of_delta": near,
+        "max_flip_margin": max([f["margin"] for f in flips], default=0.0),
+    }
+    _report(tag, stats)
+    # north-star endpoint bound (bf16 activations, fp32 accumulation): rtol
+    # 1e-2 element-wise on elements of typical magnitude (|ref| >= rms), and
+    # every element within 2e-2 rms (elements near zero cannot meet a pure rtol
+    # in ANY bf16 implementation: the mirroring oracle's own floor is reported)
+    assert rel[typical].max() <= 1e-2, stats["recon_vs_fp32"]
+    assert np.abs(err).max() <= 2e-2 * rms, stats["recon_vs_fp32"]
+    assert all(p > 0 for p in paths), stats["paths_oracle"]
+    # decisions: identical except rounds inside the numerical band of delta
+    band = max(2.0 * dist_err, 1e-4)
+    assert all(f["margin"] < band for f in flips), (band, flips)
+    assert len(flips) <= max(1, n // 16), flips
+    return stats
+
+
+def test_cfg3_batch1_64_rounds(models):
+    """cfg3 (18 layers, width 1024, P = 800, K = 4, H = 50, D = 32) at batch 1:
+    the swap-AB / split-KV kernels the single-robot latency path runs."""
+    import torch
+
+    from paper_2605_13778_b200.verifier import VerifierConfig
+
+    ae, ref = models
+    n = 64
+    draft, eps, state, signs = _inputs(n, 100)
+    env_index = [0] * n
+    vmir = _oracle_velocities(ref, draft, eps, state, env_index, True)
+    v32 = _oracle_velocities(ref, draft, eps, state, env_index, False)
+    deltas = _deltas(vmir, draft, eps, signs)
+    recon = np.empty((n, len(TAUS), 50, 32))
+    dist = np.empty((n, len(TAUS), 50))
+    branch = np.empty((n, len(TAUS)), np.int64)
+    result = np.empty((n, 8), np.int64)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    for i in range(n):
+        cfg = VerifierConfig(timesteps=TAUS, delta=float(deltas[i]), gripper_window=WINDOW)
+        r, d, b, res = ae.verify_batch(cfg, t(draft[i:i + 1]), t(eps[i:i + 1]), t(state[i:i + 1]),
+                                       t(signs[i:i + 1]))
+        recon[i], dist[i] = r[0].double().cpu().numpy(), d[0].double().cpu().numpy()
+        branch[i], result[i] = b[0].cpu().numpy(), res[0].cpu().numpy()
+    _compare("cfg3_batch1", recon, dist, branch, result, draft, eps, signs, deltas, v32, vmir)
+
+
+def test_cfg4_batched_64_envs(models):
+    """The cfg4 batched path (2-SM pair GEMMs / attention) at full size: 64
+    envs, each attending to its own prefix KV, one batched verify per delta
+    quantile."""
+    import torch
+
+    from paper_2605_13778_b200.verifier import VerifierConfig
+
+    ae, ref = models
+    n = 64
+    draft, eps, state, signs = _inputs(n, 200)
+    env_index = list(range(n))
+    vmir = _oracle_velocities(ref, draft, eps, state, env_index, True)
+    v32 = _oracle_velocities(ref, draft, eps, state, env_index, False)
+    deltas = _deltas(vmir, draft, eps, signs)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    recon = np.empty((n, len(TAUS), 50, 32))
+    dist = np.empty((n, len(TAUS), 50))
+    branch = np.empty((n, len(TAUS)), np.int64)
+    result = np.empty((n, 8), np.int64)
+    for qd in np.unique(deltas):
+        cfg = VerifierConfig(timesteps=TAUS, delta=float(qd), gripper_window=WINDOW)
+        r, d, b, res = ae.verify_batch(cfg, t(draft), t(eps), t(state), t(signs))
+        sel = deltas == qd
+        recon[sel], dist[sel] = r.double().cpu().numpy()[sel], d.double().cpu().numpy()[sel]
+        branch[sel], result[sel] = b.cpu().numpy()[sel], res.cpu().numpy()[sel]
+    _compare("cfg4_batched", recon, dist, branch, result, draft, eps, signs, deltas, v32, vmir)
+
+
+def test_full_size_euler_vs_oracle(models):
+    """cfg3 full path: 10-step Euler (tau_i = i/10, A += v/10) at full size,
+    batch 1 and a 16-env batch, vs the fp32 and bf16-mirroring oracles."""
+    import torch
+
+    from oracle import specflow_oracle as so
+
+    ae, ref = models
+    for n in (1, 16):
+        rng = np.random.default_rng(300 + n)
+        start = rng.standard_normal((n, 50, 32)).astype(np.float32)
+        state = rng.standard_normal((n, 32)).astype(np.float32)
+        chunk, status = ae.denoise_batch(torch.from_numpy(start).cuda(), torch.from_numpy(state).cuda(), 10)
+        got = chunk.double().cpu().numpy()
+        assert (status[:, 0] == -1).all()
+        res = {}
+        for mirror in (False, True):
+            want = np.stack([so.integrate_flow(
+                lambda x, tau, e=e: ref.velocity(
+                    torch.from_numpy(x.astype(np.float32))[None, None].cuda(), (tau,),
+                    torch.from_numpy(state[e:e + 1]).cuda(), mirror_bf16=mirror,
+                    env_index=[e])[0, 0].double().cpu().numpy(), start[e], 10) for e in range(n)])
+            err = np.abs(got - want)
+            res["fp32" if not mirror else "bf16_mirror"] = {
+                "max_abs_err": float(err.max()), "max_abs_ref": float(np.abs(want).max()),
+                "rel_norm_err": float(np.linalg.norm(got - want) / np.linalg.norm(want))}
+            if not mirror:
+                rms = float(np.sqrt((want ** 2).mean()))
+                typical = np.abs(want) >= rms
+                res["fp32"]["max_rel_err_where_ref_ge_rms"] = float((err / np.abs(want))[typical].max())
+                res["fp32"]["max_err_over_rms"] = float(err.max() / rms)
+                assert (err / np.abs(want))[typical].max() <= 1e-2 and err.max() <= 2e-2 * rms, res
+        _report(f"euler_full_size_b{n}", res)
