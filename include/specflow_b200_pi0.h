@@ -23,6 +23,10 @@ extern "C" {
 
 #define SF_AE_GRAPH 1 /* capture/replay the round as a CUDA graph */
 #define SF_AE_PDL 2   /* programmatic dependent launch between kernels */
+#define SF_AE_FP32 4  /* fp32 mode: the layer stack + head of sf_ae_verify / sf_ae_denoise*
+                         in fp32 activations with fp32 FMA accumulation (CUDA cores), the
+                         north star's "1e-5 in an fp32 mode" parity mode (~10 ms / verify);
+                         weights and prefix KV stay the model's bf16 values */
 
 typedef struct {
   int width;       /* 1024 */
@@ -114,6 +118,46 @@ int sf_ae_denoise(void* handle, int n_envs, int num_steps, const float* start, c
  * (sf_replan_update). */
 int sf_ae_denoise_envs(void* handle, int n_envs, const int* env_map, int num_steps, const float* start,
                        const float* state, float* chunk_out, int* status, int flags, void* stream);
+
+/* ---- one batched replanning round on the device (run_episode, runtime.py:238-326) ----
+ * ONE CUDA graph per (n_envs, verify cfg, policy): the speculative attempt for
+ * every env (sf_ae_flash_round), the round bookkeeping (sf_replan_update:
+ * periodic refresh, prefix cap, fallback compaction), then a device-selected
+ * branch of a graph SWITCH node runs the N-step Euler full path on the
+ * smallest pre-captured bucket that holds the fallback envs (buckets: powers
+ * of two up to 64, then multiples of 64), gathers / scatters the compacted
+ * rows on the device, and a final kernel marks non-finite chunks, computes
+ * switch_in_executed for accepted rounds and destandardizes the chunk. No
+ * host synchronisation inside the round. */
+typedef struct {
+  int mode_flash;        /* RuntimePolicy.mode == flash (0: every round is a full round) */
+  int periodic_refresh;  /* PF (runtime.py:247-250) */
+  int num_steps;         /* Euler steps of the full path (DenoiseConfig.num_steps) */
+  const float* std_mean; /* [D] Standardizer mean / std (actions.py:139-144) for chunk_raw; */
+  const float* std_std;  /* NULL: chunk_raw is not written */
+} sf_replan_policy_t;
+
+typedef struct {
+  float* chunk;              /* [n][H][D] standardized chunk to execute (draft or full path) */
+  float* chunk_raw;          /* [n][H][D] destandardize(chunk) (may be NULL) */
+  int* path;                 /* [n] SF_PATH_* of the round */
+  int* planned;              /* [n] actions to execute; 0 when the chunk is non-finite */
+  int* switch_in_executed;   /* [n] accepted rounds: gripper switch in chunk[:planned] against the
+                                env's current sign (runtime.py:321-323); 0 otherwise */
+  int* nonfinite;            /* [n] 1: the chunk is non-finite (the reference raises
+                                FloatingPointError, flowpolicy.py:290 / verifier.py:89) */
+  int* branch_prefixes;      /* [n][K] of the flash attempt (may be NULL) */
+  int* result;               /* [n][SF_RESULT_WORDS] of the flash attempt (may be NULL) */
+  int* n_fallback;           /* [1] envs that ran the full path (may be NULL) */
+} sf_replan_out_t;
+
+/* obs [n][draft_in], eps_verify / eps_denoise [n][H][D], state [n][S], signs [n]
+ * (current gripper sign per env) f32; fsr / has_cache [n] int32 runner state
+ * (in/out, flash_since_refresh and "has a cached context"). */
+int sf_ae_replan_round(void* handle, int n_envs, const sf_verify_cfg_t* cfg,
+                       const sf_replan_policy_t* policy, const float* obs, const float* eps_verify,
+                       const float* eps_denoise, const float* state, const float* signs, int* fsr,
+                       int* has_cache, const sf_replan_out_t* out, int flags, void* stream);
 
 /* Field protocol: velocities for n_envs x rows states x [..][rows][H][D] at
  * taus[rows] (HOST). */

@@ -62,6 +62,17 @@ class SfVerifyOut(ctypes.Structure):
     ]
 
 
+class SfReplanPolicy(ctypes.Structure):
+    _fields_ = [("mode_flash", ctypes.c_int), ("periodic_refresh", ctypes.c_int),
+                ("num_steps", ctypes.c_int), ("std_mean", ctypes.c_void_p), ("std_std", ctypes.c_void_p)]
+
+
+class SfReplanOut(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("chunk", "chunk_raw", "path", "planned",
+                                               "switch_in_executed", "nonfinite", "branch_prefixes",
+                                               "result", "n_fallback")]
+
+
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _D = ctypes.c_double
@@ -103,6 +114,8 @@ SIGNATURES = {
     "sf_ae_time_op": (_I, [_P, _I, _I, _I, _I, _P]),
     "sf_ae_profile_verify": (_I, [_P, _I, ctypes.POINTER(SfVerifyCfg), _P, _P, _P, _P, _I, _P, _P]),
     "sf_ae_velocity": (_I, [_P, _I, _I, _P, _P, _P, _P, _P]),
+    "sf_ae_replan_round": (_I, [_P, _I, ctypes.POINTER(SfVerifyCfg), ctypes.POINTER(SfReplanPolicy), _P, _P,
+                                _P, _P, _P, _P, _P, ctypes.POINTER(SfReplanOut), _I, _P]),
     "sf_fill_hash_uniform": (_I, [_P, _I, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64,
                                   ctypes.c_double, _P]),
     # include/specflow_b200_internal.h (kernel unit-test hooks)

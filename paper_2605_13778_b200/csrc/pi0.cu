@@ -30,6 +30,8 @@
 #include "common.cuh"
 #include "gemm_host.h"
 #include "stack.cuh"
+#include "stack_f32.cuh"
+#include "replan.cuh"
 #include "specflow_b200_pi0.h"
 #include "verify_epi.cuh"
 
@@ -395,6 +397,132 @@ __global__ void gather_vel_kernel(const GatherParams p) {
   }
 }
 
+// ------------------------------------------------- batched replanning round
+
+constexpr int kMaxBuckets = 32;
+
+struct ReplanSelectParams {
+  int n;
+  const int* result;
+  int* fsr;
+  int* has_cache;
+  int mode_flash, pf, r;
+  int* path;
+  int* planned;
+  int* fb_idx;
+  int* fb_count;
+  int n_buckets;
+  int bucket[kMaxBuckets];
+  cudaGraphConditionalHandle cond;
+};
+
+// round bookkeeping + compaction (replan.cuh), then the SWITCH value: the
+// smallest pre-captured Euler bucket that holds the fallback envs (n_buckets
+// = no full path this round)
+__global__ void __launch_bounds__(1024) replan_select_kernel(const ReplanSelectParams p) {
+  const int cnt = replan_update_cta(p.n, p.result, p.fsr, p.has_cache, p.mode_flash, p.pf, p.r, p.path,
+                                    p.planned, p.fb_idx);
+  if (threadIdx.x == 0) {
+    *p.fb_count = cnt;
+    unsigned sel = (unsigned)p.n_buckets;
+    for (int i = 0; i < p.n_buckets && cnt > 0; ++i)
+      if (cnt <= p.bucket[i]) {
+        sel = (unsigned)i;
+        break;
+      }
+    cudaGraphSetConditional(p.cond, sel);
+  }
+}
+
+// chunk <- draft for every env (accepted envs execute it); clear the flags
+__global__ void chunk_init_kernel(const float* __restrict__ draft, float* __restrict__ chunk,
+                                  int* __restrict__ bad, int n, int hd) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n * hd; i += gridDim.x * blockDim.x) {
+    chunk[i] = draft[i];
+    if (i < n) bad[i] = 0;
+  }
+}
+
+// bucket row j <- fallback env fb_idx[j] (rows past the count repeat the
+// first fallback env; their results are dropped)
+__global__ void bucket_gather_kernel(const int* __restrict__ fb_idx, const int* __restrict__ fb_count, int Bk,
+                                     int hd, int S, const float* __restrict__ eps_d,
+                                     const float* __restrict__ state_in, float* __restrict__ start,
+                                     float* __restrict__ state_out, int* __restrict__ env_map) {
+  const int cnt = *fb_count;
+  const int per = hd + S;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Bk * per; i += gridDim.x * blockDim.x) {
+    const int j = i / per, c = i - j * per;
+    const int e = fb_idx[j < cnt ? j : 0];
+    if (c < hd) start[(size_t)j * hd + c] = eps_d[(size_t)e * hd + c];
+    else state_out[(size_t)j * S + (c - hd)] = state_in[(size_t)e * S + (c - hd)];
+    if (c == 0) env_map[j] = e;
+  }
+}
+
+// full-path chunks back to their envs; Euler status -> non-finite flag
+__global__ void bucket_scatter_kernel(const int* __restrict__ fb_idx, const int* __restrict__ fb_count,
+                                      int hd, const float* __restrict__ A, const int* __restrict__ status,
+                                      float* __restrict__ chunk, int* __restrict__ bad) {
+  const int cnt = *fb_count;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt * hd; i += gridDim.x * blockDim.x) {
+    const int j = i / hd, c = i - j * hd;
+    const int e = fb_idx[j];
+    chunk[(size_t)e * hd + c] = A[i];
+    if (c == 0) bad[e] = (status[2 * j] >= 0 || status[2 * j + 1]) ? 1 : 0;
+  }
+}
+
+struct ReplanFinalParams {
+  int n, H, D;
+  const int* path;
+  int* planned;
+  const int* result;
+  const float* signs;
+  float* chunk;
+  int* bad;
+  int* sie;
+  float* chunk_raw;
+  const float* mean;
+  const float* stdv;
+};
+
+// one warp per env: non-finite accepted chunks (actions.py:65-74 rejects them,
+// verifier.py:89 raises on a non-finite reconstruction), switch_in_executed
+// (runtime.py:321-323: gripper_switch(chunk[:planned], sign)), planned = 0 for
+// a non-finite chunk, destandardize (actions.py:139-144: raw = z * std + mean)
+__global__ void replan_finalize_kernel(const ReplanFinalParams p) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= p.n) return;
+  const int e = warp, hd = p.H * p.D;
+  float* c = p.chunk + (size_t)e * hd;
+  const bool acc = p.path[e] == SF_PATH_FLASH_ACCEPTED;
+  int bad = p.bad[e];
+  if (acc) {
+    bool nf = p.result[e * SF_RESULT_WORDS + SF_RES_NONFINITE] >= 0;
+    for (int i = lane; i < hd; i += 32) nf |= !isfinite(c[i]);
+    bad = __any_sync(0xffffffffu, nf) ? 1 : 0;
+  }
+  const int pl = p.planned[e];
+  int sw = 0;
+  if (acc && !bad) {
+    const float sg = p.signs[e];
+    bool hit = false;
+    for (int h = lane; h < pl; h += 32) hit |= c[(size_t)h * p.D + p.D - 1] * sg <= 0.f;
+    sw = __any_sync(0xffffffffu, hit) ? 1 : 0;
+  }
+  if (lane == 0) {
+    p.bad[e] = bad;
+    p.sie[e] = sw;
+    if (bad) p.planned[e] = 0;
+  }
+  if (p.chunk_raw)
+    for (int i = lane; i < hd; i += 32) {
+      const int d = i % p.D;
+      p.chunk_raw[(size_t)e * hd + i] = __fadd_rn(__fmul_rn(c[i], p.stdv[d]), p.mean[d]);
+    }
+}
+
 // ----------------------------------------------------------------- handle
 
 struct Buffers {
@@ -450,6 +578,16 @@ struct Buffers {
   CUtensorMap* d_maps = nullptr;
   unsigned* d_ctr = nullptr;
   float* sws = nullptr;
+  // fp32 mode (SF_AE_FP32): fp32 activations of the CUDA-core layer stack
+  bool fp32 = false;
+  float* f_rs = nullptr;   // [M] RMS row scales
+  float* f_qkv = nullptr;  // [M][(nh + 2) * 256] device row order
+  float* f_q = nullptr;    // [M][nh * 256]
+  float* f_k = nullptr;    // [M][256]
+  float* f_v = nullptr;    // [M][256]
+  float* f_o = nullptr;    // [M][nh * 256]
+  float* f_gu = nullptr;   // [M][2 * mlp]
+  float* f_h = nullptr;    // [M][mlp]
 };
 
 struct Handle {
@@ -472,7 +610,33 @@ struct Handle {
   uint8_t* v_img = nullptr;  // [L][E][nblk][32 KB] prefix V^T block images
   int img_blocks = 0;
   std::map<long long, std::unique_ptr<Buffers>> buffers;  // key: (B, K, mode)
+  std::map<uint64_t, std::unique_ptr<struct Replan>> replans;
   cudaStream_t capture_stream = nullptr;
+  cudaStream_t body_stream = nullptr;  // conditional-body captures
+};
+
+// Graph-resident replanning round (sf_ae_replan_round): owned device buffers
+// and the instantiated graph for one (n, cfg, policy, state pointers) key.
+struct Replan {
+  int n = 0, K = 0;
+  Buffers* bf = nullptr;             // flash buffers (B = n, K)
+  std::vector<int> buckets;          // Euler bucket sizes
+  std::vector<Buffers*> bb;          // denoise buffers per bucket
+  float* eps_d = nullptr;            // [n][H][D] staged denoise noise
+  float* chunk = nullptr;            // [n][H][D]
+  float* chunk_raw = nullptr;        // [n][H][D]
+  float* mean = nullptr;             // [D]
+  float* stdv = nullptr;             // [D]
+  int *path = nullptr, *planned = nullptr, *sie = nullptr, *bad = nullptr;
+  int *fb_idx = nullptr, *fb_count = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int fixed_kernels = 0;             // kernels of a round without the full path
+  ~Replan() {
+    if (exec) cudaGraphExecDestroy(exec);
+    for (void* q : {(void*)eps_d, (void*)chunk, (void*)chunk_raw, (void*)mean, (void*)stdv, (void*)path,
+                    (void*)planned, (void*)sie, (void*)bad, (void*)fb_idx, (void*)fb_count})
+      if (q) cudaFree(q);
+  }
 };
 
 int T_of(const Handle& h) { return 1 + h.cfg.horizon; }
@@ -1203,8 +1367,67 @@ void trace_mark(cudaStream_t s) {
   g_trace->push_back(ev);
 }
 
+// fp32 mode: the layer stack + head in fp32 on CUDA cores (stack_f32.cuh).
+int alloc_f32(Handle& h, Buffers& b) {
+  const sf_ae_config_t& c = h.cfg;
+  const size_t M = (size_t)b.M, nq = (size_t)c.q_heads * c.head_dim;
+  int rc;
+  if ((rc = dalloc(&b.f_rs, M)) || (rc = dalloc(&b.f_qkv, M * (nq + 2 * c.head_dim))) ||
+      (rc = dalloc(&b.f_q, M * nq)) || (rc = dalloc(&b.f_k, M * c.head_dim)) ||
+      (rc = dalloc(&b.f_v, M * c.head_dim)) || (rc = dalloc(&b.f_o, M * nq)) ||
+      (rc = dalloc(&b.f_gu, M * 2 * c.mlp)) || (rc = dalloc(&b.f_h, M * c.mlp)))
+    return rc;
+  b.fp32 = true;
+  return SF_OK;
+}
+
+int run_stack_f32(Handle& h, Buffers& b, cudaStream_t s) {
+  using namespace sf::f32;
+  const sf_ae_config_t& c = h.cfg;
+  const int M = b.M, W = c.width, nq = c.q_heads * c.head_dim, hd = c.head_dim;
+  const int T = T_of(h), L = c.layers, P = c.prefix_len;
+  const dim3 rms_grid((M * 32 + 255) / 256);
+  auto gemm = [&](bool resid, const float* A, int lda, const void* Wt, int N, int K, const float* rs,
+                  const float* bias, float* C, int ldc) {
+    const dim3 grid((N + 63) / 64, (M + 63) / 64);
+    if (resid)
+      gemm_f32_kernel<E_RESID><<<grid, 256, 0, s>>>(A, lda, (const bf16*)Wt, M, N, K, rs, bias, C, ldc);
+    else
+      gemm_f32_kernel<E_STORE><<<grid, 256, 0, s>>>(A, lda, (const bf16*)Wt, M, N, K, rs, bias, C, ldc);
+  };
+  const size_t attn_smem = sizeof(float) * ((size_t)NH * 256 + (size_t)NH * (P + T));
+  static size_t attn_smem_set = 0;
+  if (attn_smem > attn_smem_set) {
+    SF_CHECK_CUDA(cudaFuncSetAttribute(attn_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)attn_smem));
+    attn_smem_set = attn_smem;
+  }
+  for (int l = 0; l < L; ++l) {
+    rms_rows_kernel<<<rms_grid, 256, 0, s>>>(b.x, M, W, c.eps, b.f_rs);
+    gemm(false, b.x, W, h.w.qkv[l], nq + 2 * hd, W, b.f_rs, nullptr, b.f_qkv, nq + 2 * hd);
+    RopeParams rp{b.f_qkv, h.rope_t, P + T, M, c.q_heads, b.env_rows, T, P, b.f_q, b.f_k, b.f_v};
+    rope_split_f32_kernel<<<M, 256, 0, s>>>(rp);
+    AttnParams ap{b.f_q, b.f_k, b.f_v,
+                  h.k_prefix + (size_t)l * h.n_prefix_envs * P * hd,
+                  h.vt_prefix + (size_t)l * h.n_prefix_envs * hd * P,
+                  b.env_map, M, c.q_heads, b.env_rows, T, b.K, P, 1.f / sqrtf((float)hd), b.f_o};
+    attn_f32_kernel<<<M, 256, attn_smem, s>>>(ap);
+    gemm(true, b.f_o, nq, h.w.o[l], W, nq, nullptr, nullptr, b.x, W);
+    rms_rows_kernel<<<rms_grid, 256, 0, s>>>(b.x, M, W, c.eps, b.f_rs);
+    gemm(false, b.x, W, h.w.gu[l], 2 * c.mlp, W, b.f_rs, nullptr, b.f_gu, 2 * c.mlp);
+    geglu_f32_kernel<<<592, 256, 0, s>>>(b.f_gu, M, c.mlp, b.f_h);
+    gemm(true, b.f_h, c.mlp, h.w.down[l], W, c.mlp, nullptr, nullptr, b.x, W);
+  }
+  rms_rows_kernel<<<rms_grid, 256, 0, s>>>(b.x, M, W, c.eps, b.f_rs);
+  gemm(false, b.x, W, h.w.out_w, c.action_dim, W, b.f_rs, (const float*)h.w.out_b, b.vel, c.action_dim);
+  SF_CHECK_CUDA(cudaGetLastError());
+  count_launch(L * 9 + 2);
+  return SF_OK;
+}
+
 // The layer stack + head on the current X (used by verify and Euler).
 int run_stack(Handle& h, Buffers& b, cudaStream_t s, bool pdl) {
+  if (b.fp32) return run_stack_f32(h, b, s);
   if (b.use_stack && !g_trace) return launch_stack(b, s, pdl);
   int rc;
   for (int l = 0; l < h.cfg.layers; ++l) {
@@ -1322,6 +1545,8 @@ int enqueue_denoise(Handle& h, Buffers& b, int n_steps, cudaStream_t s, bool pdl
   return SF_OK;
 }
 
+// mode: 0 verify, 1 denoise, 2 velocity; + kModeF32 for the fp32-mode buffers
+constexpr int kModeF32 = 8;
 Buffers* get_buffers(Handle& h, int B, int K, int mode, int* rc) {
   const long long key = ((long long)mode << 40) | ((long long)B << 8) | K;
   auto it = h.buffers.find(key);
@@ -1329,6 +1554,7 @@ Buffers* get_buffers(Handle& h, int B, int K, int mode, int* rc) {
   auto b = std::make_unique<Buffers>();
   *rc = build(h, *b, B, K);
   if (*rc) return nullptr;
+  if ((mode & kModeF32) && (*rc = alloc_f32(h, *b))) return nullptr;
   Buffers* raw = b.get();
   h.buffers[key] = std::move(b);
   return raw;
@@ -1433,12 +1659,15 @@ extern "C" int sf_ae_create(const sf_ae_config_t* cfg, const sf_ae_weights_t* w,
 extern "C" int sf_ae_destroy(void* handle) {
   auto* h = static_cast<Handle*>(handle);
   if (!h) return SF_OK;
+  h->replans.clear();
   for (auto& kv : h->buffers) {
     Buffers& b = *kv.second;
     if (b.graph) cudaGraphExecDestroy(b.graph);
     void* ptrs[] = {b.x, b.xb, b.ssq, b.q, b.ks, b.vt, b.attn, b.h, b.vel, b.draft, b.eps,
                     b.state, b.signs, b.recon, b.dist, b.branch, b.result, b.status, b.ws,
-                    b.counters, b.ap.ws, b.sws, b.d_maps, b.d_ctr, b.env_map, b.env_ident};
+                    b.counters, b.ap.ws, b.sws, b.d_maps, b.d_ctr, b.env_map, b.env_ident,
+                    b.obs, b.obs_b, b.dh1, b.dh2, b.f_rs, b.f_qkv, b.f_q, b.f_k, b.f_v, b.f_o,
+                    b.f_gu, b.f_h};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -1452,6 +1681,7 @@ extern "C" int sf_ae_destroy(void* handle) {
   if (h->v_img) cudaFree(h->v_img);
   if (h->temb_euler) cudaFree(h->temb_euler);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
+  if (h->body_stream) cudaStreamDestroy(h->body_stream);
   delete h;
   return SF_OK;
 }
@@ -1535,7 +1765,7 @@ static int verify_common(Handle* h, int n_envs, const sf_verify_cfg_t* cfg, cons
   SF_REQUIRE(n_envs >= 1 && n_envs <= h->n_prefix_envs, "n_envs exceeds the prefix pool");
   int rc = check_verify_cfg(cfg, signs);
   if (rc) return rc;
-  Buffers* b = get_buffers(*h, n_envs, cfg->k, 0, &rc);
+  Buffers* b = get_buffers(*h, n_envs, cfg->k, (flags & SF_AE_FP32) ? kModeF32 : 0, &rc);
   if (!b) return rc;
   SF_REQUIRE(!with_draft || b->has_draft, "this expert was built without a draft model");
   if ((rc = ensure_temb(*h, cfg, s))) return rc;
@@ -1674,7 +1904,7 @@ extern "C" int sf_ae_denoise_envs(void* handle, int n_envs, const int* env_map, 
   SF_REQUIRE(num_steps >= 1 && num_steps <= 64, "num_steps must be in [1, 64]");
   cudaStream_t s = (cudaStream_t)stream;
   int rc = 0;
-  Buffers* b = get_buffers(*h, n_envs, 1, 1, &rc);
+  Buffers* b = get_buffers(*h, n_envs, 1, 1 | ((flags & SF_AE_FP32) ? kModeF32 : 0), &rc);
   if (!b) return rc;
   const sf_ae_config_t& c = h->cfg;
   if (h->temb_euler_n != num_steps) {
@@ -1715,6 +1945,247 @@ extern "C" int sf_ae_denoise_envs(void* handle, int n_envs, const int* env_map, 
   }
   SF_CHECK_CUDA(cudaMemcpyAsync(chunk_out, b->draft, hd * 4, cudaMemcpyDeviceToDevice, s));
   SF_CHECK_CUDA(cudaMemcpyAsync(status, b->status, (size_t)n_envs * 8, cudaMemcpyDeviceToDevice, s));
+  return SF_OK;
+}
+
+namespace {
+
+// Euler buckets: powers of two up to 64, then multiples of 64, capped at n
+std::vector<int> replan_buckets(int n) {
+  std::vector<int> b;
+  for (int v = 1; v < 64 && v < n; v *= 2) b.push_back(v);
+  for (int v = 64; v < n; v += 64) b.push_back(v);
+  b.push_back(n);
+  return b;
+}
+
+int build_replan(Handle& h, Replan& R, int n, const sf_verify_cfg_t* cfg, const sf_replan_policy_t* pol,
+                 const float* signs_unused, int* fsr, int* has_cache, bool pdl, bool fp32) {
+  (void)signs_unused;
+  const sf_ae_config_t& c = h.cfg;
+  const int hd = c.horizon * c.action_dim;
+  int rc = 0;
+  R.n = n;
+  R.K = cfg->k;
+  const int f32mode = fp32 ? kModeF32 : 0;
+  R.bf = get_buffers(h, n, cfg->k, f32mode, &rc);
+  if (!R.bf) return rc;
+  SF_REQUIRE(R.bf->has_draft, "the replanning round needs the draft model");
+  R.buckets = replan_buckets(n);
+  SF_REQUIRE((int)R.buckets.size() <= kMaxBuckets, "too many Euler buckets");
+  for (int bk : R.buckets) {
+    Buffers* b = get_buffers(h, bk, 1, 1 | f32mode, &rc);
+    if (!b) return rc;
+    R.bb.push_back(b);
+  }
+  if ((rc = dalloc(&R.eps_d, (size_t)n * hd)) || (rc = dalloc(&R.chunk, (size_t)n * hd)) ||
+      (rc = dalloc(&R.chunk_raw, (size_t)n * hd)) || (rc = dalloc(&R.mean, (size_t)c.action_dim)) ||
+      (rc = dalloc(&R.stdv, (size_t)c.action_dim)) || (rc = dalloc(&R.path, n)) ||
+      (rc = dalloc(&R.planned, n)) || (rc = dalloc(&R.sie, n)) || (rc = dalloc(&R.bad, n)) ||
+      (rc = dalloc(&R.fb_idx, n)) || (rc = dalloc(&R.fb_count, 1)))
+    return rc;
+  if (pol->std_mean) {
+    SF_CHECK_CUDA(cudaMemcpy(R.mean, pol->std_mean, sizeof(float) * c.action_dim, cudaMemcpyDeviceToDevice));
+    SF_CHECK_CUDA(cudaMemcpy(R.stdv, pol->std_std, sizeof(float) * c.action_dim, cudaMemcpyDeviceToDevice));
+  }
+  if (!h.capture_stream)
+    SF_CHECK_CUDA(cudaStreamCreateWithFlags(&h.capture_stream, cudaStreamNonBlocking));
+  if (!h.body_stream) SF_CHECK_CUDA(cudaStreamCreateWithFlags(&h.body_stream, cudaStreamNonBlocking));
+  cudaStream_t cs = h.capture_stream;
+  Buffers& bf = *R.bf;
+  const int64_t before = sf_launch_count(0);
+  cudaGraph_t g = nullptr;
+  SF_CHECK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  auto fail = [&](int code) {
+    cudaGraph_t junk = nullptr;
+    cudaStreamEndCapture(cs, &junk);
+    if (junk) cudaGraphDestroy(junk);
+    sf::count_launch(-(int)(sf_launch_count(0) - before));
+    return code;
+  };
+  // 1. the speculative attempt for every env (draft MLP -> verify -> gate -> decision)
+  if ((rc = enqueue_verify(h, bf, cfg, cs, pdl, true))) return fail(rc);
+  // 2. bookkeeping + compaction + bucket select (sets the SWITCH value)
+  cudaStreamCaptureStatus st;
+  cudaGraph_t cg = nullptr;
+  if (cudaStreamGetCaptureInfo(cs, &st, nullptr, &cg, nullptr, nullptr) != cudaSuccess || !cg)
+    return fail(SF_ECUDA);
+  cudaGraphConditionalHandle cond;
+  if (cudaGraphConditionalHandleCreate(&cond, cg, (unsigned)R.buckets.size(), cudaGraphCondAssignDefault) !=
+      cudaSuccess) {
+    sf::set_error("cudaGraphConditionalHandleCreate failed");
+    return fail(SF_ECUDA);
+  }
+  ReplanSelectParams sp{};
+  sp.n = n;
+  sp.result = bf.result;
+  sp.fsr = fsr;
+  sp.has_cache = has_cache;
+  sp.mode_flash = pol->mode_flash;
+  sp.pf = pol->periodic_refresh;
+  sp.r = cfg->replan_size;
+  sp.path = R.path;
+  sp.planned = R.planned;
+  sp.fb_idx = R.fb_idx;
+  sp.fb_count = R.fb_count;
+  sp.n_buckets = (int)R.buckets.size();
+  for (int i = 0; i < sp.n_buckets; ++i) sp.bucket[i] = R.buckets[i];
+  sp.cond = cond;
+  replan_select_kernel<<<1, 1024, 0, cs>>>(sp);
+  chunk_init_kernel<<<(n * hd + 255) / 256 < 1184 ? (n * hd + 255) / 256 : 1184, 256, 0, cs>>>(
+      bf.draft, R.chunk, R.bad, n, hd);
+  sf::count_launch(2);
+  // 3. SWITCH over the Euler buckets
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  if (cudaStreamGetCaptureInfo(cs, &st, nullptr, &cg, &deps, &ndeps) != cudaSuccess) return fail(SF_ECUDA);
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = cond;
+  cp.conditional.type = cudaGraphCondTypeSwitch;
+  cp.conditional.size = (unsigned)R.buckets.size();
+  cudaGraphNode_t cnode;
+  cudaError_t ce = cudaGraphAddNode(&cnode, cg, deps, ndeps, &cp);
+  if (ce != cudaSuccess) {
+    sf::set_error("conditional SWITCH node: %s", cudaGetErrorString(ce));
+    return fail(SF_ECUDA);
+  }
+  if (cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies) != cudaSuccess)
+    return fail(SF_ECUDA);
+  const int64_t body0 = sf_launch_count(0);
+  for (size_t i = 0; i < R.buckets.size(); ++i) {
+    Buffers& b = *R.bb[i];
+    const int bk = R.buckets[i];
+    cudaStream_t bs = h.body_stream;
+    if (cudaStreamBeginCaptureToGraph(bs, cp.conditional.phGraph_out[i], nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      sf::set_error("body capture %zu failed", i);
+      return fail(SF_ECUDA);
+    }
+    const int per = hd + c.state_dim;
+    const int gblocks = (bk * per + 255) / 256 < 1184 ? (bk * per + 255) / 256 : 1184;
+    bucket_gather_kernel<<<gblocks, 256, 0, bs>>>(R.fb_idx, R.fb_count, bk, hd, c.state_dim, R.eps_d, bf.state,
+                                                  b.draft, b.state, b.env_map);
+    int brc = enqueue_denoise(h, b, pol->num_steps, bs, pdl);
+    const int sblocks = (bk * hd + 255) / 256 < 1184 ? (bk * hd + 255) / 256 : 1184;
+    bucket_scatter_kernel<<<sblocks, 256, 0, bs>>>(R.fb_idx, R.fb_count, hd, b.draft, b.status, R.chunk, R.bad);
+    cudaGraph_t body = nullptr;
+    cudaError_t be = cudaStreamEndCapture(bs, &body);
+    if (brc) return fail(brc);
+    if (be != cudaSuccess) {
+      sf::set_error("body capture %zu: %s", i, cudaGetErrorString(be));
+      return fail(SF_ECUDA);
+    }
+  }
+  // body kernels run only when their bucket is selected: not counted here
+  sf::count_launch(-(int)(sf_launch_count(0) - body0));
+  // 4. non-finite flags, switch_in_executed, destandardize
+  ReplanFinalParams fp{n, c.horizon, c.action_dim, R.path, R.planned, bf.result, bf.signs, R.chunk, R.bad,
+                       R.sie, pol->std_mean ? R.chunk_raw : nullptr, R.mean, R.stdv};
+  replan_finalize_kernel<<<(n * 32 + 255) / 256, 256, 0, cs>>>(fp);
+  sf::count_launch(1);
+  ce = cudaStreamEndCapture(cs, &g);
+  R.fixed_kernels = (int)(sf_launch_count(0) - before);
+  sf::count_launch(-R.fixed_kernels);
+  if (ce != cudaSuccess) {
+    sf::set_error("replan capture: %s", cudaGetErrorString(ce));
+    if (g) cudaGraphDestroy(g);
+    return SF_ECUDA;
+  }
+  ce = cudaGraphInstantiate(&R.exec, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) {
+    sf::set_error("replan graph instantiate: %s", cudaGetErrorString(ce));
+    R.exec = nullptr;
+    return SF_ECUDA;
+  }
+  return SF_OK;
+}
+
+}  // namespace
+
+extern "C" int sf_ae_replan_round(void* handle, int n_envs, const sf_verify_cfg_t* cfg,
+                                  const sf_replan_policy_t* policy, const float* obs, const float* eps_verify,
+                                  const float* eps_denoise, const float* state, const float* signs, int* fsr,
+                                  int* has_cache, const sf_replan_out_t* out, int flags, void* stream) {
+  auto* h = static_cast<Handle*>(handle);
+  SF_REQUIRE(h && cfg && policy && obs && eps_verify && eps_denoise && state && signs && fsr && has_cache &&
+                 out && out->chunk && out->path && out->planned,
+             "null argument");
+  SF_REQUIRE(h->k_prefix, "no prefix KV bound (sf_ae_set_prefix)");
+  SF_REQUIRE(n_envs >= 1 && n_envs <= h->n_prefix_envs, "n_envs exceeds the prefix pool");
+  SF_REQUIRE(policy->num_steps >= 1 && policy->num_steps <= 64, "num_steps must be in [1, 64]");
+  SF_REQUIRE(policy->periodic_refresh >= 0, "periodic_refresh must be >= 0");
+  SF_REQUIRE(!policy->std_mean == !policy->std_std, "standardizer needs both mean and std");
+  int rc = check_verify_cfg(cfg, signs);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const sf_ae_config_t& c = h->cfg;
+  if ((rc = ensure_temb(*h, cfg, s))) return rc;
+  if (h->temb_euler_n != policy->num_steps) {
+    if (h->temb_euler) cudaFree(h->temb_euler);
+    if ((rc = dalloc(&h->temb_euler, (size_t)policy->num_steps * c.width))) return rc;
+    std::vector<float> taus(policy->num_steps);
+    for (int i = 0; i < policy->num_steps; ++i) taus[i] = (float)((double)i / (double)policy->num_steps);
+    if ((rc = compute_temb(*h, taus.data(), policy->num_steps, h->temb_euler, s))) return rc;
+    SF_CHECK_CUDA(cudaStreamSynchronize(s));
+    h->temb_euler_n = policy->num_steps;
+    for (auto& kv : h->buffers)
+      if (kv.second->graph) {  // denoise graphs baked the old time embedding
+        cudaGraphExecDestroy(kv.second->graph);
+        kv.second->graph = nullptr;
+      }
+    h->replans.clear();
+  }
+  const bool pdl = (flags & SF_AE_PDL) != 0, fp32 = (flags & SF_AE_FP32) != 0;
+  uint64_t key = 1469598103934665603ull;
+  auto mix = [&](const void* q, size_t nb) {
+    const unsigned char* b = static_cast<const unsigned char*>(q);
+    for (size_t i = 0; i < nb; ++i) key = (key ^ b[i]) * 1099511628211ull;
+  };
+  const void* keyed[] = {fsr, has_cache, policy->std_mean, policy->std_std};
+  const int knobs[] = {n_envs, cfg_key(cfg), policy->mode_flash, policy->periodic_refresh, policy->num_steps,
+                       (int)pdl, (int)fp32};
+  mix(keyed, sizeof(keyed));
+  mix(knobs, sizeof(knobs));
+  auto it = h->replans.find(key);
+  if (it == h->replans.end()) {
+    auto R = std::make_unique<Replan>();
+    rc = build_replan(*h, *R, n_envs, cfg, policy, signs, fsr, has_cache, pdl, fp32);
+    if (rc == SF_ECUDA && pdl) {  // programmatic edges inside conditional bodies unsupported: plain edges
+      R = std::make_unique<Replan>();
+      rc = build_replan(*h, *R, n_envs, cfg, policy, signs, fsr, has_cache, false, fp32);
+    }
+    if (rc) return rc;
+    it = h->replans.emplace(key, std::move(R)).first;
+  }
+  Replan& R = *it->second;
+  Buffers& bf = *R.bf;
+  const size_t hd = (size_t)n_envs * c.horizon * c.action_dim;
+  SF_CHECK_CUDA(cudaMemcpyAsync(bf.obs, obs, (size_t)n_envs * c.draft_in * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(bf.eps, eps_verify, hd * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(R.eps_d, eps_denoise, hd * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(bf.state, state, (size_t)n_envs * c.state_dim * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(bf.signs, signs, (size_t)n_envs * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaGraphLaunch(R.exec, s));
+  sf::count_launch(R.fixed_kernels);
+  SF_CHECK_CUDA(cudaMemcpyAsync(out->chunk, R.chunk, hd * 4, cudaMemcpyDeviceToDevice, s));
+  if (out->chunk_raw && policy->std_mean)
+    SF_CHECK_CUDA(cudaMemcpyAsync(out->chunk_raw, R.chunk_raw, hd * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(out->path, R.path, (size_t)n_envs * 4, cudaMemcpyDeviceToDevice, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(out->planned, R.planned, (size_t)n_envs * 4, cudaMemcpyDeviceToDevice, s));
+  if (out->switch_in_executed)
+    SF_CHECK_CUDA(cudaMemcpyAsync(out->switch_in_executed, R.sie, (size_t)n_envs * 4, cudaMemcpyDeviceToDevice, s));
+  if (out->nonfinite)
+    SF_CHECK_CUDA(cudaMemcpyAsync(out->nonfinite, R.bad, (size_t)n_envs * 4, cudaMemcpyDeviceToDevice, s));
+  if (out->branch_prefixes)
+    SF_CHECK_CUDA(cudaMemcpyAsync(out->branch_prefixes, bf.branch, (size_t)n_envs * cfg->k * 4,
+                                  cudaMemcpyDeviceToDevice, s));
+  if (out->result)
+    SF_CHECK_CUDA(cudaMemcpyAsync(out->result, bf.result, (size_t)n_envs * SF_RESULT_WORDS * 4,
+                                  cudaMemcpyDeviceToDevice, s));
+  if (out->n_fallback)
+    SF_CHECK_CUDA(cudaMemcpyAsync(out->n_fallback, R.fb_count, 4, cudaMemcpyDeviceToDevice, s));
   return SF_OK;
 }
 

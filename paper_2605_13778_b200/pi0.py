@@ -30,7 +30,7 @@ import torch
 from . import _capi, _device
 from .actions import ChannelLayout
 
-SF_AE_GRAPH, SF_AE_PDL = 1, 2
+SF_AE_GRAPH, SF_AE_PDL, SF_AE_FP32 = 1, 2, 4
 TID_A_W, TID_S_W, TID_T1_W, TID_T2_W, TID_OUT_W = 1, 2, 3, 4, 5
 TID_DRAFT_BASE = 20
 TID_LAYER_BASE = 100
@@ -138,7 +138,16 @@ class ActionExpert:
     def __init__(self, cfg: AEConfig = PI0, seed: int = 0, n_envs: int = 1, kv_seed: int = 1,
                  layout: ChannelLayout | None = None, std: float = 0.02,
                  flags: int = SF_AE_GRAPH | SF_AE_PDL, env_offset: int = 0,
-                 draft_gripper_bias: float = 0.0):
+                 draft_gripper_bias: float = 0.0, precision: str = "bf16"):
+        """precision "bf16": tcgen05 kernels, bf16 activations / fp32 accumulation
+        (the performance path); "fp32": verify / denoise run the fp32 mode
+        (SF_AE_FP32: fp32 activations and FMA accumulation on CUDA cores, the
+        north star's 1e-5 parity mode). Weights and prefix KV are bf16 in both."""
+        if precision not in ("bf16", "fp32"):
+            raise ValueError(f"unknown precision {precision!r}")
+        if precision == "fp32":
+            flags |= SF_AE_FP32
+        self.precision = precision
         self.cfg = cfg
         self.horizon = cfg.horizon
         self.dim = cfg.action_dim
@@ -411,60 +420,90 @@ class ActionExpert:
 
 class BatchedReplanner:
     """Device-side replanning rounds for B independent envs (run_episode,
-    runtime.py:219-334, minus the conveyor): per round one batched flash graph
+    runtime.py:219-334, minus the conveyor), ONE graph launch per round with no
+    host synchronisation (``sf_ae_replan_round``): the batched flash attempt
     (draft + K-branch verify + gate + decision for every env), the round
-    bookkeeping on the device (``sf_replan_update``: periodic-refresh counter,
-    path codes, planned prefix with the cap, fallback compaction), then the
-    10-step Euler full path only on the compacted fallback bucket (padded to a
-    power of two so each bucket size keeps one CUDA graph;
-    ``sf_ae_denoise_envs`` maps bucket rows to their envs' prefix KV). The
-    only host sync per round is the fallback count. Returns device tensors:
-    the chunk to execute [B, H, D] (draft for accepted envs, full-path chunk
-    otherwise), path codes (``_capi.SF_PATH_*``), planned prefix lengths."""
+    bookkeeping on the device (periodic-refresh counter, path codes, planned
+    prefix with the cap, fallback compaction), then a graph SWITCH node picks
+    the smallest pre-captured Euler bucket (powers of two up to 64, then
+    multiples of 64) holding the fallback envs and runs the N-step full path
+    on it (bucket rows gathered / scattered on the device, each attending to
+    its env's prefix KV). A final kernel flags non-finite chunks (planned = 0;
+    the reference raises FloatingPointError, flowpolicy.py:290 /
+    verifier.py:89), computes ``switch_in_executed`` for accepted rounds
+    (runtime.py:321-323) and destandardizes the chunk when a Standardizer is
+    given (actions.py:139-144, runtime.py:325).
+
+    ``round`` returns device tensors (chunk [B, H, D] standardized, path codes
+    ``_capi.SF_PATH_*``, planned, branch prefixes [B, K], flash result words
+    [B, 8]); ``chunk_raw``, ``switch_in_executed``, ``nonfinite`` and
+    ``n_fallback`` are attributes updated by the same launch."""
 
     def __init__(self, ae: ActionExpert, n_envs: int, vcfg, replan_size: int = 12,
                  periodic_refresh: int = 2, phase_fallback: bool = True, prefix_cap: bool = True,
-                 flash: bool = True, num_steps: int = 10):
+                 flash: bool = True, num_steps: int = 10, standardizer=None):
         if n_envs > ae.n_envs:
             raise ValueError(f"{n_envs} envs but the prefix pool holds {ae.n_envs}")
+        if replan_size < 1:
+            raise ValueError("replan_size must be >= 1")
+        if periodic_refresh < 0:
+            raise ValueError("periodic_refresh must be >= 0")
+        from .verifier import make_cfg
+
         self.ae, self.n, self.vcfg = ae, n_envs, vcfg
         self.replan_size, self.periodic_refresh = replan_size, periodic_refresh
         self.phase_fallback, self.prefix_cap, self.flash = phase_fallback, prefix_cap, flash
         self.num_steps = num_steps
         dev = _device.device()
         i32 = dict(dtype=torch.int32, device=dev)
+        H, D, K = ae.horizon, ae.dim, len(vcfg.timesteps)
         self.fsr = torch.zeros(n_envs, **i32)        # flash rounds since the last full round
         self.has_cache = torch.zeros(n_envs, **i32)  # a full round has produced a context
+        self.chunk = torch.empty((n_envs, H, D), dtype=torch.float32, device=dev)
+        self.chunk_raw = torch.empty_like(self.chunk) if standardizer is not None else None
         self.path = torch.empty(n_envs, **i32)
         self.planned = torch.empty(n_envs, **i32)
-        self.fb_idx = torch.empty(n_envs, **i32)
-        self.fb_count = torch.zeros(1, **i32)
+        self.switch_in_executed = torch.empty(n_envs, **i32)
+        self.nonfinite = torch.empty(n_envs, **i32)
+        self.branch = torch.empty((n_envs, K), **i32)
+        self.result = torch.empty((n_envs, _capi.SF_RESULT_WORDS), **i32)
+        self.n_fallback = torch.zeros(1, **i32)
+        self._std = None
+        if standardizer is not None:
+            self._std = (torch.as_tensor(np.asarray(standardizer.mean, np.float32)).to(dev),
+                         torch.as_tensor(np.asarray(standardizer.std, np.float32)).to(dev))
+        self._cfg = make_cfg(vcfg, -1.0, phase_fallback, prefix_cap, replan_size)
+        self._pol = _capi.SfReplanPolicy(int(bool(flash)), periodic_refresh, num_steps,
+                                         self._std[0].data_ptr() if self._std else None,
+                                         self._std[1].data_ptr() if self._std else None)
+        self._out = _capi.SfReplanOut(
+            self.chunk.data_ptr(), self.chunk_raw.data_ptr() if self.chunk_raw is not None else None,
+            self.path.data_ptr(), self.planned.data_ptr(), self.switch_in_executed.data_ptr(),
+            self.nonfinite.data_ptr(), self.branch.data_ptr(), self.result.data_ptr(),
+            self.n_fallback.data_ptr())
         self.round_index = 0
+        # kernels of the selected Euler bucket body (gather, status init, N x
+        # [embed, layers x (qkv, attention, o, gate/up, down), head, update], scatter)
+        L = ae.cfg.layers
+        self.body_kernels = 3 + num_steps * ((9 * L + 2) + 2 if ae.precision == "fp32" else 3 + 5 * L)
 
     def round(self, obs: torch.Tensor, eps_verify: torch.Tensor, eps_denoise: torch.Tensor,
-              state: torch.Tensor, signs: torch.Tensor):
-        ae, n = self.ae, self.n
-        s = torch.cuda.current_stream().cuda_stream
-        draft, _, _, branch, result = ae.flash_batch(
-            self.vcfg, obs, eps_verify, state, signs, phase_fallback=self.phase_fallback,
-            prefix_cap=self.prefix_cap, replan_size=self.replan_size)
-        _capi.check(_capi.lib().sf_replan_update(
-            n, result.data_ptr(), self.fsr.data_ptr(), self.has_cache.data_ptr(), int(self.flash),
-            self.periodic_refresh, self.replan_size, self.path.data_ptr(), self.planned.data_ptr(),
-            self.fb_idx.data_ptr(), self.fb_count.data_ptr(), s), "replan update")
-        chunk = draft
-        n_fb = int(self.fb_count.item())
-        if n_fb:
-            bucket = min(n, 1 << (n_fb - 1).bit_length())
-            idx = self.fb_idx[:bucket].clone()
-            if bucket > n_fb:
-                idx[n_fb:] = idx[0]  # padding rows repeat a real env; results dropped
-            full, _ = ae.denoise_envs(idx, eps_denoise.index_select(0, idx),
-                                      state.index_select(0, idx), self.num_steps)
-            chunk = draft.clone()
-            chunk.index_copy_(0, idx[:n_fb].long(), full[:n_fb])
+              state: torch.Tensor, signs: torch.Tensor, stream=None):
+        n = self.n
+        for name, t, shape in (("obs", obs, (n, self.ae.cfg.draft_in)),
+                               ("eps_verify", eps_verify, (n, self.ae.horizon, self.ae.dim)),
+                               ("eps_denoise", eps_denoise, (n, self.ae.horizon, self.ae.dim)),
+                               ("state", state, (n, self.ae.cfg.state_dim)), ("signs", signs, (n,))):
+            if tuple(t.shape) != shape or t.dtype != torch.float32 or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous float32 tensor of shape {shape}")
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _capi.check(_capi.lib().sf_ae_replan_round(
+            self.ae._h, n, ctypes.byref(self._cfg), ctypes.byref(self._pol), obs.data_ptr(),
+            eps_verify.data_ptr(), eps_denoise.data_ptr(), state.data_ptr(), signs.data_ptr(),
+            self.fsr.data_ptr(), self.has_cache.data_ptr(), ctypes.byref(self._out), self.ae.flags, s),
+            "replan round")
         self.round_index += 1
-        return chunk, self.path, self.planned, branch, result
+        return self.chunk, self.path, self.planned, self.branch, self.result
 
 
 # ---------------------------------------------------------------- VLM prefill
