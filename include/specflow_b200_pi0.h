@@ -78,6 +78,12 @@ int sf_ae_destroy(void* handle);
  * e of a batched call attends to pool entry e. */
 int sf_ae_set_prefix(void* handle, const void* k_prefix, const void* vt_prefix, int n_envs);
 
+/* The attention reads per-64-key-block images of the bound pool, built by
+ * sf_ae_set_prefix. After the bound pool is rewritten in place (a context
+ * refresh: sf_vlm_prefill into the bound pool), call this on the stream of that
+ * write to rebuild the images before the next verify / denoise. Async. */
+int sf_ae_refresh_prefix(void* handle, void* stream);
+
 /* Batched speculative verification (verifier.py:109-150 + runtime.py:286-320)
  * for n_envs envs: draft, eps [n_envs][H][D] f32, state [n_envs][S] f32,
  * signs [n_envs] f32 (NULL: cfg->current_sign). Outputs (each may be NULL

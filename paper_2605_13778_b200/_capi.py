@@ -101,6 +101,7 @@ SIGNATURES = {
     "sf_ae_create": (_I, [_P, _P, _P]),
     "sf_ae_destroy": (_I, [_P]),
     "sf_ae_set_prefix": (_I, [_P, _P, _P, _I]),
+    "sf_ae_refresh_prefix": (_I, [_P, _P]),
     "sf_ae_verify": (_I, [_P, _I, ctypes.POINTER(SfVerifyCfg), _P, _P, _P, _P,
                           ctypes.POINTER(SfVerifyOut), _I, _P]),
     "sf_ae_denoise": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, _P]),

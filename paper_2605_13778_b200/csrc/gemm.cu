@@ -41,20 +41,9 @@ int num_sms() {
 
 using KernelFn = void (*)(CUtensorMap, CUtensorMap, Params);
 
-// batch-1 swap GEMMs sized for two CTAs per SM (PDL overlap of consecutive
-// GEMMs); SF_SWAP_OCC=1 selects the single-CTA variant (full-SMEM ring)
-bool swap_occ2() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SF_SWAP_OCC");
-    v = (e && atoi(e) == 1) ? 0 : 1;
-  }
-  return v == 1;
-}
-
 template <int KIND>
 KernelFn swap_fn() {
-  return swap_occ2() ? gemm_swap_kernel<KIND, 2> : gemm_swap_kernel<KIND, 1>;
+  return gemm_swap_kernel<KIND>;
 }
 template <int KIND>
 KernelFn persistent_fn() {
@@ -148,7 +137,7 @@ int plan(Op* op, const void* A, int rows_a, int lda, const void* B, int rows_b, 
   p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;  // every split gets >= 1 block
   p.e = e;
   const uint32_t stage_bytes = kAStageBytes + ((bn * BK * 2 + 1023) & ~1023);
-  const size_t budget = swap_ab && swap_occ2() ? 113 * 1024 - kTailBytes - 1024 : 227 * 1024 - kTailBytes - 1024;
+  const size_t budget = 227 * 1024 - kTailBytes - 1024;
   int stages = (int)(budget / stage_bytes);
   if (stages > max_stages) stages = max_stages;
   if (stages > 16) stages = 16;
@@ -159,7 +148,7 @@ int plan(Op* op, const void* A, int rows_a, int lda, const void* B, int rows_b, 
   region = (region + 1023) & ~size_t(1023);
   // split-K partial workspace (caller provides op->p.ws of op->ws_bytes)
   op->ws_bytes = p.splits > 1 ? (size_t)p.splits * p.total_tiles * (bn / 16) * BM * 16 * 4 : 0;
-  SF_REQUIRE(region + kTailBytes + 1024 <= budget + kTailBytes + 1024, "GEMM shared memory over budget");
+  SF_REQUIRE(region + kTailBytes + 1024 <= 227 * 1024, "GEMM shared memory over budget");
   p.smem_stage_region = (uint32_t)region;
   op->smem = region + kTailBytes + 1024;
   if (swap_ab) {

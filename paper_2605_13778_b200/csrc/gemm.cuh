@@ -527,11 +527,8 @@ __device__ __forceinline__ void reduce_chunks(const EpiArgs& e, const Params& p,
 #undef mine
 }
 
-// OCC = 2: register budget for two co-resident CTAs per SM, so the next
-// kernel's CTAs (PDL) start and stream their weights while this one drains
-// (the plan caps the stage ring at half the SMEM).
-template <int KIND, int OCC>
-__global__ void __launch_bounds__(kThreads, OCC)
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 1)
     gemm_swap_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const Params p) {
   extern __shared__ uint8_t smem_raw[];

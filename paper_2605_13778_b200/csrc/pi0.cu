@@ -1656,9 +1656,10 @@ extern "C" int sf_ae_create(const sf_ae_config_t* cfg, const sf_ae_weights_t* w,
   return SF_OK;
 }
 
-extern "C" int sf_ae_destroy(void* handle) {
-  auto* h = static_cast<Handle*>(handle);
-  if (!h) return SF_OK;
+// Drop every plan / graph / activation buffer (they bake the prefix pool's
+// tensor maps and pointers); the replanning graphs go first (they reference
+// the buffers).
+static void free_buffers(Handle* h) {
   h->replans.clear();
   for (auto& kv : h->buffers) {
     Buffers& b = *kv.second;
@@ -1671,6 +1672,13 @@ extern "C" int sf_ae_destroy(void* handle) {
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
+  h->buffers.clear();
+}
+
+extern "C" int sf_ae_destroy(void* handle) {
+  auto* h = static_cast<Handle*>(handle);
+  if (!h) return SF_OK;
+  free_buffers(h);
   cudaFree(h->temb);
   cudaFree(h->temb_hidden);
   cudaFree(h->temb_tau_dev);
@@ -1705,6 +1713,8 @@ extern "C" int sf_ae_set_prefix(void* handle, const void* k_prefix, const void* 
     const size_t bytes = (size_t)c.layers * n_envs * nblk * 32768;
     if (getenv("SF_NO_KV_IMAGES") == nullptr && c.head_dim == 256 &&
         cudaMalloc(&h->k_img, bytes) == cudaSuccess && cudaMalloc(&h->v_img, bytes) == cudaSuccess) {
+      // the pool may have been written on any stream (setup call: full sync)
+      SF_CHECK_CUDA(cudaDeviceSynchronize());
       prefix_image_kernel<<<148 * 8, 256>>>(h->k_prefix, h->vt_prefix, h->k_img, h->v_img,
                                             c.layers * n_envs, c.prefix_len, nblk);
       SF_CHECK_CUDA(cudaGetLastError());
@@ -1717,16 +1727,22 @@ extern "C" int sf_ae_set_prefix(void* handle, const void* k_prefix, const void* 
     }
   }
   // plans embed the prefix tensor maps: drop them
-  for (auto& kv : h->buffers) {
-    Buffers& b = *kv.second;
-    if (b.graph) cudaGraphExecDestroy(b.graph);
-    void* ptrs[] = {b.x, b.xb, b.ssq, b.q, b.ks, b.vt, b.attn, b.h, b.vel, b.draft, b.eps,
-                    b.state, b.signs, b.recon, b.dist, b.branch, b.result, b.status, b.ws,
-                    b.counters, b.ap.ws, b.sws, b.d_maps, b.d_ctr, b.env_map, b.env_ident};
-    for (void* p : ptrs)
-      if (p) cudaFree(p);
-  }
-  h->buffers.clear();
+  free_buffers(h);
+  return SF_OK;
+}
+
+// Re-derive the attention's block images after the bound pool was rewritten
+// in place (a context refresh, e.g. sf_vlm_prefill into the bound pool), on
+// `stream` after that write. Graphs stay valid (same image pointers).
+extern "C" int sf_ae_refresh_prefix(void* handle, void* stream) {
+  auto* h = static_cast<Handle*>(handle);
+  SF_REQUIRE(h && h->k_prefix, "no prefix KV bound (sf_ae_set_prefix)");
+  if (!h->k_img) return SF_OK;  // tensor-map path reads the pool directly
+  const sf_ae_config_t& c = h->cfg;
+  prefix_image_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+      h->k_prefix, h->vt_prefix, h->k_img, h->v_img, c.layers * h->n_prefix_envs, c.prefix_len, h->img_blocks);
+  SF_CHECK_CUDA(cudaGetLastError());
+  sf::count_launch();
   return SF_OK;
 }
 

@@ -255,6 +255,13 @@ class ActionExpert:
                     "prefix")
         self.n_envs = E
 
+    def refresh_prefix(self, stream=None):
+        """Re-derive the attention's block images of the bound pool after it
+        was rewritten in place (context refresh into ``k_prefix`` /
+        ``vt_prefix``), ordered on ``stream`` after that write."""
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _capi.check(_capi.lib().sf_ae_refresh_prefix(self._h, s), "refresh prefix")
+
     def __del__(self):
         try:
             if getattr(self, "_h", None):
@@ -580,8 +587,10 @@ class VLMPrefill:
             pass
 
     def prefill(self, x: torch.Tensor, k_pool: torch.Tensor | None = None,
-                vt_pool: torch.Tensor | None = None, stream=None):
-        """x [E, P, W] f32 -> (k_pool [L, E, P, 256], vt_pool [L, E, 256, P]) bf16."""
+                vt_pool: torch.Tensor | None = None, stream=None, expert: "ActionExpert | None" = None):
+        """x [E, P, W] f32 -> (k_pool [L, E, P, 256], vt_pool [L, E, 256, P]) bf16.
+        ``expert``: an ActionExpert whose BOUND pool this prefill rewrites in
+        place; its attention block images are refreshed on the same stream."""
         cfg = self.cfg
         E = x.shape[0]
         dev = x.device
@@ -594,5 +603,7 @@ class VLMPrefill:
         s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
         _capi.check(_capi.lib().sf_vlm_prefill(self._h, E, x.contiguous().data_ptr(), k_pool.data_ptr(),
                                                vt_pool.data_ptr(), s), "vlm prefill")
+        if expert is not None:
+            expert.refresh_prefix(s)
         return k_pool, vt_pool
 

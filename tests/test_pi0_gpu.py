@@ -437,3 +437,40 @@ def test_vlm_prefill_matches_oracle_and_feeds_the_expert():
     s = torch.from_numpy(rng.standard_normal((E, S)).astype(np.float32)).cuda()
     recon, dist, _, _ = ae.verify_batch(VerifierConfig(timesteps=(0.2, 0.6), delta=0.5), d, e_, s)
     assert torch.isfinite(recon).all() and torch.isfinite(dist).all()
+
+
+def test_prefix_refresh_in_place():
+    """A context refresh written INTO the bound pool (VLMPrefill.prefill with
+    expert=...) is what the next verify attends to: same outputs as a fresh
+    expert bound to the refreshed pool (advisor r1: stale block images)."""
+    import dataclasses
+
+    import torch
+
+    from paper_2605_13778_b200 import pi0
+    from paper_2605_13778_b200.verifier import VerifierConfig
+
+    vcfg = pi0.VLMConfig(width=512, layers=2, mlp=1024, prefix_len=96)
+    vlm = pi0.VLMPrefill(vcfg, seed=7)
+    E = 2
+    rng = np.random.default_rng(9)
+    _, dcfg = _pair()
+    dcfg = dataclasses.replace(dcfg, prefix_len=vcfg.prefix_len)
+    kp, vtp = vlm.prefill(torch.from_numpy(rng.standard_normal((E, 96, 512)).astype(np.float32)).cuda())
+    ae = pi0.ActionExpert(dcfg, seed=0, n_envs=E, kv_seed=1)
+    ae.bind_prefix(kp, vtp)
+    H, D, S = dcfg.horizon, dcfg.action_dim, dcfg.state_dim
+    d = torch.from_numpy(rng.standard_normal((E, H, D)).astype(np.float32)).cuda()
+    e_ = torch.from_numpy(rng.standard_normal((E, H, D)).astype(np.float32)).cuda()
+    s = torch.from_numpy(rng.standard_normal((E, S)).astype(np.float32)).cuda()
+    vc = VerifierConfig(timesteps=(0.2, 0.6), delta=0.5)
+    before = ae.verify_batch(vc, d, e_, s)[0].clone()
+    # refresh in place, then verify again through the same (captured) graph
+    vlm.prefill(torch.from_numpy(rng.standard_normal((E, 96, 512)).astype(np.float32)).cuda(), kp, vtp,
+                expert=ae)
+    after = ae.verify_batch(vc, d, e_, s)[0].clone()
+    fresh = pi0.ActionExpert(dcfg, seed=0, n_envs=E, kv_seed=1)
+    fresh.bind_prefix(kp.clone(), vtp.clone())
+    want = fresh.verify_batch(vc, d, e_, s)[0]
+    assert not torch.equal(before, after)
+    assert torch.equal(after, want)
