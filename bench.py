@@ -79,6 +79,7 @@ def parse(argv=None):
     ap.add_argument("--audit-envs", type=int, default=8)
     ap.add_argument("--cpu-sample-envs", type=int, default=2)
     ap.add_argument("--calibrate", action="store_true", help="print deciding-distance quantiles and exit")
+    ap.add_argument("--sweep", action="store_true", help="cfg5 sweep (K, H, delta) instead of the bench line")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU/gloo: shard + seed + gather plumbing only (no GPU, no kernels)")
     return ap.parse_args(argv)
@@ -745,6 +746,140 @@ def latency_tiny():
     return out
 
 
+# --------------------------------------------------------------- cfg5 sweep
+
+CFG5_DELTAS = (0.0, 0.05, 0.1, 0.15, 0.2, 0.3)   # PAPER.md:684-691 grid
+CFG5_KS = (1, 2, 4, 8)
+CFG5_HS = (16, 50, 100)
+
+
+def sweep_tiny():
+    """cfg5 on the tiny trained policy: the reference's own models re-trained
+    per chunk horizon (tests/golden/cfg5_h{16,100}_*.ckpt, cfg2_*.ckpt for H =
+    50; specflow.bench.cli run --seed 7 with chunk.horizon = H), replayed on the
+    330 recorded flash-attempt observations of the reference's cfg2 episodes
+    (draft / encoder features, normalised state, current gripper sign; the
+    noise is re-drawn per H from the recorded verify seeds, verifier.py:129).
+    Per (H, K): device p50 of one fused flash attempt (runtime.flash_attempt's
+    device path, numpy in / out) next to the reference algorithm's CPU p50 (oracle
+    port, numpy float64, 1 thread); per (H, K, delta): mean accepted prefix and
+    accept / rejected / phase-fallback rates (runtime.py:286-320)."""
+    import numpy as np
+
+    from oracle import specflow_oracle as so
+    from paper_2605_13778_b200 import checkpoint as ck
+    from paper_2605_13778_b200 import precision
+    from paper_2605_13778_b200.flowpolicy import ConditioningCache, _run_full
+    from paper_2605_13778_b200.verifier import VerifierConfig, tiny_flash_round
+
+    gold = ROOT / "tests" / "golden"
+    tr = np.load(gold / "cfg2_trace.npz")
+    sel = np.nonzero(tr["call_kind"] == 1)[0]
+    rows = []
+    for H in CFG5_HS:
+        main = gold / ("cfg2_main.ckpt" if H == 50 else f"cfg5_h{H}_main.ckpt")
+        dr = gold / ("cfg2_draft.ckpt" if H == 50 else f"cfg5_h{H}_draft.ckpt")
+        enc, field, std, _ = ck.load_main_checkpoint(main)
+        draft, _ = ck.load_draft_checkpoint(dr)
+        lay = field.layout
+        D = lay.dim
+        with precision("fp64"):
+            embs = [(_run_full(enc.net, tr["call_efeat"][i], enc.embed_dim, None, np.zeros(0), np.zeros(1), 1, 1,
+                               0)[1]) for i in sel]
+            for K in CFG5_KS:
+                taus = tuple((k + 1) / (K + 1) for k in range(K))
+                stats = []
+                for delta in CFG5_DELTAS:
+                    cfg = VerifierConfig(timesteps=taus, delta=delta, gripper_window=24)
+                    L, paths = [], []
+                    for j, i in enumerate(sel):
+                        eps = np.random.default_rng(int(tr["call_seed"][i])).standard_normal((H, D))
+                        _, rep = tiny_flash_round(field, draft.net, tr["call_dfeat"][i], ConditioningCache(embs[j]),
+                                                  tr["call_state"][i], eps, cfg, float(tr["call_sign"][i]), lay)
+                        L.append(rep.prefix)
+                        paths.append(rep.decision)
+                    n = len(paths)
+                    stats.append({"delta": delta, "mean_prefix": float(np.mean(L)),
+                                  "accept_rate": paths.count("flash_accepted") / n,
+                                  "rejected_rate": paths.count("flash_rejected_fallback") / n,
+                                  "phase_fallback_rate": paths.count("flash_phase_fallback") / n})
+                i0 = int(sel[0])
+                eps0 = np.random.default_rng(int(tr["call_seed"][i0])).standard_normal((H, D))
+                cfg = VerifierConfig(timesteps=taus, delta=0.15, gripper_window=24)
+                dev_ms = host_p50_ms(lambda: tiny_flash_round(
+                    field, draft.net, tr["call_dfeat"][i0], ConditioningCache(embs[0]), tr["call_state"][i0], eps0,
+                    cfg, float(tr["call_sign"][i0]), lay), 200)
+                fw = [np.asarray(w) for w in field.net.weights]
+                fb = [np.asarray(b) for b in field.net.biases]
+                dws = [np.asarray(w) for w in draft.net.weights]
+                dbs = [np.asarray(b) for b in draft.net.biases]
+
+                def ref():
+                    dv = so.propose(dws, dbs, tr["call_dfeat"][i0], H, D)
+                    so.verify(lambda x, t: so.mlp_field_velocity(fw, fb, x, t, embs[0], tr["call_state"][i0]),
+                              dv, eps0, taus, 0.15, lay.continuous_dims, "l2", 24, float(tr["call_sign"][i0]))
+
+                cpu_ms = host_p50_ms(ref, 100)
+                rows.append({"H": H, "K": K, "taus": list(taus), "spec_round_p50_ms_device_fp64": dev_ms,
+                             "spec_round_p50_ms_cpu_reference": cpu_ms, "attempts": int(len(sel)),
+                             "delta_sweep": stats})
+    return {"workload": "cfg5 tiny: reference-trained D=3 models per H, 330 recorded flash observations",
+            "cpu_reference": "oracle/specflow_oracle.py (numpy float64), 1 thread", "rows": rows}
+
+
+def sweep_pi0(envs=64):
+    """cfg5 at pi0 scale (random-init AE, bf16): batch-1 spec round / verify p50
+    per (H, K), and over `envs` envs the accepted prefix / fallback rates at
+    delta quantiles of the observed distances (random drafts with a one-signed
+    gripper column so the phase gate does not mask the threshold sweep)."""
+    import dataclasses
+
+    import numpy as np
+    import torch
+
+    from paper_2605_13778_b200 import _capi
+    from paper_2605_13778_b200.pi0 import PI0, ActionExpert
+    from paper_2605_13778_b200.verifier import VerifierConfig
+
+    rows = []
+    for H in CFG5_HS:
+        cfg = dataclasses.replace(PI0, horizon=H)
+        ae = ActionExpert(cfg, n_envs=envs, draft_gripper_bias=GRIP)
+        g = torch.Generator(device="cuda").manual_seed(H)
+        D, S, F = cfg.action_dim, cfg.state_dim, cfg.draft_in
+        obs = torch.randn((envs, F), generator=g, device="cuda")
+        eps = torch.randn((envs, H, D), generator=g, device="cuda")
+        state = torch.randn((envs, S), generator=g, device="cuda")
+        signs = torch.ones(envs, device="cuda")
+        for K in CFG5_KS:
+            taus = tuple((k + 1) / (K + 1) for k in range(K))
+            vc = VerifierConfig(timesteps=taus, delta=0.15, gripper_window=24)
+            o1 = ae.flash_batch(vc, obs[:1], eps[:1], state[:1], signs[:1])
+            for _ in range(3):
+                ae.flash_batch(vc, obs[:1], eps[:1], state[:1], signs[:1], outputs=o1)
+            torch.cuda.synchronize()
+            spec = p50_ms(lambda: ae.flash_batch(vc, obs[:1], eps[:1], state[:1], signs[:1], outputs=o1), 20)
+            draft, _, dist, _, _ = ae.flash_batch(vc, obs, eps, state, signs)
+            d = dist.float().cpu().numpy()
+            sweep = []
+            for q in (0.0, 0.1, 0.25, 0.5, 0.75, 0.9):
+                delta = float(np.quantile(d, q)) if q > 0 else 0.0
+                _, _, _, res = ae.verify_batch(VerifierConfig(timesteps=taus, delta=delta, gripper_window=24),
+                                               draft, eps, state, signs)
+                r = res.cpu().numpy()
+                path = r[:, _capi.SF_RES_PATH]
+                sweep.append({"distance_quantile": q, "delta": delta,
+                              "mean_prefix": float(r[:, _capi.SF_RES_PREFIX].mean()),
+                              "accept_rate": float((path == _capi.SF_PATH_FLASH_ACCEPTED).mean()),
+                              "rejected_rate": float((path == _capi.SF_PATH_FLASH_REJECTED).mean()),
+                              "phase_fallback_rate": float((path == _capi.SF_PATH_FLASH_PHASE).mean())})
+            rows.append({"H": H, "K": K, "taus": list(taus), "spec_round_b1_p50_ms": spec, "envs": envs,
+                         "delta_sweep": sweep})
+        del ae
+        torch.cuda.empty_cache()
+    return {"workload": "cfg5 pi0-scale (random-init AE, bf16, 1 GPU)", "rows": rows}
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -755,6 +890,11 @@ def main():
         return
     if args.dry_run:
         run_dry(args, rank, world)
+        return
+    if args.sweep:
+        if rank == 0:
+            print(json.dumps({"metric": "cfg5 sweep: latency vs K, H; accepted prefix / fallback rate vs delta",
+                              "tiny": sweep_tiny(), "pi0": sweep_pi0()}), flush=True)
         return
     run_ours(args, rank, world, local)
 
