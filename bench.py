@@ -743,6 +743,65 @@ def latency_tiny():
     out["cpu_reference_full_round_p50_ms"] = host_p50_ms(ref_full, 100)
     out["cpu_reference_cores"] = 1
     out["cpu_reference_kind"] = "port (oracle/specflow_oracle.py, numpy float64)"
+    out["cfg2"] = latency_cfg2()
+    return out
+
+
+def latency_cfg2():
+    """cfg2: the reference-trained default policy (tests/golden/cfg2_*.ckpt,
+    D=3, H=50, K=2, delta=0.15, N=10) on a recorded flash observation:
+    runtime.flash_attempt / full_round p50 (numpy in/out, fp64) next to the
+    reference algorithm's CPU p50 (oracle port, numpy float64, 1 thread)."""
+    import numpy as np
+
+    from oracle import specflow_oracle as so
+    from paper_2605_13778_b200 import checkpoint as ck
+    from paper_2605_13778_b200 import precision
+    from paper_2605_13778_b200.draft import DraftModel
+    from paper_2605_13778_b200.flowpolicy import ConditioningCache, ContextEncoder, ObsNormalizer, Observation
+    from paper_2605_13778_b200.runtime import Models, RunnerState, RuntimePolicy, flash_attempt, full_round
+    from paper_2605_13778_b200.verifier import VerifierConfig
+
+    gold = ROOT / "tests" / "golden"
+    tr = np.load(gold / "cfg2_trace.npz")
+    enc, field, std, _ = ck.load_main_checkpoint(gold / "cfg2_main.ckpt")
+    draft, _ = ck.load_draft_checkpoint(gold / "cfg2_draft.ckpt")
+    ident = ObsNormalizer.identity(5, 3)
+    models = Models(encoder=ContextEncoder(net=enc.net, n_tasks=enc.n_tasks, normalizer=ident), field=field,
+                    standardizer=std, draft=DraftModel(net=draft.net, layout=draft.layout, horizon=draft.horizon,
+                                                       n_tasks=draft.n_tasks, normalizer=ident))
+    cfg = VerifierConfig(timesteps=tuple(tr["taus"]), delta=float(tr["delta"]), gripper_window=int(tr["window"]))
+    policy = RuntimePolicy(verifier_cfg=cfg)
+    i = int(np.nonzero(tr["call_kind"] == 1)[0][0])
+    f = tr["call_dfeat"][i]
+    obs = Observation(world_features=f[:5], task_id=int(np.argmax(f[5:7])), robot_state=f[7:10])
+    st = RunnerState(cache=ConditioningCache(tr["call_emb"][i]), gripper_sign=float(tr["call_sign"][i]))
+    out = {"config": "cfg2: reference-trained D=3, H=50, K=2 policy, recorded observation, fp64"}
+    with precision("fp64"):
+        for _ in range(20):
+            flash_attempt(obs, models, policy, st, 1, 7)
+            full_round(obs, models, policy, 0, 0, 7)
+        out["spec_round_p50_ms"] = host_p50_ms(lambda: flash_attempt(obs, models, policy, st, 1, 7), 300)
+        out["full_round_p50_ms"] = host_p50_ms(lambda: full_round(obs, models, policy, 0, 0, 7), 300)
+    fw, fb = [np.asarray(w) for w in field.net.weights], [np.asarray(b) for b in field.net.biases]
+    dws, dbs = [np.asarray(w) for w in draft.net.weights], [np.asarray(b) for b in draft.net.biases]
+    ews, ebs = [np.asarray(w) for w in enc.net.weights], [np.asarray(b) for b in enc.net.biases]
+    emb, state, sign = tr["call_emb"][i], f[7:10], float(tr["call_sign"][i])
+
+    def ref_spec():
+        dv = so.propose(dws, dbs, f, 50, 3)
+        e = np.random.default_rng(1).standard_normal((50, 3))
+        so.verify(lambda x, t: so.mlp_field_velocity(fw, fb, x, t, emb, state), dv, e, cfg.timesteps, cfg.delta,
+                  2, "l2", cfg.gripper_window, sign)
+
+    def ref_full():
+        em = so.encode_context(ews, ebs, f[:7])
+        a0 = np.random.default_rng(2).standard_normal((50, 3))
+        so.integrate_flow(lambda x, t: so.mlp_field_velocity(fw, fb, x, t, em, state), a0, 10)
+
+    out["cpu_reference_spec_round_p50_ms"] = host_p50_ms(ref_spec, 100)
+    out["cpu_reference_full_round_p50_ms"] = host_p50_ms(ref_full, 100)
+    out["cpu_reference_cores"] = 1
     return out
 
 

@@ -29,7 +29,7 @@
 #include "attention.cuh"
 #include "common.cuh"
 #include "gemm_host.h"
-#include "stack.cuh"
+#include "gemm.cuh"
 #include "stack_f32.cuh"
 #include "replan.cuh"
 #include "specflow_b200_pi0.h"
@@ -571,13 +571,6 @@ struct Buffers {
   bf16* dh2 = nullptr;
   gemm::Op dops[3];
   bool has_draft = false;
-  // batch-1 layer-stack megakernel (stack.cuh): one launch for the whole stack
-  bool use_stack = false;
-  std::vector<gemm::Op> sops;  // per layer: qkv, o, gu, down; then head (stack splits)
-  stack::Args sargs{};
-  CUtensorMap* d_maps = nullptr;
-  unsigned* d_ctr = nullptr;
-  float* sws = nullptr;
   // fp32 mode (SF_AE_FP32): fp32 activations of the CUDA-core layer stack
   bool fp32 = false;
   float* f_rs = nullptr;   // [M] RMS row scales
@@ -813,31 +806,12 @@ int build(Handle& h, Buffers& b, int B, int K) {
     if (sw) return gemm::plan(op, wt, n_out, k_in, act, rows, k_in, k_in, bn, 0, 1, e);
     return gemm::plan(op, act, rows, k_in, wt, n_out, k_in, k_in, bn, 1, 0, e);
   };
-  // stack (megakernel) split count: every (tile, split) task on its own SM
   int nsm = 148;
   {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  // experimental (opt-in, SF_STACK=1): slower than the tuned per-op chain so far
-  const bool want_stack = swap && getenv("SF_STACK") != nullptr;
-  if (want_stack) b.sops.resize(4 * L + 1);
-  auto stack_splits = [&](int n_out, int k_in) {
-    const int tiles = (n_out + gemm::BM - 1) / gemm::BM, nkb = k_in / gemm::BK;
-    int S = nsm / tiles;
-    S = S > 16 ? 16 : S;
-    S = S > nkb ? nkb : S;
-    S = S < 1 ? 1 : S;
-    const int kbps = (nkb + S - 1) / S;
-    return (nkb + kbps - 1) / kbps;
-  };
-  auto plan_sop = [&](int idx, const void* wt, int n_out, const void* act, int k_in,
-                      const gemm::EpiArgs& e) {
-    if (!want_stack) return (int)SF_OK;
-    return gemm::plan(&b.sops[idx], wt, n_out, k_in, act, b.M, k_in, k_in, bn_swap,
-                      stack_splits(n_out, k_in), 1, e);
-  };
   struct Spec {
     const void* wt;
     int n_out;
@@ -850,9 +824,7 @@ int build(Handle& h, Buffers& b, int B, int K) {
                      const gemm::EpiArgs& e) {
     const int idx = (int)(op - b.ops.data());
     if (idx < 4 * L) specs[idx] = Spec{wt, n_out, act, k_in, e};
-    int r = plan_mm(op, wt, n_out, act, b.M, k_in, swap ? bn_swap : bn_norm, swap, e);
-    if (r) return r;
-    return plan_sop((int)(op - b.ops.data()), wt, n_out, act, k_in, e);
+    return plan_mm(op, wt, n_out, act, b.M, k_in, swap ? bn_swap : bn_norm, swap, e);
   };
   for (int l = 0; l < L; ++l) {
     gemm::EpiArgs e = epi_base(gemm::EPI_QKV);
@@ -891,7 +863,6 @@ int build(Handle& h, Buffers& b, int B, int K) {
     e.bias = static_cast<const float*>(h.w.out_b);
     if ((rc = plan_mm(&b.ops[4 * L], h.w.out_w, c.action_dim, b.xb, b.M, W, bn_head, swap, e)))
       return rc;
-    if ((rc = plan_sop(4 * L, h.w.out_w, c.action_dim, b.xb, W, e))) return rc;
   }
   // --- draft MLP plans: rows = envs (swap-AB while B <= 256)
   if (b.has_draft) {
@@ -1099,147 +1070,6 @@ int build(Handle& h, Buffers& b, int B, int K) {
       if ((rc = gemm::make_map(&mp[4], b.vt, c.head_dim, b.m_ld, b.m_ld, c.head_dim / 2))) return rc;
     }
   }
-  // --- batch-1 layer-stack megakernel: phases, tensor maps, counters
-  if (want_stack && b.attn_tiles * b.attn_splits <= nsm && b.attn_tiles <= stack::kMaxTileSlots) {
-    const uint32_t b_bytes = (uint32_t)bn_swap * gemm::BK * 2;
-    const uint32_t stage_bytes = gemm::kAStageBytes + ((b_bytes + 1023) & ~1023u);
-    int stages = (int)(stack::kRingMax / stage_bytes);
-    stages = stages > stack::kMaxStages ? stack::kMaxStages : stages;
-    size_t ws = 0;
-    bool ok = stages >= 2;
-    for (auto& op : b.sops) {
-      ws = op.ws_bytes > ws ? op.ws_bytes : ws;
-      ok = ok && op.p.tiles_b == 1 && op.p.tiles_a <= stack::kMaxTileSlots &&
-           op.p.tiles_a * op.p.splits <= nsm;
-    }
-    if (ok) {
-      stack::Args& a = b.sargs;
-      a = stack::Args{};
-      // per-type plans (identical for every layer but the weight map)
-      const int type_op[stack::T_COUNT] = {0, 1, 2, 3, -1};
-      for (int t = 0; t < stack::T_COUNT; ++t) {
-        const gemm::Op& op = type_op[t] < 0 ? b.sops[4 * L] : b.sops[type_op[t]];
-        a.gp[t] = op.p;
-      }
-      std::vector<CUtensorMap> maps;  // weights [4L+1], activations [5], attention [5L]
-      for (int i = 0; i < 4 * L + 1; ++i) maps.push_back(b.sops[i].ta);
-      for (int t = 0; t < stack::T_COUNT; ++t)
-        maps.push_back(type_op[t] < 0 ? b.sops[4 * L].tb : b.sops[type_op[t]].tb);
-      for (int i = 0; i < 5 * L; ++i) maps.push_back(b.attn_maps[i]);
-      if (ws && (rc = dalloc(&b.sws, ws / sizeof(float)))) return rc;
-      SF_CHECK_CUDA(cudaMalloc(&b.d_maps, sizeof(CUtensorMap) * maps.size()));
-      SF_CHECK_CUDA(cudaMemcpy(b.d_maps, maps.data(), sizeof(CUtensorMap) * maps.size(),
-                               cudaMemcpyHostToDevice));
-      for (int t = 0; t < stack::T_COUNT; ++t) {
-        a.gp[t].ws = b.sws;
-        a.tx[t] = b.d_maps + 4 * L + 1 + t;
-      }
-      a.tw = b.d_maps;
-      a.am = b.d_maps + 4 * L + 1 + stack::T_COUNT;
-      a.layers = L;
-      a.n_phases = 5 * L + 1;
-      a.attn_tasks = b.attn_tiles * b.attn_splits;
-      const size_t n_ctr = 32 + (size_t)a.n_phases * stack::kMaxTileSlots;
-      if ((rc = dalloc(&b.d_ctr, n_ctr))) return rc;
-      a.stages = stages;
-      a.stage_bytes = stage_bytes;
-      a.b_bytes = b_bytes;
-      a.bn = bn_swap;
-      a.ap = b.ap;
-      a.grid_bar = b.d_ctr;
-      a.tile_cnt = b.d_ctr + 32;
-      b.use_stack = true;
-    }
-  }
-  return SF_OK;
-}
-
-// One cooperative launch of the layer-stack megakernel (one CTA per SM).
-int launch_stack(const Buffers& b, cudaStream_t s, bool pdl) {
-  static bool attr = false;
-  static int nsm = 0;
-  if (!attr) {
-    SF_CHECK_CUDA(cudaFuncSetAttribute(stack::stack_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)stack::kSmemBytes));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    int per_sm = 0;
-    SF_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, stack::stack_kernel, stack::kThreads, stack::kSmemBytes));
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, stack::stack_kernel);
-    int per_sm0 = 0, per_sm256 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm0, stack::stack_kernel, stack::kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm256, stack::stack_kernel, 256, 0);
-    SF_REQUIRE(per_sm >= 1,
-               "stack kernel does not fit on an SM (regs %d, local %zu, smem %zu + %zu; occ(smem 0) %d, "
-               "occ(256 thr) %d, maxThreads %d)",
-               fa.numRegs, (size_t)fa.localSizeBytes, (size_t)stack::kSmemBytes,
-               (size_t)fa.sharedSizeBytes, per_sm0, per_sm256, fa.maxThreadsPerBlock);
-    attr = true;
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(nsm);
-  cfg.blockDim = dim3(stack::kThreads);
-  cfg.dynamicSmemBytes = stack::kSmemBytes;
-  cfg.stream = s;
-  cudaLaunchAttribute a[2];
-  a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  a[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
-  a[1].id = cudaLaunchAttributeCooperative;
-  a[1].val.cooperative = 1;
-  cfg.attrs = a;
-  cfg.numAttrs = 2;
-  const bool trace = getenv("SF_STACK_TRACE") != nullptr;
-  if (!trace) {
-    SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, stack::stack_kernel, b.sargs));
-    count_launch();
-    return SF_OK;
-  }
-  // debug: per-phase %globaltimer stamps of every CTA, summarised on stdout
-  stack::Args ta = b.sargs;
-  const size_t n = (size_t)nsm * ta.n_phases * 8;
-  SF_CHECK_CUDA(cudaMalloc(&ta.dbg, n * 8));
-  SF_CHECK_CUDA(cudaMemsetAsync(ta.dbg, 0, n * 8, s));
-  SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, stack::stack_kernel, ta));
-  std::vector<unsigned long long> h(n);
-  SF_CHECK_CUDA(cudaMemcpyAsync(h.data(), ta.dbg, n * 8, cudaMemcpyDeviceToHost, s));
-  SF_CHECK_CUDA(cudaStreamSynchronize(s));
-  cudaFree(ta.dbg);
-  const unsigned long long t0 = h[0];
-  auto at = [&](int blk, int ph, int i) { return h[((size_t)blk * ta.n_phases + ph) * 8 + i]; };
-  printf("stack trace (us from phase start; avg / max over active CTAs): post_done mma_done acc_ready tile_in tile_out epi_done arrive | grid-barrier exit of the phase\n");
-  for (int ph = 0; ph < ta.n_phases; ++ph) {
-    double sum[8] = {}, mx[8] = {};
-    int cnt[8] = {};
-    unsigned long long st_min = ~0ull, st_max = 0;
-    for (int blk = 0; blk < nsm; ++blk) {
-      const unsigned long long st = at(blk, ph, 0);
-      if (!st) continue;
-      st_min = st < st_min ? st : st_min;
-      st_max = st > st_max ? st : st_max;
-    }
-    for (int blk = 0; blk < nsm; ++blk)
-      for (int i = 1; i < 8; ++i) {
-        const unsigned long long v = at(blk, ph, i);
-        if (!v) continue;
-        const double d = (double)(v - st_min) * 1e-3;
-        sum[i] += d;
-        cnt[i]++;
-        mx[i] = d > mx[i] ? d : mx[i];
-      }
-    const unsigned long long nxt = ph + 1 < ta.n_phases ? at(0, ph + 1, 0) : 0;
-    printf("  %3d start@%8.2f skew %5.2f |", ph, (double)(st_min - t0) * 1e-3, (double)(st_max - st_min) * 1e-3);
-    const int order[7] = {1, 2, 3, 7, 4, 5, 6};
-    for (int k = 0; k < 7; ++k) {
-      const int i = order[k];
-      printf(" %5.2f/%5.2f", cnt[i] ? sum[i] / cnt[i] : -1.0, mx[i]);
-    }
-    printf(" | next %6.2f\n", nxt ? (double)(nxt - st_min) * 1e-3 : -1.0);
-  }
-  count_launch();
   return SF_OK;
 }
 
@@ -1428,7 +1258,6 @@ int run_stack_f32(Handle& h, Buffers& b, cudaStream_t s) {
 // The layer stack + head on the current X (used by verify and Euler).
 int run_stack(Handle& h, Buffers& b, cudaStream_t s, bool pdl) {
   if (b.fp32) return run_stack_f32(h, b, s);
-  if (b.use_stack && !g_trace) return launch_stack(b, s, pdl);
   int rc;
   for (int l = 0; l < h.cfg.layers; ++l) {
     if ((rc = gemm::launch(b.ops[4 * l + 0], s, pdl))) return rc;
@@ -1666,7 +1495,7 @@ static void free_buffers(Handle* h) {
     if (b.graph) cudaGraphExecDestroy(b.graph);
     void* ptrs[] = {b.x, b.xb, b.ssq, b.q, b.ks, b.vt, b.attn, b.h, b.vel, b.draft, b.eps,
                     b.state, b.signs, b.recon, b.dist, b.branch, b.result, b.status, b.ws,
-                    b.counters, b.ap.ws, b.sws, b.d_maps, b.d_ctr, b.env_map, b.env_ident,
+                    b.counters, b.ap.ws, b.env_map, b.env_ident,
                     b.obs, b.obs_b, b.dh1, b.dh2, b.f_rs, b.f_qkv, b.f_q, b.f_k, b.f_v, b.f_o,
                     b.f_gu, b.f_h};
     for (void* p : ptrs)

@@ -145,3 +145,26 @@ def test_product_does_not_import_oracle():
     for f in pkg.rglob("*.py"):
         text = f.read_text()
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", text, flags=re.M), f
+
+
+def test_models_gripper_sign_matches_reference_rule():
+    """Models.gripper_sign (runtime.py:60-64): standardise the raw gripper
+    state with the gripper channel's mean / std, > 0 -> +1 else -1 (an exact
+    zero maps to -1), against the oracle restatement and the cfg2 recordings."""
+    import numpy as np
+
+    from oracle import specflow_oracle as so
+    from paper_2605_13778_b200 import checkpoint as ck
+    from paper_2605_13778_b200.runtime import Models
+
+    enc, field, std, _ = ck.load_main_checkpoint(GOLDEN / "cfg2_main.ckpt")
+    models = Models(encoder=enc, field=field, standardizer=std)
+    gi = field.layout.gripper_index
+    mean, sd = float(std.mean[gi]), float(std.std[gi])
+    for raw in (-3.0, -1.0, 0.0, 0.5, 1.0, 2.5, mean, mean + 1e-12, mean - 1e-12):
+        assert models.gripper_sign(raw) == so.gripper_sign(raw, mean, sd)
+    assert models.gripper_sign(mean) == -1.0  # standardised exact zero -> -1
+    tr = np.load(GOLDEN / "cfg2_trace.npz")
+    flash = tr["call_kind"] == 1
+    for raw, sign in zip(tr["call_raw_grip"][flash], tr["call_sign"][flash]):
+        assert models.gripper_sign(float(raw)) == float(sign)

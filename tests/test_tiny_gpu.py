@@ -204,3 +204,52 @@ def test_distances_bit_exact_fp64():
         diff = a[:, :c] - b[:, :c]
         want = np.sqrt(np.sum(diff * diff, axis=1))
         assert np.array_equal(continuous_distances(a, b, lay), want), c
+
+
+def test_cfg2_public_runtime_api_replay():
+    """The reference-shaped entry points themselves (runtime.full_round /
+    runtime.flash_attempt with Observation objects, runtime.py:157-198) on the
+    recorded cfg2 calls: the round's seed from _stream_seed(episode, round,
+    stream) (runtime.py:152-154), identical decisions, fp64 endpoints within
+    1e-10 of the reference's. Observations are rebuilt from the recorded
+    (normalised) features with identity normalisers."""
+    from paper_2605_13778_b200 import precision
+    from paper_2605_13778_b200.draft import DraftModel
+    from paper_2605_13778_b200.flowpolicy import ContextEncoder, ObsNormalizer, Observation
+    from paper_2605_13778_b200.runtime import Models, RunnerState, RuntimePolicy, flash_attempt, full_round
+    from paper_2605_13778_b200.verifier import VerifierConfig
+
+    tr = cfg2_trace()
+    enc, field, std, draft = cfg2_models()
+    ident = ObsNormalizer.identity(5, 3)
+    models = Models(encoder=ContextEncoder(net=enc.net, n_tasks=enc.n_tasks, normalizer=ident), field=field,
+                    standardizer=std,
+                    draft=DraftModel(net=draft.net, layout=draft.layout, horizon=draft.horizon,
+                                     n_tasks=draft.n_tasks, normalizer=ident))
+    cfg = VerifierConfig(timesteps=tuple(tr["taus"]), delta=float(tr["delta"]), gripper_window=int(tr["window"]))
+    policy = RuntimePolicy(verifier_cfg=cfg, replan_size=int(tr["replan_size"]))
+    n_full = n_flash = 0
+    with precision("fp64"):
+        for i in range(0, len(tr["call_kind"]), 3):
+            f = tr["call_dfeat"][i]
+            obs = Observation(world_features=f[:5], task_id=int(np.argmax(f[5:7])), robot_state=f[7:10])
+            ep = int(tr["episode_seeds"][int(tr["call_episode"][i])])
+            r = int(tr["call_round"][i])
+            if tr["call_kind"][i] == 0:
+                chunk, cache, seed = full_round(obs, models, policy, r, 0, ep)
+                assert seed == int(tr["call_seed"][i])
+                np.testing.assert_allclose(cache.embedding, tr["call_emb"][i], rtol=1e-10, atol=1e-10)
+                np.testing.assert_allclose(chunk.values, tr["call_chunk"][i], rtol=1e-9, atol=1e-9)
+                n_full += 1
+            else:
+                from paper_2605_13778_b200.flowpolicy import ConditioningCache
+
+                st = RunnerState(cache=ConditioningCache(tr["call_emb"][i]), gripper_sign=float(tr["call_sign"][i]))
+                chunk, rep, seed = flash_attempt(obs, models, policy, st, r, ep)
+                assert seed == int(tr["call_seed"][i])
+                np.testing.assert_allclose(chunk.values, tr["call_draft"][i], rtol=1e-10, atol=1e-10)
+                np.testing.assert_allclose(rep.distances, tr["call_distances"][i], rtol=1e-10, atol=1e-10)
+                assert rep.branch_prefixes == tuple(int(x) for x in tr["call_branch"][i])
+                assert rep.gripper_switch_detected == bool(tr["call_switch"][i])
+                n_flash += 1
+    assert n_full > 50 and n_flash > 50
