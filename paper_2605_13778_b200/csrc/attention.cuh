@@ -58,8 +58,12 @@ constexpr int kPartStride = HD + 2;  // split-KV partial O row stride in SMEM (f
 constexpr int kMaxSplitsKV = 16;     // split-KV cluster size limit
 
 struct Params {
-  int M;            // valid token rows
-  int env_rows;     // rows per env (multiple of 16)
+  int M;            // valid token rows (n_envs * env_rows)
+  int env_rows;     // rows per env: K * (1 + H), dense (no per-env padding)
+  int n_envs;
+  int tiles_env;    // 16-token query tiles per env: ceil(env_rows / 16); a
+                    // tile never straddles two envs (one prefix per tile),
+                    // rows past the env's last token are computed, not stored
   int seg_len;      // tokens per branch segment (1 + H)
   int segs;         // branches per env (K)
   int prefix_len;   // P
@@ -173,9 +177,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x, split = blockIdx.y;
-  const int m0 = tile * 16;                 // first token of the tile
-  const int env = m0 / p.env_rows;
+  const int env = tile / p.tiles_env;
   const int env_start = env * p.env_rows;
+  const int m0 = env_start + (tile - env * p.tiles_env) * 16;  // first token of the tile
   const int seg_first = (m0 - env_start) / p.seg_len;
   // first suffix key token, rounded down to a 64-key boundary so every TMA box
   // of the transposed V starts on an aligned inner coordinate (3 blocks then
@@ -341,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int seg_q = local_q / p.seg_len;
     const int t_q = local_q - seg_q * p.seg_len;
     const bool real_q = local_q < p.segs * p.seg_len && tok < p.M;
+    const bool store_q = local_q < p.env_rows && tok < p.M;  // the row's token belongs to this env
     const int seg_lo = seg_q * p.seg_len;                         // local token range of the
     const int seg_hi = seg_lo + (t_q >= 1 ? p.seg_len : 1);       // row's visible suffix keys
     __shared__ float xm[2 * 2 * BQ];                              // [2 parity][2 half][128]
@@ -493,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                       __uint_as_float(o[u][2 * k + 1]) * inv);
             w[k] = *reinterpret_cast<uint32_t*>(&b2);
           }
-          if (tok < p.M) {
+          if (store_q) {
             uint4* d4 = reinterpret_cast<uint4*>(dst + c0 + 16 * u);
             d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
             d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
@@ -622,7 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float iv = inv[rr];
         const int row = my_r0 + rr;
         const int tok = m0 + (row >> 3), head = row & 7;
-        if (tok < p.M) {
+        if (tok < p.M && tok - env_start < p.env_rows) {
           uint32_t w4[4];
 #pragma unroll
           for (int z = 0; z < 4; ++z) {
@@ -703,9 +708,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // blocks the tile visits: the prefix blocks plus the suffix blocks covering
   // the segments of its 16 tokens (p.n_blocks is the bound over all tiles)
   auto tile_geom = [&](int tile, int& m0, int& env, int& env_start, int& sb, int& nbt) {
-    m0 = tile * 16;
-    env = m0 / p.env_rows;
+    env = tile / p.tiles_env;
     env_start = env * p.env_rows;
+    m0 = env_start + (tile - env * p.tiles_env) * 16;
     const int lo = m0 - env_start;
     const int seg_first = lo / p.seg_len;
     int hi = min(lo + 15, p.segs * p.seg_len - 1);
@@ -933,6 +938,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int seg_q = local_q / p.seg_len;
       const int t_q = local_q - seg_q * p.seg_len;
       const bool real_q = local_q < p.segs * p.seg_len && tok < p.M;
+      const bool store_q = local_q < p.env_rows && tok < p.M;  // the row's token belongs to this env
       const int seg_lo = seg_q * p.seg_len;
       const int seg_hi = seg_lo + (t_q >= 1 ? p.seg_len : 1);
       float m_used = -INFINITY, l_sum = 0.f;
@@ -1069,7 +1075,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       sm100::tc_fence_before();
       sm100::mbar_arrive(o_free);
-      if (tok < p.M) {
+      if (store_q) {
         __nv_bfloat16* dst = p.out + (size_t)tok * (kHeads * HD) + head * HD + half * 128;
 #pragma unroll
         for (int u4 = 0; u4 < 4; ++u4)
@@ -1209,9 +1215,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = pair_rank();
   const bool leader = rank == 0;
-  const int tiles_env = p.env_rows / 16;
+  const int tiles_env = p.tiles_env;
   const int pairs_env = (tiles_env + 1) / 2;
-  const int n_pairs = (p.M / p.env_rows) * pairs_env;
+  const int n_pairs = p.n_envs * pairs_env;
   const int cl = blockIdx.x >> 1, n_cl = gridDim.x >> 1;
   const int my_pairs = cl < n_pairs ? (n_pairs - 1 - cl) / n_cl + 1 : 0;
   // pair tile -> env, this CTA's first token, validity, first suffix key block
@@ -1514,6 +1520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int seg_q = local_q / p.seg_len;
       const int t_q = local_q - seg_q * p.seg_len;
       const bool real_q = valid && local_q < p.segs * p.seg_len && tok < p.M;
+      const bool store_q = valid && local_q < p.env_rows && tok < p.M;  // the row's token belongs to this env
       const int seg_lo = seg_q * p.seg_len;
       const int seg_hi = seg_lo + (t_q >= 1 ? p.seg_len : 1);
       float m_used = -INFINITY, l_sum = 0.f;
@@ -1626,7 +1633,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       pend = nsb > 0;
       pend_lsum = l_sum;
       pend_tok = tok;
-      pend_store = valid && tok < p.M;
+      pend_store = store_q;
       pend_glast = g - 1;
     }
     if (pend) epilogue(pend_lsum, pend_tok, pend_store, pend_glast, false);

@@ -1,7 +1,7 @@
 // pi0-scale Action Expert: verify chain and Euler full path (sm_100a).
 //
 // Per verify round (B envs x K branches, T = 1 + H suffix tokens per branch,
-// env_rows = round_up(K*T, 16) token rows per env):
+// env_rows = K*T token rows per env, dense; rows padded to 16 at the end):
 //   embed        x_t = tau a + (1-tau) eps (verifier.py:73) -> action_in + temb,
 //                state_proj; fp32 residual X, bf16 copy, RMS partial sums
 //   18 x layer   QKV GEMM (RMS scale + RoPE fused)  -> MQA attention vs the
@@ -713,8 +713,11 @@ int build(Handle& h, Buffers& b, int B, int K) {
   const int nq = c.q_heads * c.head_dim;
   b.B = B;
   b.K = K;
-  b.env_rows = ((K * T + 15) / 16) * 16;
-  b.M = B * b.env_rows;
+  // dense env rows (no per-env padding: the GEMMs see only real tokens; the
+  // attention's 16-token query tiles restart at every env), rows padded to a
+  // multiple of 16 at the end of the batch
+  b.env_rows = K * T;
+  b.M = ((B * b.env_rows + 15) / 16) * 16;
   b.m_ld = ((b.M + 63) / 64) * 64;
   int rc;
 #define ALLOC(ptr, n) \
@@ -768,7 +771,8 @@ int build(Handle& h, Buffers& b, int B, int K) {
   // suffix keys of the (<= 2) segments a 16-token tile touches, from a
   // 64-aligned start: span <= 63 + 2 * T
   const int n_blocks = n_prefix_blocks + (63 + 2 * T + attn::BKEY - 1) / attn::BKEY;
-  b.attn_tiles = b.M / 16;
+  const int tiles_env = (b.env_rows + 15) / 16;
+  b.attn_tiles = B * tiles_env;
   int asplit = 148 / b.attn_tiles;
   if (getenv("SF_ATTN_SPLITS")) asplit = atoi(getenv("SF_ATTN_SPLITS"));  // debug override
   if (asplit < 1) asplit = 1;
@@ -1013,8 +1017,10 @@ int build(Handle& h, Buffers& b, int B, int K) {
   }
   // --- attention plans (per layer: 5 tensor maps)
   attn::Params& ap = b.ap;
-  ap.M = b.M;
+  ap.M = B * b.env_rows;
   ap.env_rows = b.env_rows;
+  ap.n_envs = B;
+  ap.tiles_env = tiles_env;
   ap.seg_len = T;
   ap.segs = K;
   ap.prefix_len = c.prefix_len;
@@ -1052,7 +1058,7 @@ int build(Handle& h, Buffers& b, int B, int K) {
   // 2-SM attention for batched rounds (one split): 128-key superblocks, CTA r
   // of a pair loads key block 2G + r and dims [128 r, 128 r + 128) of V^T
   // (default; SF_ATTN_SINGLE=1 selects the 1-SM persistent kernel)
-  b.attn_pair = b.attn_splits == 1 && b.env_rows / 16 >= 2 && getenv("SF_ATTN_SINGLE") == nullptr;
+  b.attn_pair = b.attn_splits == 1 && tiles_env >= 2 && getenv("SF_ATTN_SINGLE") == nullptr;
   if (b.attn_pair) {
     b.attn_pair_maps.resize(5 * L);
     for (int l = 0; l < L; ++l) {
@@ -1088,7 +1094,7 @@ int launch_attn_pair(const Buffers& b, int l, cudaStream_t s, bool pdl) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   const CUtensorMap* mp = &b.attn_pair_maps[5 * l];
-  const int tiles_env = b.env_rows / 16;
+  const int tiles_env = b.ap.tiles_env;
   const int pairs = b.B * ((tiles_env + 1) / 2);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * (pairs < nsm / 2 ? pairs : nsm / 2));  // persistent: one CTA pair per 2 SMs
@@ -1240,7 +1246,7 @@ int run_stack_f32(Handle& h, Buffers& b, cudaStream_t s) {
     AttnParams ap{b.f_q, b.f_k, b.f_v,
                   h.k_prefix + (size_t)l * h.n_prefix_envs * P * hd,
                   h.vt_prefix + (size_t)l * h.n_prefix_envs * hd * P,
-                  b.env_map, M, c.q_heads, b.env_rows, T, b.K, P, 1.f / sqrtf((float)hd), b.f_o};
+                  b.env_map, M, b.B, c.q_heads, b.env_rows, T, b.K, P, 1.f / sqrtf((float)hd), b.f_o};
     attn_f32_kernel<<<M, 256, attn_smem, s>>>(ap);
     gemm(true, b.f_o, nq, h.w.o[l], W, nq, nullptr, nullptr, b.x, W);
     rms_rows_kernel<<<rms_grid, 256, 0, s>>>(b.x, M, W, c.eps, b.f_rs);
@@ -2251,6 +2257,8 @@ int vlm_build(VlmHandle& h, VlmBuffers& b, int E, void* k_pool, void* vt_pool) {
   attn::Params& ap = b.ap;
   ap.M = b.M;
   ap.env_rows = P;
+  ap.n_envs = E;
+  ap.tiles_env = P / 16;
   ap.seg_len = P;
   ap.segs = 0;
   ap.prefix_len = P;

@@ -129,7 +129,7 @@ struct AttnParams {
   const __nv_bfloat16* kp;       // layer's prefix K pool [E_pool][P][256]
   const __nv_bfloat16* vtp;      // layer's prefix V^T pool [E_pool][256][P]
   const int* env_map;            // [B] pool slot per batch env
-  int M, nh, env_rows, T, K, P;
+  int M, B, nh, env_rows, T, K, P;
   float scale;
   float* o;  // [M][nh * 256]
 };
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(256) attn_f32_kernel(const AttnParams p) {
   const int m = blockIdx.x;
   const int e = m / p.env_rows, local = m - e * p.env_rows;
   float* out = p.o + (size_t)m * p.nh * 256;
-  if (local >= p.K * p.T) {  // padding row
+  if (e >= p.B || local >= p.K * p.T) {  // padding row
     for (int i = threadIdx.x; i < p.nh * 256; i += blockDim.x) out[i] = 0.f;
     return;
   }

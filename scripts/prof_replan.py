@@ -1,5 +1,9 @@
-"""Drive cfg4 replanning rounds for an ncu launch list: warm-up rounds, then
-ONE round between cudaProfilerStart/Stop (run ncu with --profile-from-start off).
+"""ncu launch list of one cfg4 replanning round. ncu cannot profile the kernel
+nodes of a graph that holds conditional nodes (the round's Euler SWITCH), so
+after warm-up rounds the same work is replayed as its two plain graphs between
+cudaProfilerStart/Stop: the flash attempt for every env (sf_ae_flash_round)
+and the 10-step Euler on the bucket the round selected (sf_ae_denoise_envs on
+the compacted fallback envs) -- the kernels the SWITCH body runs.
 
 usage: ncu --profile-from-start off --metrics gpu__time_duration.sum --csv \
          --log-file gpurun_out/replan_launches.csv python scripts/prof_replan.py
@@ -25,11 +29,21 @@ def main():
     for _ in range(4):
         rp.round(obs, ev, ed, st, sg)
     torch.cuda.synchronize()
+    n_fb = int(rp.n_fallback.item())
+    bucket = min(b for b in ([1, 2, 4, 8, 16, 32] + list(range(64, E + 64, 64))) if b >= n_fb)
+    idx = torch.nonzero(rp.path != 0).flatten().to(torch.int32)
+    idx = torch.cat([idx, idx[:1].repeat(bucket - len(idx))]).contiguous()
+    start, state = ed[idx.long()].contiguous(), st[idx.long()].contiguous()
+    for _ in range(2):
+        ae.flash_batch(vc, obs, ev, st, sg, replan_size=bench.REPLAN)
+        ae.denoise_envs(idx, start, state, 10)
+    torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStart()
-    rp.round(obs, ev, ed, st, sg)
+    ae.flash_batch(vc, obs, ev, st, sg, replan_size=bench.REPLAN)
+    ae.denoise_envs(idx, start, state, 10)
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStop()
-    print("fallback envs:", int(rp.n_fallback.item()))
+    print("fallback envs:", n_fb, "bucket:", bucket)
 
 
 if __name__ == "__main__":
