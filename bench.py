@@ -715,6 +715,7 @@ def latency_tiny():
             out[f"spec_round_p50_ms_{prec}"] = host_p50_ms(
                 lambda: flash_attempt(obs, models, policy, state, 1, 7), 300)
             out[f"full_round_p50_ms_{prec}"] = host_p50_ms(lambda: full_round(obs, models, policy, 0, 0, 7), 300)
+    out.update(tiny_kernel_p50(field_net, draft_net, enc_net, h, d, lay.continuous_dims))
     # the reference algorithm on the host (numpy float64)
     fw = [np.asarray(w) for w in field_net.weights]
     fb = [np.asarray(b) for b in field_net.biases]
@@ -745,6 +746,51 @@ def latency_tiny():
     out["cpu_reference_kind"] = "port (oracle/specflow_oracle.py, numpy float64)"
     out["cfg2"] = latency_cfg2()
     return out
+
+
+def tiny_kernel_p50(field_net, draft_net, enc_net, h, d, cdims):
+    """Device time of ONE fused launch (sf_tiny_flash_round: draft + K-branch
+    verify + gate + decision; sf_tiny_full_round: encode + 10 Euler steps) on
+    device-resident inputs, CUDA events around each launch, p50 of 200."""
+    import torch
+
+    from paper_2605_13778_b200 import _capi, _device, precision
+    from paper_2605_13778_b200.verifier import VerifierConfig, make_cfg
+
+    lib = _capi.lib()
+    res = {}
+    for prec in ("fp32", "fp64"):
+        with precision(prec):
+            dt = _device.tdtype()
+            dev = torch.device("cuda")
+            g = torch.Generator(device="cuda").manual_seed(0)
+            feats, emb, state = (torch.randn(n, generator=g, device=dev).to(dt) for n in (10, 39, 3))
+            eps = torch.randn(h * d, generator=g, device=dev).to(dt)
+            outv = torch.empty(h * d * 5, dtype=dt, device=dev)
+            words = torch.empty(32, dtype=torch.int32, device=dev)
+            cfg = make_cfg(VerifierConfig(timesteps=(0.25, 0.5, 0.75), delta=1.42, gripper_window=24), -1.0)
+            es = outv.element_size()
+            o = _capi.SfVerifyOut(outv.data_ptr(), outv.data_ptr() + h * d * es, outv.data_ptr() + 4 * h * d * es,
+                                  words.data_ptr() + 32, words.data_ptr())
+            s_ = torch.cuda.current_stream().cuda_stream
+            dd, fd, ed = draft_net.device().desc, field_net.device().desc, enc_net.device().desc
+
+            def spec():
+                _capi.check(lib.sf_tiny_flash_round(_device.code(), dd, feats.data_ptr(), fd, emb.data_ptr(), 39,
+                                                    state.data_ptr(), 3, eps.data_ptr(), h, d, cdims, cfg, o, s_))
+
+            def full():
+                _capi.check(lib.sf_tiny_full_round(_device.code(), ed, feats.data_ptr(), 39, fd, state.data_ptr(), 3,
+                                                   eps.data_ptr(), h, d, 10, outv.data_ptr(), None, words.data_ptr(),
+                                                   s_))
+
+            for fn in (spec, full):
+                for _ in range(20):
+                    fn()
+            torch.cuda.synchronize()
+            res[f"spec_round_kernel_p50_ms_{prec}"] = p50_ms(spec, 200)
+            res[f"full_round_kernel_p50_ms_{prec}"] = p50_ms(full, 200)
+    return res
 
 
 def latency_cfg2():
