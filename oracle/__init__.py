@@ -10,5 +10,8 @@ baseline — never as the thing measured or shipped.
   function citing the reference file:line it follows. Pinned against golden
   vectors produced by the real reference (``tests/golden/make_golden.py``).
 * ``pi0_oracle`` — numpy restatement of the pi0-scale Action Expert the
-  builder defined (no reference implementation exists; see its header).
+  builder defined (no reference implementation exists; see its header), in a
+  bf16-mirroring and an unrounded fp32 precision mode.
+* ``pi0_torch`` — the same model vectorised in torch (full-size checks in
+  seconds), pinned to ``pi0_oracle`` by ``tests/test_oracle_torch_cpu.py``.
 """

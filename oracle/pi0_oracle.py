@@ -17,9 +17,12 @@ Precision model (identical rounding points to the device path):
   * q, k (after RoPE), v, softmax P, attention output and GeGLU output are
     rounded to bf16 where the device stores them;
   * the action head output (velocity) is fp32.
+``field_velocity(..., bf16_points=False)`` is the unrounded fp32 model (same
+bf16-valued weights and KV, activations never rounded): the north star's
+precision reference and the fp32 mode's (SF_AE_FP32) target.
 Parity is "unpinned" against any external reference for this model (there is
-none); GPU parity is checked against this oracle at reduced depth/width and
-through size-independent properties at full size.
+none); GPU parity is checked against this oracle at reduced depth/width and,
+through its torch port (oracle/pi0_torch.py), at full cfg3/cfg4 size.
 """
 
 from __future__ import annotations
