@@ -905,17 +905,12 @@ int build(Handle& h, Buffers& b, int B, int K) {
   // then as many K splits as keep one wave with clusters <= 6 CTAs (8- and
   // 16-CTA clusters schedule poorly). SF_TUNE=1 times candidates instead.
   if (swap && getenv("SF_TUNE") == nullptr) {
-    // experiment (SF_HALF_GRID=n): every GEMM grid <= n CTAs, so the next
-    // kernel's CTAs (PDL) are resident on the free SMs while this one runs
-    const int cap = getenv("SF_HALF_GRID") ? atoi(getenv("SF_HALF_GRID")) : nsm;
+    const int bn = b.M > 128 ? (((b.M + 1) / 2 + 15) / 16) * 16 : bn_swap;
+    const int tiles_b = (b.M + bn - 1) / bn;
     for (int cls = 0; cls < 4; ++cls) {
       const Spec& sp = specs[cls];
-      int bn = b.M > 128 ? (((b.M + 1) / 2 + 15) / 16) * 16 : bn_swap;
-      const int tiles_a = (sp.n_out + gemm::BM - 1) / gemm::BM;
-      if (tiles_a * ((b.M + bn - 1) / bn) > cap) bn = bn_swap;  // one token tile
-      const int tiles_b = (b.M + bn - 1) / bn;
-      const int tiles = tiles_a * tiles_b, nkb = sp.k_in / gemm::BK;
-      int S = cap / tiles;
+      const int tiles = ((sp.n_out + gemm::BM - 1) / gemm::BM) * tiles_b, nkb = sp.k_in / gemm::BK;
+      int S = nsm / tiles;
       // 8-CTA clusters only while they fill at most half the GPU
       S = S > 8 ? 8 : (S < 1 ? 1 : S);
       if (S > 6 && tiles * S > nsm / 2) S = 6;
