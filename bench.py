@@ -332,11 +332,14 @@ def run_dry(args, rank, world):
 
 # --------------------------------------------------------------- GPU side
 
-def audit(ae, vcfg, lo, draft, recon, dist, branch, result, eps_v, state, signs, envs_local, dev):
+def audit(ae, vcfg, lo, draft, recon, dist, branch, result, eps_v, state, signs, envs_local, dev,
+          round_chunk=None, round_path=None, eps_d=None):
     """Re-verify sampled envs with the oracle after the timed region: device
     draft vs the oracle draft; decisions vs the bf16-mirroring oracle (flips
     counted with their distance to delta, |d - delta| < 1e-4 reported as
-    near-threshold); endpoints vs the unrounded fp32 model."""
+    near-threshold); endpoints vs the unrounded fp32 model; and the executed
+    chunk of (up to 2) sampled envs that fell back in the last replanning round
+    vs the oracle's 10-step Euler (flowpolicy.py:273-292) on the fp32 model."""
     import numpy as np
 
     from oracle import pi0_oracle as po
@@ -386,7 +389,23 @@ def audit(ae, vcfg, lo, draft, recon, dist, branch, result, eps_v, state, signs,
     err, refa = np.stack(errs), np.stack(refs)
     rms = float(np.sqrt((refa ** 2).mean()))
     typ = np.abs(refa) >= rms
+    euler = []
+    if round_chunk is not None:
+        paths = round_path.cpu().numpy()
+        for j, i in enumerate(sel):
+            if paths[i] == 0 or len(euler) == 2:
+                continue
+            e_idx = [j]
+            st1 = state[i:i + 1]
+            want = so.integrate_flow(
+                lambda x, t: ref.velocity(torch.from_numpy(x.astype(np.float32))[None, None].to(dev), (t,), st1,
+                                          mirror_bf16=False, env_index=e_idx)[0, 0].double().cpu().numpy(),
+                eps_d[i].double().cpu().numpy(), 10)
+            got = round_chunk[i].double().cpu().numpy()
+            euler.append({"env": lo + int(i), "rel_norm_err_vs_fp32": float(np.linalg.norm(got - want) /
+                                                                             np.linalg.norm(want))})
     return {"checked_envs": ids, "flips": flips, "flip_margins": margins, "near_threshold": int(near),
+            "fallback_chunk_vs_fp32_euler": euler,
             "dist_max_abs_err_vs_bf16_oracle": derr,
             "recon_max_err_over_rms_vs_fp32": float(np.abs(err).max() / rms),
             "recon_max_rel_err_typical_vs_fp32": float((np.abs(err) / np.abs(refa))[typ].max()),
@@ -533,7 +552,11 @@ def run_ours(args, rank, world, local):
                 "achieved": gu_tflops, "peak": tc_peak, "unit": "TFLOP/s", "frac": gu_tflops / tc_peak,
                 "traffic": traffic, "traffic_source": "profiles/ncu_summary.json (ncu --set full capture)",
                 "peak_kind": f"{peak_kind} burst bf16", "algorithmic_flops_per_launch": gu_flops,
-                "ms_per_launch": gu_ms, "ms_per_launch_in_step_ncu": in_step}
+                "ms_per_launch": gu_ms, "ms_per_launch_in_step_ncu": in_step,
+                "frac_in_step_ncu": (gu_flops / (in_step / 1e3) / 1e12 / tc_peak) if in_step else None,
+                "timing_note": "achieved/frac from back-to-back launches of the planned layer-0 op (CUDA events); "
+                               "frac_in_step_ncu from the kernel's duration inside a replanning round under "
+                               "ncu (profiles/ncu_summary.json r2, ~1.42 GHz)"}
 
     # algorithmic FLOPs: flash attempt for every env + 10-step Euler for each fallback env
     T = cfg.seg_len
@@ -597,7 +620,7 @@ def run_ours(args, rank, world, local):
         sample = sorted({int(round(i * (E - 1) / max(n - 1, 1))) for i in range(n)})
         try:
             line["parity"] = audit(ae, vcfg, lo, outs[0], outs[1], outs[2], outs[3], outs[4], eps_v, state,
-                                   signs, sample, dev)
+                                   signs, sample, dev, rp.chunk, rp.path, eps_d)
         except Exception as exc:  # the audit must never hide the timing line
             line["parity"] = {"error": repr(exc)}
 

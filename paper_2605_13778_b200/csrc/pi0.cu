@@ -359,6 +359,11 @@ struct StatusParams {
   int B;
 };
 
+// dst[0 .. n) = v (the per-env gripper sign when the caller passes one sign)
+__global__ void fill_f32_kernel(float* dst, int n, float v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = v;
+}
+
 __global__ void status_init_kernel(const StatusParams p) {
   for (int e = threadIdx.x; e < p.B; e += blockDim.x) {
     p.status[2 * e] = -1;
@@ -1632,10 +1637,10 @@ static int verify_common(Handle* h, int n_envs, const sf_verify_cfg_t* cfg, cons
                                 cudaMemcpyDeviceToDevice, s));
   if (signs) {
     SF_CHECK_CUDA(cudaMemcpyAsync(b->signs, signs, n_envs * 4, cudaMemcpyDeviceToDevice, s));
-  } else {
-    std::vector<float> hs(n_envs, (float)cfg->current_sign);
-    SF_CHECK_CUDA(cudaMemcpyAsync(b->signs, hs.data(), n_envs * 4, cudaMemcpyHostToDevice, s));
-    SF_CHECK_CUDA(cudaStreamSynchronize(s));  // hs is a host temporary
+  } else {  // one sign for every env: filled on the stream (no host staging, no sync)
+    fill_f32_kernel<<<(n_envs + 255) / 256, 256, 0, s>>>(b->signs, n_envs, (float)cfg->current_sign);
+    SF_CHECK_CUDA(cudaGetLastError());
+    sf::count_launch();
   }
   const bool pdl = (flags & SF_AE_PDL) != 0;
   if (flags & SF_AE_GRAPH) {
