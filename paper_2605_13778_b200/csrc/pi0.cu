@@ -1743,6 +1743,28 @@ extern "C" int sf_ae_denoise_envs(void* handle, int n_envs, const int* env_map, 
                                   const float* start, const float* state, float* chunk_out,
                                   int* status, int flags, void* stream);
 
+// Euler time embeddings for tau_i = i / N; every captured denoise graph and
+// replanning graph baked the previous table's pointer, so all are dropped.
+static int set_euler_steps(Handle& h, int num_steps, cudaStream_t s) {
+  if (h.temb_euler_n == num_steps) return SF_OK;
+  int rc;
+  h.replans.clear();
+  for (auto& kv : h.buffers)
+    if (kv.second->graph && kv.second->graph_key & 0x40000000) {
+      cudaGraphExecDestroy(kv.second->graph);
+      kv.second->graph = nullptr;
+    }
+  if (h.temb_euler) cudaFree(h.temb_euler);
+  h.temb_euler = nullptr;
+  if ((rc = dalloc(&h.temb_euler, (size_t)num_steps * h.cfg.width))) return rc;
+  std::vector<float> taus(num_steps);
+  for (int i = 0; i < num_steps; ++i) taus[i] = (float)((double)i / (double)num_steps);
+  if ((rc = compute_temb(h, taus.data(), num_steps, h.temb_euler, s))) return rc;
+  SF_CHECK_CUDA(cudaStreamSynchronize(s));
+  h.temb_euler_n = num_steps;
+  return SF_OK;
+}
+
 extern "C" int sf_ae_denoise(void* handle, int n_envs, int num_steps, const float* start,
                              const float* state, float* chunk_out, int* status, int flags,
                              void* stream) {
@@ -1763,19 +1785,7 @@ extern "C" int sf_ae_denoise_envs(void* handle, int n_envs, const int* env_map, 
   Buffers* b = get_buffers(*h, n_envs, 1, 1 | ((flags & SF_AE_FP32) ? kModeF32 : 0), &rc);
   if (!b) return rc;
   const sf_ae_config_t& c = h->cfg;
-  if (h->temb_euler_n != num_steps) {
-    if (h->temb_euler) cudaFree(h->temb_euler);
-    if ((rc = dalloc(&h->temb_euler, (size_t)num_steps * c.width))) return rc;
-    std::vector<float> taus(num_steps);
-    for (int i = 0; i < num_steps; ++i) taus[i] = (float)((double)i / (double)num_steps);
-    if ((rc = compute_temb(*h, taus.data(), num_steps, h->temb_euler, s))) return rc;
-    SF_CHECK_CUDA(cudaStreamSynchronize(s));
-    h->temb_euler_n = num_steps;
-    if (b->graph) {
-      cudaGraphExecDestroy(b->graph);
-      b->graph = nullptr;
-    }
-  }
+  if ((rc = set_euler_steps(*h, num_steps, s))) return rc;
   const size_t hd = (size_t)n_envs * c.horizon * c.action_dim;
   // batch env e attends to pool slot env_map[e] (fallback envs compacted by
   // sf_replan_update); identity when no map is given
@@ -1978,21 +1988,7 @@ extern "C" int sf_ae_replan_round(void* handle, int n_envs, const sf_verify_cfg_
   cudaStream_t s = (cudaStream_t)stream;
   const sf_ae_config_t& c = h->cfg;
   if ((rc = ensure_temb(*h, cfg, s))) return rc;
-  if (h->temb_euler_n != policy->num_steps) {
-    if (h->temb_euler) cudaFree(h->temb_euler);
-    if ((rc = dalloc(&h->temb_euler, (size_t)policy->num_steps * c.width))) return rc;
-    std::vector<float> taus(policy->num_steps);
-    for (int i = 0; i < policy->num_steps; ++i) taus[i] = (float)((double)i / (double)policy->num_steps);
-    if ((rc = compute_temb(*h, taus.data(), policy->num_steps, h->temb_euler, s))) return rc;
-    SF_CHECK_CUDA(cudaStreamSynchronize(s));
-    h->temb_euler_n = policy->num_steps;
-    for (auto& kv : h->buffers)
-      if (kv.second->graph) {  // denoise graphs baked the old time embedding
-        cudaGraphExecDestroy(kv.second->graph);
-        kv.second->graph = nullptr;
-      }
-    h->replans.clear();
-  }
+  if ((rc = set_euler_steps(*h, policy->num_steps, s))) return rc;
   const bool pdl = (flags & SF_AE_PDL) != 0, fp32 = (flags & SF_AE_FP32) != 0;
   uint64_t key = 1469598103934665603ull;
   auto mix = [&](const void* q, size_t nb) {

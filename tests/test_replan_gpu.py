@@ -191,3 +191,59 @@ def test_replan_round_no_host_sync_and_launch_accounting():
     assert _capi.launch_count() > c0
     torch.cuda.synchronize()
     assert dt < 0.05, f"round blocked the host for {dt * 1e3:.1f} ms"
+
+
+def test_replan_round_full_only_and_single_env():
+    """mode_flash = 0 (RuntimePolicy.mode == full_only): every round is a full
+    round (path FULL, planned R) and the chunk is the Euler path; one env
+    (bucket set {1}) goes through the same graph."""
+    import torch
+
+    from paper_2605_13778_b200 import _capi, pi0
+    from paper_2605_13778_b200.verifier import VerifierConfig
+
+    dcfg = pi0.AEConfig(**SMALL)
+    for n in (1, 5):
+        ae = pi0.ActionExpert(dcfg, seed=0, n_envs=n, kv_seed=1)
+        vc = VerifierConfig(timesteps=(0.25, 0.5, 0.75), delta=2.5, gripper_window=6)
+        rp = pi0.BatchedReplanner(ae, n, vc, replan_size=4, periodic_refresh=2, flash=False)
+        g = torch.Generator(device="cuda").manual_seed(n)
+        H, D, S = dcfg.horizon, dcfg.action_dim, dcfg.state_dim
+        mk = lambda *sh: torch.randn(sh, generator=g, device="cuda")
+        for _ in range(3):
+            obs, ev, ed, st = mk(n, dcfg.draft_in), mk(n, H, D), mk(n, H, D), mk(n, S)
+            chunk, path, planned, _, _ = rp.round(obs, ev, ed, st, torch.ones(n, device="cuda"))
+            assert (path == _capi.SF_PATH_FULL).all() and (planned == 4).all()
+            assert int(rp.n_fallback.item()) == n
+            full, _ = ae.denoise_batch(ed, st, 10)
+            torch.testing.assert_close(chunk, full, rtol=2e-3, atol=2e-3 * full.abs().max().item())
+
+
+def test_replan_round_fp32_mode():
+    """The replanning round in the fp32 mode (SF_AE_FP32): bookkeeping as
+    run_episode, fallback chunks equal to the fp32-mode Euler of those envs."""
+    import torch
+
+    from paper_2605_13778_b200 import pi0
+    from paper_2605_13778_b200.verifier import VerifierConfig
+
+    dcfg = pi0.AEConfig(**SMALL)
+    n = 6
+    ae = pi0.ActionExpert(dcfg, seed=0, n_envs=n, kv_seed=1, draft_gripper_bias=6.0, precision="fp32")
+    vc = VerifierConfig(timesteps=(0.25, 0.5, 0.75), delta=2.5, gripper_window=6)
+    rp = pi0.BatchedReplanner(ae, n, vc, replan_size=4, periodic_refresh=2)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    H, D, S = dcfg.horizon, dcfg.action_dim, dcfg.state_dim
+    mk = lambda *sh: torch.randn(sh, generator=g, device="cuda")
+    signs = torch.where(torch.arange(n, device="cuda") % 2 == 0, 1.0, -1.0)
+    for r in range(3):
+        obs, ev, ed, st = mk(n, dcfg.draft_in), mk(n, H, D), mk(n, H, D), mk(n, S)
+        fsr0, hc0 = rp.fsr.cpu().numpy(), rp.has_cache.cpu().numpy()
+        chunk, path, planned, _, result = rp.round(obs, ev, ed, st, signs)
+        want_path, want_planned, idx = _replan_ref(result.cpu().numpy(), fsr0, hc0, 2, 4)
+        np.testing.assert_array_equal(path.cpu().numpy(), want_path)
+        np.testing.assert_array_equal(planned.cpu().numpy(), want_planned)
+        if len(idx):
+            m = torch.from_numpy(idx.astype(np.int32)).cuda()
+            full, _ = ae.denoise_envs(m, ed[m.long()], st[m.long()], 10)
+            torch.testing.assert_close(chunk[m.long()], full, rtol=1e-5, atol=1e-5 * full.abs().max().item())
