@@ -508,28 +508,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   if (p.splits > 1) {
-    // Split-KV merge through L2: every split writes its unnormalised partial
-    // O in bf16 (the merged output is bf16 too; writes are the slow side of
-    // L2, ~35 GB/s per SM) as [HD/8 octets][128 rows] uint4 (each warp store
-    // is 512 contiguous bytes) plus fp32 (m, l) per row; after one cluster
-    // barrier (release/acquire at cluster scope orders the global stores)
-    // cluster rank s merges rows [s*rows, (s+1)*rows) in a fixed split order
-    // (deterministic), accumulating in fp32.
+    // Split-KV merge over DSMEM (the S split CTAs of a tile are one cluster):
+    // cluster rank t owns query rows [t*rows, t*rows + rows). After every
+    // CTA's MMAs retired (cluster barrier 1: the K/V stage region is free),
+    // each split pushes its unnormalised bf16 O rows and fp32 (m, l) straight
+    // into the owner's SMEM ([split][HD/8 octets][rows] uint4, rows fastest:
+    // conflict-free), cluster barrier 2 (release / acquire at cluster scope)
+    // makes them visible, and the owner merges its rows from local SMEM in
+    // a fixed split order (deterministic), accumulating in fp32. No L2
+    // round trip for the partials.
     cg::cluster_group cluster = cg::this_cluster();
     const int S = p.splits;
     const int rows = (BQ + S - 1) / S;
     const int my_r0 = split * rows;
     const int my_nr = max(0, min(BQ, my_r0 + rows) - my_r0);
-    const size_t part_words = (size_t)HD * BQ / 2;  // bf16 pairs per (tile, split)
-    uint4* ws_o = reinterpret_cast<uint4*>(p.ws);  // [(tile*S + s)][HD/8][BQ]
-    float2* ws_ml = reinterpret_cast<float2*>(p.ws + (size_t)p.tiles * S * part_words);
+    uint4* recv_o = reinterpret_cast<uint4*>(sKV);                                  // [S][HD/8][rows]
+    float2* recv_ml = reinterpret_cast<float2*>(sKV + (size_t)S * (HD / 8) * rows * 16);  // [S][rows]
+    if (threadIdx.x == 64) ATT_STAMP(5);
+    cluster.sync();  // every split's MMAs retired: the peers' K/V regions are free
     if (warp >= 2) {
       const int q = warp & 3;
       const int half = (warp - 2) >> 2;
       const int r = q * 32 + lane;
       const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
-      uint4* dst = ws_o + (size_t)(tile * S + split) * (HD / 8) * BQ + r;
-      if (half == 0) ws_ml[(size_t)(tile * S + split) * BQ + r] = make_float2(m_fin, l_fin);
+      const int owner = r / rows, rr = r - owner * rows;
+      uint4* dst_o = cluster.map_shared_rank(recv_o, owner) + (size_t)split * (HD / 8) * rows + rr;
+      if (half == 0)
+        *(cluster.map_shared_rank(recv_ml, owner) + split * rows + rr) = make_float2(m_fin, l_fin);
 #pragma unroll 1
       for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 64) {
         uint32_t o[4][16];
@@ -547,96 +552,57 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                         __uint_as_float(o[u][k + 2 * z + 1]));
               w[z] = *reinterpret_cast<uint32_t*>(&b2);
             }
-            __stcg(dst + (size_t)((c0 + 16 * u + k) >> 3) * BQ, make_uint4(w[0], w[1], w[2], w[3]));
+            dst_o[(size_t)((c0 + 16 * u + k) >> 3) * rows] = make_uint4(w[0], w[1], w[2], w[3]);
           }
       }
     }
-    if (threadIdx.x == 64) ATT_STAMP(5);
-    cluster.sync();
+    cluster.sync();  // the partials of every split are in this CTA's SMEM
     if (threadIdx.x == 64) ATT_STAMP(6);
     // merge weights: wgt[row][s] = 2^(m_s - max_s m_s), inv[row] = 1 / sum_s wgt l_s
     float* wgt = reinterpret_cast<float*>(sP);  // [rows][S]
     float* inv = wgt + BQ * kMaxSplitsKV;       // [rows]
     if (threadIdx.x < my_nr) {
-      const int row = my_r0 + threadIdx.x;
-      float2 ml[kMaxSplitsKV];
-#pragma unroll
-      for (int s2 = 0; s2 < kMaxSplitsKV; ++s2)
-        if (s2 < S) ml[s2] = __ldcg(ws_ml + (size_t)(tile * S + s2) * BQ + row);
       float mx = -INFINITY;
-#pragma unroll
-      for (int s2 = 0; s2 < kMaxSplitsKV; ++s2)
-        if (s2 < S) mx = fmaxf(mx, ml[s2].x);
+      for (int s2 = 0; s2 < S; ++s2) mx = fmaxf(mx, recv_ml[s2 * rows + threadIdx.x].x);
       float L = 0.f;
-#pragma unroll
-      for (int s2 = 0; s2 < kMaxSplitsKV; ++s2)
-        if (s2 < S) {
-          const float w = ml[s2].x > -INFINITY ? exp2f(ml[s2].x - mx) : 0.f;
-          wgt[threadIdx.x * kMaxSplitsKV + s2] = w;
-          L += w * ml[s2].y;
-        }
+      for (int s2 = 0; s2 < S; ++s2) {
+        const float2 ml = recv_ml[s2 * rows + threadIdx.x];
+        const float w = ml.x > -INFINITY ? exp2f(ml.x - mx) : 0.f;
+        wgt[threadIdx.x * kMaxSplitsKV + s2] = w;
+        L += w * ml.y;
+      }
       inv[threadIdx.x] = L > 0.f ? 1.f / L : 0.f;
     }
     __syncthreads();
-    // (row, octet) outputs: rows fastest so the split loads are contiguous runs;
-    // unconditional (clamped) loads keep every split's octet in registers
     const int total = my_nr * (HD / 8);
-    constexpr int IT = 3;  // items per thread per round: all their split loads in flight at once
-    for (int base = threadIdx.x; base < total; base += IT * kThreads) {
-      float a[IT][8];
+    for (int idx = threadIdx.x; idx < total; idx += kThreads) {
+      const int rr = idx % my_nr, c8 = idx / my_nr;
+      float a[8];
 #pragma unroll
-      for (int it = 0; it < IT; ++it)
+      for (int z = 0; z < 8; ++z) a[z] = 0.f;
+      for (int s2 = 0; s2 < S; ++s2) {
+        const uint4 v = recv_o[((size_t)s2 * (HD / 8) + c8) * rows + rr];
+        const float w = wgt[rr * kMaxSplitsKV + s2];
+        const uint32_t pk[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int z = 0; z < 8; ++z) a[it][z] = 0.f;
-      for (int s0 = 0; s0 < S; s0 += 8) {
-        uint4 v[IT][8];
-#pragma unroll
-        for (int it = 0; it < IT; ++it) {
-          const int idx = min(base + it * kThreads, total - 1);
-          const int rr = idx % my_nr, c8 = idx / my_nr;
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int su = min(s0 + u, S - 1);
-            v[it][u] = __ldcg(ws_o + ((size_t)(tile * S + su) * (HD / 8) + c8) * BQ + my_r0 + rr);
-          }
-        }
-#pragma unroll
-        for (int it = 0; it < IT; ++it) {
-          const int idx = min(base + it * kThreads, total - 1);
-          const int rr = idx % my_nr;
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (s0 + u < S) {
-              const float w = wgt[rr * kMaxSplitsKV + s0 + u];
-              const uint32_t pk[4] = {v[it][u].x, v[it][u].y, v[it][u].z, v[it][u].w};
-#pragma unroll
-              for (int z = 0; z < 4; ++z) {
-                const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&pk[z]);
-                const float2 f = __bfloat1622float2(b2);
-                a[it][2 * z] += w * f.x;
-                a[it][2 * z + 1] += w * f.y;
-              }
-            }
+        for (int z = 0; z < 4; ++z) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[z]));
+          a[2 * z] += w * f.x;
+          a[2 * z + 1] += w * f.y;
         }
       }
+      const float iv = inv[rr];
+      const int row = my_r0 + rr;
+      const int tok = m0 + (row >> 3), head = row & 7;
+      if (tok < p.M && tok - env_start < p.env_rows) {
+        uint32_t w4[4];
 #pragma unroll
-      for (int it = 0; it < IT; ++it) {
-        const int idx = base + it * kThreads;
-        if (idx >= total) break;
-        const int rr = idx % my_nr, c8 = idx / my_nr;
-        const float iv = inv[rr];
-        const int row = my_r0 + rr;
-        const int tok = m0 + (row >> 3), head = row & 7;
-        if (tok < p.M && tok - env_start < p.env_rows) {
-          uint32_t w4[4];
-#pragma unroll
-          for (int z = 0; z < 4; ++z) {
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(a[it][2 * z] * iv, a[it][2 * z + 1] * iv);
-            w4[z] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-          *reinterpret_cast<uint4*>(p.out + (size_t)tok * (kHeads * HD) + head * HD + 8 * c8) =
-              make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        for (int z = 0; z < 4; ++z) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(a[2 * z] * iv, a[2 * z + 1] * iv);
+          w4[z] = *reinterpret_cast<uint32_t*>(&b2);
         }
+        *reinterpret_cast<uint4*>(p.out + (size_t)tok * (kHeads * HD) + head * HD + 8 * c8) =
+            make_uint4(w4[0], w4[1], w4[2], w4[3]);
       }
     }
     if (threadIdx.x == 64) ATT_STAMP(7);
