@@ -6,6 +6,8 @@
 #ifndef SPECFLOW_B200_INTERNAL_H
 #define SPECFLOW_B200_INTERNAL_H
 
+#include <stddef.h>
+
 #include "specflow_b200.h"
 
 #ifdef __cplusplus
@@ -32,6 +34,11 @@ int sf_dbg_gemm_trace(const void* A, int rows_a, const void* B, int rows_b, int 
 int sf_dbg_gemm_time(const void* A, int rows_a, const void* B, int rows_b, int K, int bn,
                      int splits, int swap_ab, void* out, int iters, int pdl, float* us,
                      void* stream);
+
+/* Per-stage %globaltimer stamps of the last batch-1 engine launch run with
+ * SF_B1_TRACE set: [148 CTAs][stages][4] (stage start, operand ready,
+ * accumulator / softmax done, stage done), copied to host `out` (n entries). */
+int sf_ae_b1_trace(void* ae_handle, unsigned long long* out, size_t n);
 
 #ifdef __cplusplus
 }

@@ -124,6 +124,7 @@ SIGNATURES = {
                          ctypes.c_float, _P]),
     "sf_dbg_gemm_time": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P, _P]),
     "sf_dbg_gemm_trace": (_I, [_P, _I, _P, _I, _I, _I, _I, _P, _P, _P]),
+    "sf_ae_b1_trace": (_I, [_P, _P, ctypes.c_size_t]),
 }
 
 _lib = None

@@ -27,11 +27,13 @@
 #include <vector>
 
 #include "attention.cuh"
+#include "b1engine.cuh"
 #include "common.cuh"
 #include "gemm_host.h"
 #include "gemm.cuh"
 #include "stack_f32.cuh"
 #include "replan.cuh"
+#include "specflow_b200_internal.h"
 #include "specflow_b200_pi0.h"
 #include "verify_epi.cuh"
 
@@ -611,6 +613,7 @@ struct Handle {
   std::map<uint64_t, std::unique_ptr<struct Replan>> replans;
   cudaStream_t capture_stream = nullptr;
   cudaStream_t body_stream = nullptr;  // conditional-body captures
+  struct B1Engine* b1 = nullptr;       // persistent batch-1 Euler engine (lazy)
 };
 
 // Graph-resident replanning round (sf_ae_replan_round): owned device buffers
@@ -1515,6 +1518,196 @@ static void free_buffers(Handle* h) {
   h->buffers.clear();
 }
 
+namespace sf {
+namespace pi0 {
+// ----------------------------------------------------------- batch-1 engine
+// The persistent one-launch Euler full path (b1engine.cuh) for n_envs == 1:
+// device buffers + weight tensor maps, built on first use.
+struct B1Engine {
+  b1::Params p{};
+  float *x = nullptr, *acc_qkv = nullptr, *acc_gu = nullptr, *acc_head = nullptr, *ssq = nullptr, *A = nullptr;
+  bf16 *part_o = nullptr, *qb = nullptr, *kb = nullptr, *vt = nullptr, *xb = nullptr, *hb = nullptr;
+  unsigned* cnt = nullptr;
+  size_t ssq_n = 0;
+  float2* part_ml = nullptr;
+  unsigned* bar = nullptr;
+  unsigned long long* dbg = nullptr;
+  size_t dbg_n = 0;
+};
+
+static void destroy_b1(Handle* h) {
+  if (!h->b1) return;
+  B1Engine& e = *h->b1;
+  void* ptrs[] = {e.x, e.acc_qkv, e.acc_gu, e.acc_head, e.ssq, e.A, e.part_o, e.part_ml, e.bar, e.dbg,
+                  e.qb, e.kb, e.vt, e.xb, e.hb, e.cnt};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  delete h->b1;
+  h->b1 = nullptr;
+}
+
+// The engine's static plan is written for the pi0-scale geometry (width 1024,
+// 8 x 256 heads, GeGLU 4096, <= 64 suffix tokens) on a 148-SM part.
+static bool b1_supported(const Handle& h) {
+  const sf_ae_config_t& c = h.cfg;
+  if (getenv("SF_NO_B1ENGINE")) return false;
+  if (c.width != b1::kW || c.q_heads != b1::kHeads || c.head_dim != b1::kHD || c.mlp != b1::kMlp) return false;
+  if (c.horizon + 1 > b1::kTok || c.action_dim % 4 != 0 || c.action_dim > 32 || c.layers > b1::kMaxL) return false;
+  if (!h.k_img || c.prefix_len < 64) return false;
+  static int nsm = -1;
+  if (nsm < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return nsm >= b1::kGrid;
+}
+
+static int build_b1(Handle& h) {
+  if (h.b1) return SF_OK;
+  const sf_ae_config_t& c = h.cfg;
+  auto e = std::make_unique<B1Engine>();
+  int rc;
+  const int L = c.layers, T = 1 + c.horizon;
+  if ((rc = dalloc(&e->x, (size_t)b1::kTok * b1::kW)) || (rc = dalloc(&e->acc_qkv, (size_t)b1::kTok * b1::kQKV)) ||
+      (rc = dalloc(&e->acc_gu, (size_t)b1::kTok * 2 * b1::kMlp)) ||
+      (rc = dalloc(&e->acc_head, (size_t)b1::kTok * c.action_dim)) ||
+      (rc = dalloc(&e->ssq, (size_t)(2 * L + 1) * b1::kTok)) ||
+      (rc = dalloc(&e->xb, (size_t)b1::kTok * b1::kW)) || (rc = dalloc(&e->hb, (size_t)b1::kTok * b1::kMlp)) ||
+      (rc = dalloc(&e->cnt, (size_t)8 * 64)) ||
+      (rc = dalloc(&e->A, (size_t)2 * c.horizon * c.action_dim)) ||
+      (rc = dalloc(&e->part_o, (size_t)b1::kAttQT * b1::kAttSplits * 128 * b1::kHD)) ||
+      (rc = dalloc(&e->part_ml, (size_t)b1::kAttQT * b1::kAttSplits * 128)) || (rc = dalloc(&e->bar, 64)) ||
+      (rc = dalloc(&e->qb, (size_t)b1::kTok * b1::kQF)) || (rc = dalloc(&e->kb, (size_t)b1::kTok * b1::kHD)) ||
+      (rc = dalloc(&e->vt, (size_t)b1::kHD * b1::kTok)))
+    return rc;
+  b1::Params& p = e->p;
+  for (int l = 0; l < L; ++l) {
+    if ((rc = gemm::make_map(&p.wmap[4 * l + 0], h.w.qkv[l], b1::kQKV, b1::kW, b1::kW, 128)) ||
+        (rc = gemm::make_map(&p.wmap[4 * l + 1], h.w.o[l], b1::kW, b1::kQF, b1::kQF, 128)) ||
+        (rc = gemm::make_map(&p.wmap[4 * l + 2], h.w.gu[l], 2 * b1::kMlp, b1::kW, b1::kW, 128)) ||
+        (rc = gemm::make_map(&p.wmap[4 * l + 3], h.w.down[l], b1::kW, b1::kMlp, b1::kMlp, 128)) ||
+        (rc = gemm::make_map(&p.wmap64[2 * l + 0], h.w.qkv[l], b1::kQKV, b1::kW, b1::kW, 64)) ||
+        (rc = gemm::make_map(&p.wmap64[2 * l + 1], h.w.gu[l], 2 * b1::kMlp, b1::kW, b1::kW, 64)))
+      return rc;
+  }
+  if ((rc = gemm::make_map(&p.wmap[4 * L], h.w.out_w, c.action_dim, b1::kW, b1::kW, 128)) ||
+      (rc = gemm::make_map(&p.qmap, e->qb, b1::kTok * b1::kHeads, b1::kHD, b1::kHD, 128)) ||
+      (rc = gemm::make_map(&p.kmap, e->kb, b1::kTok, b1::kHD, b1::kHD, 64)) ||
+      (rc = gemm::make_map(&p.vmap, e->vt, b1::kHD, b1::kTok, b1::kTok, 256)) ||
+      (rc = gemm::make_map(&p.xmap, e->xb, b1::kTok, b1::kW, b1::kW, 64)) ||
+      (rc = gemm::make_map(&p.hmap, e->hb, b1::kTok, b1::kMlp, b1::kMlp, 64)) ||
+      (rc = gemm::make_map(&p.pmap, e->part_o, b1::kAttQT * b1::kAttSplits * 128, b1::kHD, b1::kHD, 128)))
+    return rc;
+  e->ssq_n = (size_t)(2 * L + 1) * b1::kTok;
+  p.xb = e->xb;
+  p.hb = e->hb;
+  p.cnt = e->cnt;
+  p.qb = e->qb;
+  p.kb = e->kb;
+  p.vt = e->vt;
+  p.L = L;
+  p.T = T;
+  p.H = c.horizon;
+  p.D = c.action_dim;
+  p.S = c.state_dim;
+  p.P = c.prefix_len;
+  p.npb = (c.prefix_len + 63) / 64;
+  // KV splits over npb prefix blocks + 1 suffix block; the last split holds
+  // the suffix block and at most one prefix block (its worker-written ring
+  // items must fit the 4-slot ring at the task start)
+  {
+    const int nbk = p.npb + 1;
+    const int last = p.npb >= 1 ? 2 : 1;
+    const int rest = nbk - last, per = (rest + b1::kAttSplits - 2) / (b1::kAttSplits - 1);
+    p.att_b[0] = 0;
+    for (int s = 1; s < b1::kAttSplits; ++s) p.att_b[s] = std::min(rest, p.att_b[s - 1] + per);
+    p.att_b[b1::kAttSplits] = nbk;
+  }
+  p.inv_width = 1.f / (float)c.width;
+  p.eps = c.eps;
+  p.scale_log2 = 1.4426950408889634f / sqrtf((float)c.head_dim);
+  p.rope = static_cast<const float2*>(h.w.rope);
+  p.a_w = static_cast<const float*>(h.w.a_w);
+  p.a_b = static_cast<const float*>(h.w.a_b);
+  p.s_w = static_cast<const float*>(h.w.s_w);
+  p.s_b = static_cast<const float*>(h.w.s_b);
+  p.out_b = static_cast<const float*>(h.w.out_b);
+  p.x = e->x;
+  p.acc_qkv = e->acc_qkv;
+  p.acc_gu = e->acc_gu;
+  p.acc_head = e->acc_head;
+  p.ssq1 = e->ssq;                                // [L + 1][64]
+  p.ssq2 = e->ssq + (size_t)(L + 1) * b1::kTok;   // [L][64]
+  p.A = e->A;
+  p.part_o = e->part_o;
+  p.part_ml = e->part_ml;
+  p.bar = e->bar;
+  SF_CHECK_CUDA(cudaFuncSetAttribute(b1::engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)b1::kSmemBytes));
+  h.b1 = e.release();
+  return SF_OK;
+}
+
+// One Euler full round of one env (flowpolicy.py:273-292) as one cooperative
+// launch: start/state/chunk_out/status are device pointers (sf_ae_denoise).
+static int run_b1(Handle& h, int num_steps, const float* start, const float* state, const int* env_map,
+                  float* chunk_out, int* status, cudaStream_t s) {
+  int rc;
+  if ((rc = build_b1(h))) return rc;
+  B1Engine& e = *h.b1;
+  const sf_ae_config_t& c = h.cfg;
+  b1::Params p = e.p;
+  p.n_steps = num_steps;
+  p.temb = h.temb_euler;
+  p.state = state;
+  p.env_map = env_map;
+  p.k_img = h.k_img;
+  p.v_img = h.v_img;
+  p.n_img_envs = h.n_prefix_envs;
+  p.chunk_out = chunk_out;
+  p.status = status;
+  const int n_st = b1::stages_per_step(p.L) * num_steps + 1;
+  if (getenv("SF_B1_TRACE")) {
+    const size_t n = (size_t)b1::kGrid * n_st * 8;
+    if (e.dbg_n < n) {
+      if (e.dbg) cudaFree(e.dbg);
+      e.dbg = nullptr;
+      if ((rc = dalloc(&e.dbg, n))) return rc;
+      e.dbg_n = n;
+    }
+    p.dbg = e.dbg;
+  }
+  SF_CHECK_CUDA(cudaMemsetAsync(e.bar, 0, 64, s));
+  SF_CHECK_CUDA(cudaMemsetAsync(e.cnt, 0, sizeof(unsigned) * 8 * 64, s));
+  SF_CHECK_CUDA(cudaMemsetAsync(e.ssq, 0, sizeof(float) * e.ssq_n, s));
+  SF_CHECK_CUDA(cudaMemcpyAsync(e.A, start, sizeof(float) * c.horizon * c.action_dim, cudaMemcpyDeviceToDevice, s));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(b1::kGrid);
+  cfg.blockDim = dim3(b1::kThreads);
+  cfg.dynamicSmemBytes = b1::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeCooperative;
+  a[0].val.cooperative = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  SF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, b1::engine_kernel, p));
+  count_launch();
+  return SF_OK;
+}
+}  // namespace pi0
+}  // namespace sf
+
+extern "C" int sf_ae_b1_trace(void* handle, unsigned long long* out, size_t n) {
+  auto* h = static_cast<Handle*>(handle);
+  SF_REQUIRE(h && out, "null argument");
+  SF_REQUIRE(h->b1 && h->b1->dbg && n <= h->b1->dbg_n, "no batch-1 engine trace (run with SF_B1_TRACE=1)");
+  SF_CHECK_CUDA(cudaDeviceSynchronize());
+  SF_CHECK_CUDA(cudaMemcpy(out, h->b1->dbg, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return SF_OK;
+}
+
 extern "C" int sf_ae_destroy(void* handle) {
   auto* h = static_cast<Handle*>(handle);
   if (!h) return SF_OK;
@@ -1530,6 +1723,7 @@ extern "C" int sf_ae_destroy(void* handle) {
   if (h->temb_euler) cudaFree(h->temb_euler);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
   if (h->body_stream) cudaStreamDestroy(h->body_stream);
+  destroy_b1(h);
   delete h;
   return SF_OK;
 }
@@ -1782,6 +1976,11 @@ extern "C" int sf_ae_denoise_envs(void* handle, int n_envs, const int* env_map, 
   SF_REQUIRE(num_steps >= 1 && num_steps <= 64, "num_steps must be in [1, 64]");
   cudaStream_t s = (cudaStream_t)stream;
   int rc = 0;
+  if (n_envs == 1 && !(flags & SF_AE_FP32) && b1_supported(*h)) {
+    // batch 1: the whole round is one persistent launch (b1engine.cuh)
+    if ((rc = set_euler_steps(*h, num_steps, s))) return rc;
+    return run_b1(*h, num_steps, start, state, env_map, chunk_out, status, s);
+  }
   Buffers* b = get_buffers(*h, n_envs, 1, 1 | ((flags & SF_AE_FP32) ? kModeF32 : 0), &rc);
   if (!b) return rc;
   const sf_ae_config_t& c = h->cfg;
