@@ -304,7 +304,10 @@ __device__ __forceinline__ Smem carve(uint8_t* base) {
   s.bempty = bars + 28;
   s.tmem_slot = reinterpret_cast<uint32_t*>(bars + 36);
   s.flag = reinterpret_cast<int*>(bars + 37);
-  float* f = reinterpret_cast<float*>(c + 256);
+  // the float scratch starts after the 38 barrier / slot words (304 B): at
+  // c + 256 it overlapped bempty[4..7] and the flag, so the softmax exchange
+  // of an attention stage could corrupt a live B-slot barrier
+  float* f = reinterpret_cast<float*>(c + 512);
   s.xm = f;            // 512 floats
   s.wts = f + 512;     // 64 * kAttSplits
   s.rs = f + 512 + 64 * kAttSplits;
