@@ -913,16 +913,26 @@ int build(Handle& h, Buffers& b, int B, int K) {
   // then as many K splits as keep one wave with clusters <= 6 CTAs (8- and
   // 16-CTA clusters schedule poorly). SF_TUNE=1 times candidates instead.
   if (swap && getenv("SF_TUNE") == nullptr) {
-    const int bn = b.M > 128 ? (((b.M + 1) / 2 + 15) / 16) * 16 : bn_swap;
-    const int tiles_b = (b.M + bn - 1) / bn;
+    // SF_B1_PLAN="bn:S,bn:S,bn:S,bn:S" (qkv, o, gu, down; 0 = the rule's
+    // value) overrides the rule for batches above 128 rows: the in-graph
+    // sweep (scripts/b1_plan_sweep.py) times whole verify rounds with it
+    int force_bn[4] = {0, 0, 0, 0}, force_s[4] = {0, 0, 0, 0};
+    if (const char* fp = getenv("SF_B1_PLAN")) {
+      if (b.M > 128)
+        sscanf(fp, "%d:%d,%d:%d,%d:%d,%d:%d", &force_bn[0], &force_s[0], &force_bn[1], &force_s[1], &force_bn[2],
+               &force_s[2], &force_bn[3], &force_s[3]);
+    }
     for (int cls = 0; cls < 4; ++cls) {
       const Spec& sp = specs[cls];
+      const int bn = force_bn[cls] > 0 ? force_bn[cls] : (b.M > 128 ? (((b.M + 1) / 2 + 15) / 16) * 16 : bn_swap);
+      const int tiles_b = (b.M + bn - 1) / bn;
       const int tiles = ((sp.n_out + gemm::BM - 1) / gemm::BM) * tiles_b, nkb = sp.k_in / gemm::BK;
       int S = nsm / tiles;
       // 8-CTA clusters only while they fill at most half the GPU
       S = S > 8 ? 8 : (S < 1 ? 1 : S);
       if (S > 6 && tiles * S > nsm / 2) S = 6;
       S = S > nkb ? nkb : S;
+      if (force_s[cls] > 0) S = force_s[cls];
       for (int l = 0; l < L; ++l) {
         const Spec& q = specs[4 * l + cls];
         if ((rc = gemm::plan(&b.ops[4 * l + cls], q.wt, q.n_out, q.k_in, q.act, b.M, q.k_in, q.k_in,
