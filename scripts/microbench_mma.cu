@@ -102,7 +102,8 @@ int main() {
             {128, 64, 1, 64, 1, 1},  {128, 64, 1, 64, 2, 1},  {128, 64, 1, 64, 4, 1},  {64, 64, 1, 64, 4, 1},
             {128, 64, 1, 64, 2, 0},  {128, 64, 1, 64, 4, 0},  {128, 208, 1, 64, 1, 1}, {128, 128, 1, 64, 1, 1},
             {64, 64, 1, 64, 1, 2},   {128, 64, 1, 64, 1, 2},  {64, 64, 1, 64, 1, 3},   {128, 208, 1, 64, 1, 2},
-            {64, 64, 1, 64, 2, 2},   {128, 64, 1, 64, 2, 2}};
+            {64, 64, 1, 64, 2, 2},   {128, 64, 1, 64, 2, 2},  {128, 56, 1, 64, 1, 1},  {64, 56, 1, 64, 1, 1},
+            {64, 56, 1, 63, 3, 1},   {128, 56, 1, 63, 3, 1},  {64, 64, 1, 63, 3, 1}};
   for (int rnd = 1; rnd < 2; ++rnd) {
   cudaMemcpyToSymbol(g_random, &rnd, sizeof(int));
   printf("operands: %s\n", rnd ? "random bf16" : "constant pattern");
