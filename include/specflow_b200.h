@@ -22,6 +22,7 @@
 #ifndef SPECFLOW_B200_H
 #define SPECFLOW_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -97,6 +98,12 @@ const char* sf_last_error(void);
 int sf_version(void);
 /* Number of kernels the library launched on this thread since the last reset. */
 int64_t sf_launch_count(int reset);
+
+/* Staging helpers for the host-facing API: async copy of `bytes` from a
+ * (pinned) host buffer to the device on `stream`; copy back and synchronize
+ * the stream. */
+int sf_copy_h2d(void* dst, const void* src, size_t bytes, void* stream);
+int sf_copy_d2h_sync(void* dst, const void* src, size_t bytes, void* stream);
 
 /* ------------------------------------------------------------------ tiny path
  * cfg1/cfg2: tanh-MLP draft + endpoint-parameterised MLP field.

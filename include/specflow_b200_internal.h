@@ -40,6 +40,12 @@ int sf_dbg_gemm_time(const void* A, int rows_a, const void* B, int rows_b, int K
  * accumulator / softmax done, stage done), copied to host `out` (n entries). */
 int sf_ae_b1_trace(void* ae_handle, unsigned long long* out, size_t n);
 
+/* %globaltimer stamps of the fused tiny flash round (cluster rank 0): on != 0
+ * enables them for the following launches; `out` (32 entries, may be NULL)
+ * receives the stamps of the last launch (0 start, 1 weights issued, 8-15
+ * draft layers done, 2 branches packed, 16-23 field layers done, 3 end). */
+int sf_tiny_trace(int on, unsigned long long* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,8 @@ SIGNATURES = {
     "sf_last_error": (ctypes.c_char_p, []),
     "sf_version": (_I, []),
     "sf_launch_count": (ctypes.c_int64, [_I]),
+    "sf_copy_h2d": (_I, [_P, _P, ctypes.c_size_t, _P]),
+    "sf_copy_d2h_sync": (_I, [_P, _P, ctypes.c_size_t, _P]),
     "sf_tiny_flash_round": (_I, [_I, ctypes.POINTER(SfMlp), _P, ctypes.POINTER(SfMlp), _P, _I, _P, _I,
                                  _P, _I, _I, _I, ctypes.POINTER(SfVerifyCfg),
                                  ctypes.POINTER(SfVerifyOut), _P]),
@@ -125,6 +127,7 @@ SIGNATURES = {
     "sf_dbg_gemm_time": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P, _P]),
     "sf_dbg_gemm_trace": (_I, [_P, _I, _P, _I, _I, _I, _I, _P, _P, _P]),
     "sf_ae_b1_trace": (_I, [_P, _P, ctypes.c_size_t]),
+    "sf_tiny_trace": (_I, [_I, _P]),
 }
 
 _lib = None

@@ -11,8 +11,13 @@
 //    are streamed with unrolled loads.
 //  * Each layer is split across the cluster by output neuron; a warp owns one
 //    output row at a time (K activation rows from SMEM), reduces with
-//    shuffles and pushes the activation into every CTA's SMEM over DSMEM,
-//    then one cluster barrier per layer.
+//    shuffles and pushes the activation into every CTA's SMEM with
+//    st.async (DSMEM stores that complete_tx on the receiver's mbarrier).
+//    A layer ends when the CTA's own output buffer has received all bytes --
+//    no cluster barrier per layer (cluster.sync() compiles to MEMBAR.ALL.GPU
+//    + the cluster barrier, ~0.8 us per layer measured). Three activation
+//    buffers rotate so that a layer's pushes only target a buffer every CTA
+//    has finished reading (see cluster_mlp).
 //  * The speculative round fuses draft MLP -> K-branch interpolation/packing
 //    -> field MLP -> reconstruction -> distances -> warp-ballot prefix scan ->
 //    gripper gate -> decision; the full round fuses encoder -> N Euler steps.
@@ -46,7 +51,6 @@ struct DevMlp {
   const T* w[SF_MAX_LAYERS];
   const T* b[SF_MAX_LAYERS];
   int woff[SF_MAX_LAYERS];  // element offset of this CTA's slice in the SMEM arena; -1 = global
-  int boff[SF_MAX_LAYERS];  // element offset of this CTA's bias slice (always resident)
 };
 
 template <typename T>
@@ -100,100 +104,16 @@ __device__ void init_bars(const DevMlp<T>& m, uint64_t* bars) {
     if (m.woff[l] >= 0) sm100::mbar_init(&bars[l], 1);
 }
 
-// Bias slices go to SMEM once per launch (no global load on the layer path).
-template <typename T>
-__device__ void stage_biases(const DevMlp<T>& m, T* arena, int rank, int csize) {
-  for (int l = 0; l < m.n_layers; ++l) {
-    int r0, r1;
-    slice_rows(m.sizes[l + 1], rank, csize, r0, r1);
-    for (int j = r0 + (int)threadIdx.x; j < r1; j += blockDim.x)
-      arena[m.boff[l] + (j - r0)] = __ldg(m.b[l] + j);
-  }
-}
 
-// One layer for `rows` activation rows. in: this CTA's SMEM [rows][n_in];
-// out: [rows][n_out] written into EVERY CTA's SMEM (DSMEM push).
-template <typename T>
-__device__ void cluster_layer(cg::cluster_group& cluster, const DevMlp<T>& m, int l,
-                              const T* arena, uint64_t* bars, int rows, const T* in, T* out) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rank = (int)cluster.block_rank(), csize = (int)cluster.num_blocks();
-  const int n_in = m.sizes[l], n_out = m.sizes[l + 1], ld = m.ld[l];
-  const bool resident = m.woff[l] >= 0;
-  const bool act = l + 1 < m.n_layers;
-  int r0, r1;
-  slice_rows(n_out, rank, csize, r0, r1);
-  if (resident && r1 > r0) sm100::mbar_wait(&bars[l], 0);
-  for (int j = r0 + warp; j < r1; j += kWarps) {
-    T acc[kMaxRows];
-#pragma unroll
-    for (int r = 0; r < kMaxRows; ++r) acc[r] = T(0);
-    if (resident) {
-      const T* wr = arena + m.woff[l] + (size_t)(j - r0) * ld;
-      for (int i = lane; i < n_in; i += 32) {
-        const T w = wr[i];
-#pragma unroll
-        for (int r = 0; r < kMaxRows; ++r)
-          if (r < rows) acc[r] = fma(w, in[r * n_in + i], acc[r]);
-      }
-    } else {
-      const T* wr = m.w[l] + (size_t)j * ld;
-      int i = lane;
-      for (; i + 96 < n_in; i += 128) {  // 4 independent loads in flight per lane
-        const T w0 = __ldg(wr + i), w1 = __ldg(wr + i + 32), w2 = __ldg(wr + i + 64),
-                w3 = __ldg(wr + i + 96);
-#pragma unroll
-        for (int r = 0; r < kMaxRows; ++r) {
-          if (r < rows) {
-            const T* a = in + r * n_in + i;
-            acc[r] = fma(w0, a[0], acc[r]);
-            acc[r] = fma(w1, a[32], acc[r]);
-            acc[r] = fma(w2, a[64], acc[r]);
-            acc[r] = fma(w3, a[96], acc[r]);
-          }
-        }
-      }
-      for (; i < n_in; i += 32) {
-        const T w = __ldg(wr + i);
-#pragma unroll
-        for (int r = 0; r < kMaxRows; ++r)
-          if (r < rows) acc[r] = fma(w, in[r * n_in + i], acc[r]);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < kMaxRows; ++r) {
-      if (r < rows) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], off);
-      }
-    }
-    T mine = T(0);
-#pragma unroll
-    for (int r = 0; r < kMaxRows; ++r)
-      if (r == lane) mine = acc[r];
-    T z = add_rn(mine, arena[m.boff[l] + (j - r0)]);  // z = a @ W.T + b (nets.py:103)
-    if (act) z = tanh_t(z);                  // tanh on hidden layers (nets.py:104)
-    for (int r = 0; r < rows; ++r) {
-      const T v = __shfl_sync(0xffffffffu, z, r);
-      for (int c = lane; c < csize; c += 32) cluster.map_shared_rank(out, c)[r * n_out + j] = v;
-    }
+// Optional trace (sf_tiny_trace): %globaltimer stamps of rank 0, thread 0.
+__device__ int g_tiny_trace_on = 0;
+__device__ unsigned long long g_tiny_trace[32];
+__device__ __forceinline__ void tstamp(int k) {
+  if (g_tiny_trace_on && threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tiny_trace[k] = t;
   }
-  cluster.sync();
-}
-
-// Whole MLP; ping-pongs bufA (input) / bufB. Returns the buffer holding the output.
-template <typename T>
-__device__ T* cluster_mlp(cg::cluster_group& cluster, const DevMlp<T>& m, const T* arena,
-                          uint64_t* bars, int rows, T* bufA, T* bufB) {
-  T* in = bufA;
-  T* out = bufB;
-  for (int l = 0; l < m.n_layers; ++l) {
-    cluster_layer<T>(cluster, m, l, arena, bars, rows, in, out);
-    T* t = in;
-    in = out;
-    out = t;
-  }
-  return in;
 }
 
 // SMEM map shared by all cluster kernels:
@@ -202,27 +122,156 @@ template <typename T>
 struct Frame {
   uint64_t* bars0;
   uint64_t* bars1;
-  T* bufA;
-  T* bufB;
+  uint64_t* full;  // [3] activation buffer i received all of a layer's pushes
+  T* buf0;         // activation buffer i at buf0 + i * stride (no indexed array: it
+  int stride;      // would live on the stack)
   T* extra;
   T* arena;
+  __device__ T* buf(int i) const { return buf0 + i * stride; }
 };
+
+constexpr int kFrameBars = 2 * SF_MAX_LAYERS + 4;
 
 template <typename T>
 __device__ Frame<T> frame(unsigned char* smem, int buf_elems, int extra_elems) {
   Frame<T> f;
   f.bars0 = reinterpret_cast<uint64_t*>(smem);
   f.bars1 = f.bars0 + SF_MAX_LAYERS;
-  f.bufA = reinterpret_cast<T*>(smem + 2 * SF_MAX_LAYERS * sizeof(uint64_t));
-  f.bufB = f.bufA + buf_elems;
-  f.extra = f.bufB + buf_elems;
+  f.full = f.bars1 + SF_MAX_LAYERS;
+  f.buf0 = reinterpret_cast<T*>(smem + kFrameBars * sizeof(uint64_t));
+  f.stride = buf_elems;
+  f.extra = f.buf0 + 3 * buf_elems;
   f.arena = f.extra + extra_elems;
   return f;
 }
 
 template <typename T>
 size_t frame_bytes(int buf_elems, int extra_elems) {
-  return 2 * SF_MAX_LAYERS * sizeof(uint64_t) + sizeof(T) * ((size_t)2 * buf_elems + extra_elems);
+  return kFrameBars * sizeof(uint64_t) + sizeof(T) * ((size_t)3 * buf_elems + extra_elems);
+}
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// DSMEM store that signals `bytes` on the receiving CTA's mbarrier
+__device__ __forceinline__ void st_async(uint32_t addr, float v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr),
+               "r"(__float_as_uint(v)), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t addr, double v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr),
+               "l"(__double_as_longlong(v)), "r"(bar)
+               : "memory");
+}
+
+// One layer for `rows` activation rows. in: this CTA's SMEM [rows][n_in];
+// out: f.buf(oi) [rows][n_out] of EVERY CTA (st.async push). Returns after
+// this CTA's own f.buf(oi) holds the whole layer output. `ph` carries the
+// phase bits of the three full barriers (identical in every thread).
+template <typename T, int ROWS>
+__device__ void cluster_layer(cg::cluster_group& cluster, const Frame<T>& f, const DevMlp<T>& m, int l,
+                              uint64_t* bars, const T* in, int oi, uint32_t& ph) {
+  constexpr int rows = ROWS;  // compile-time: no predicated lanes / divergent shuffles
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster.block_rank(), csize = (int)cluster.num_blocks();
+  const int n_in = m.sizes[l], n_out = m.sizes[l + 1], ld = m.ld[l];
+  const bool resident = m.woff[l] >= 0;
+  const bool act = l + 1 < m.n_layers;
+  const T* arena = f.arena;
+  // arm this layer's fill of my output buffer (its previous fill was consumed
+  // before the previous layer; early remote bytes only make tx-count negative)
+  if (threadIdx.x == 0) sm100::mbar_arrive_expect_tx(&f.full[oi], (uint32_t)(rows * n_out * sizeof(T)));
+  int r0, r1;
+  slice_rows(n_out, rank, csize, r0, r1);
+  // lane c < csize pushes to CTA c
+  uint32_t rout = 0, rbar = 0;
+  if (lane < csize) {
+    rout = mapa_u32(sm100::smem_u32(f.buf(oi)), (uint32_t)lane);
+    rbar = mapa_u32(sm100::smem_u32(&f.full[oi]), (uint32_t)lane);
+  }
+  if (resident && r1 > r0) sm100::mbar_wait(&bars[l], 0);
+  for (int j = r0 + warp; j < r1; j += kWarps) {
+    const T bias = __ldg(m.b[l] + j);  // in flight during the dot products
+    T acc[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) acc[r] = T(0);
+    if (resident) {
+      const T* wr = arena + m.woff[l] + (size_t)(j - r0) * ld;
+      for (int i = lane; i < n_in; i += 32) {
+        const T w = wr[i];
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) acc[r] = fma(w, in[r * n_in + i], acc[r]);
+      }
+    } else {
+      const T* wr = m.w[l] + (size_t)j * ld;
+      int i = lane;
+      for (; i + 96 < n_in; i += 128) {  // 4 independent loads in flight per lane
+        const T w0 = __ldg(wr + i), w1 = __ldg(wr + i + 32), w2 = __ldg(wr + i + 64),
+                w3 = __ldg(wr + i + 96);
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+          const T* a = in + r * n_in + i;
+          acc[r] = fma(w0, a[0], acc[r]);
+          acc[r] = fma(w1, a[32], acc[r]);
+          acc[r] = fma(w2, a[64], acc[r]);
+          acc[r] = fma(w3, a[96], acc[r]);
+        }
+      }
+      for (; i < n_in; i += 32) {
+        const T w = __ldg(wr + i);
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) acc[r] = fma(w, in[r * n_in + i], acc[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], off);
+    }
+    T mine = T(0);
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r)
+      if (r == lane) mine = acc[r];
+    T z = add_rn(mine, bias);  // z = a @ W.T + b (nets.py:103)
+    if (act) z = tanh_t(z);    // tanh on hidden layers (nets.py:104)
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const T v = __shfl_sync(0xffffffffu, z, r);
+      if (lane < csize) st_async(rout + (uint32_t)((r * n_out + j) * sizeof(T)), v, rbar);
+    }
+  }
+  sm100::mbar_wait(&f.full[oi], (ph >> oi) & 1u);
+  ph ^= 1u << oi;
+}
+
+// Whole MLP on input `in` (ready in this CTA: received, or filled locally and
+// __syncthreads'd). Layer 0 pushes into buffer o0, layer 1 into a1, then they
+// alternate. The rotation is race-free when a1 is the buffer holding `in` and
+// o0 is a buffer no CTA still reads: layer s >= 1 pushes into the input of
+// layer s - 1, and a CTA pushes layer s only after it received every CTA's
+// layer s - 1 output, i.e. after every CTA finished reading that input.
+// Returns the index of the buffer holding the output.
+template <typename T>
+__device__ int cluster_mlp(cg::cluster_group& cluster, const Frame<T>& f, const DevMlp<T>& m, uint64_t* bars,
+                           int rows, const T* in, int o0, int a1, uint32_t& ph) {
+  int oi = o0;
+  for (int l = 0; l < m.n_layers; ++l) {
+    switch (rows) {
+#define SF_ROWS_CASE(R) \
+  case R: cluster_layer<T, R>(cluster, f, m, l, bars, in, oi, ph); break;
+      SF_ROWS_CASE(1) SF_ROWS_CASE(2) SF_ROWS_CASE(3) SF_ROWS_CASE(4)
+      SF_ROWS_CASE(5) SF_ROWS_CASE(6) SF_ROWS_CASE(7) SF_ROWS_CASE(8)
+#undef SF_ROWS_CASE
+      default: __trap();
+    }
+    tstamp(8 + l + (rows > 1 ? 8 : 0));
+    in = f.buf(oi);
+    oi = (oi == o0) ? a1 : o0;
+  }
+  return (oi == o0) ? a1 : o0;
 }
 
 // Prologue: barrier init, weight staging for up to two nets, cluster-wide
@@ -232,14 +281,16 @@ __device__ void prologue(cg::cluster_group& cluster, const Frame<T>& f, const De
                          const DevMlp<T>* n1) {
   init_bars(n0, f.bars0);
   if (n1) init_bars(*n1, f.bars1);
-  if (threadIdx.x == 0) sm100::fence_barrier_init();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 3; ++i) sm100::mbar_init(&f.full[i], 1);
+    sm100::fence_barrier_init();
+  }
   __syncthreads();
   const int rank = (int)cluster.block_rank(), csize = (int)cluster.num_blocks();
   stage_weights(n0, f.arena, f.bars0, rank, csize);
   if (n1) stage_weights(*n1, f.arena, f.bars1, rank, csize);
-  stage_biases(n0, f.arena, rank, csize);
-  if (n1) stage_biases(*n1, f.arena, rank, csize);
-  __syncthreads();
+  // biases are read per output row in cluster_layer (global loads here would
+  // serialise ~1 us of latency per layer into the prologue)
 }
 
 // ------------------------------------------------------------ flash round
@@ -276,19 +327,23 @@ __global__ void __launch_bounds__(kThreads, 1) tiny_flash_round_kernel(const Fla
   const Frame<T> f = frame<T>(smem_raw, p.buf_elems, p.extra_elems);
   T* s_draft = f.extra;
   const int HD = p.H * p.D;
+  tstamp(0);
   prologue<T>(cluster, f, p.field, p.has_draft ? &p.draft : nullptr);
+  tstamp(1);
 
+  uint32_t ph = 0;
   // 1. draft (draft.py:57-61)
   const T* draft_vals;
   if (p.has_draft) {
-    for (int i = threadIdx.x; i < p.draft.sizes[0]; i += blockDim.x) f.bufA[i] = p.draft_in[i];
+    for (int i = threadIdx.x; i < p.draft.sizes[0]; i += blockDim.x) f.buf(0)[i] = p.draft_in[i];
     __syncthreads();
-    cluster.sync();
-    const T* o = cluster_mlp<T>(cluster, p.draft, f.arena, f.bars1, 1, f.bufA, f.bufB);
-    for (int i = threadIdx.x; i < HD; i += blockDim.x) s_draft[i] = o[i];
+    cluster.sync();  // every CTA's barriers are initialised before the first push
+    const int oi = cluster_mlp<T>(cluster, f, p.draft, f.bars1, 1, f.buf(0), 1, 0, ph);
+    for (int i = threadIdx.x; i < HD; i += blockDim.x) s_draft[i] = f.buf(oi)[i];
     __syncthreads();
     draft_vals = s_draft;
   } else {
+    cluster.sync();
     draft_vals = p.draft_in;
   }
   if (cluster.block_rank() == 0 && p.out_draft)
@@ -304,23 +359,28 @@ __global__ void __launch_bounds__(kThreads, 1) tiny_flash_round_kernel(const Fla
     else if (i == HD) v = tau;
     else if (i < HD + 1 + p.emb_dim) v = p.emb[i - HD - 1];
     else v = p.state[i - HD - 1 - p.emb_dim];
-    f.bufA[idx] = v;
+    f.buf(0)[idx] = v;  // no push targets buffer 0 until every CTA finished field layer 0
   }
   __syncthreads();
-  cluster.sync();
+  tstamp(2);
 
-  // 3. field MLP over the K branches as one K-row batch
-  const T* out = cluster_mlp<T>(cluster, p.field, f.arena, f.bars0, p.K, f.bufA, f.bufB);
+  // 3. field MLP over the K branches as one K-row batch; layer 0 pushes into
+  // buffer 2 (never used before), so a CTA still copying the draft output out
+  // of buffer 1 is not overwritten
+  const int fo = cluster_mlp<T>(cluster, f, p.field, f.bars0, p.K, f.buf(0), 2, 0, ph);
+  const T* out = f.buf(fo);
 
   // 4. epilogue on rank 0
   if (cluster.block_rank() == 0) {
-    T* s_recon = (out == f.bufA) ? f.bufB : f.bufA;
+    T* s_recon = f.buf(fo == 1 ? 0 : 1);
     T* s_dist = s_recon + p.K * HD;
     verify_epilogue_cta<T, true>(
         draft_vals, p.eps, [&](int k, int i) { return out[k * HD + i]; }, p.H, p.D, p.C, p.K,
         p.taus, p.delta, p.metric, p.window, p.sign, p.phase_fallback, p.prefix_cap,
         p.replan_size, p.out_recon, p.out_dist, p.out_branch, p.out_result, s_recon, s_dist);
   }
+  tstamp(3);
+  cluster.sync();  // no CTA exits while its pushes to peers may be in flight
 }
 
 // ------------------------------------------------------------- full round
@@ -356,18 +416,21 @@ __global__ void __launch_bounds__(kThreads, 1) tiny_full_round_kernel(const Full
   prologue<T>(cluster, f, p.field, p.has_enc ? &p.enc : nullptr);
 
   // encode_context: emb = [features, MLP(features)] (flowpolicy.py:143-147)
+  uint32_t ph = 0;
+  int last = 2;  // buffer holding the previous MLP's output (read by lagging CTAs)
   if (p.has_enc) {
     const int fi = p.enc.sizes[0];
     for (int i = threadIdx.x; i < fi; i += blockDim.x) {
-      f.bufA[i] = p.enc_in[i];
+      f.buf(0)[i] = p.enc_in[i];
       s_emb[i] = p.enc_in[i];
     }
     __syncthreads();
-    cluster.sync();
-    const T* o = cluster_mlp<T>(cluster, p.enc, f.arena, f.bars1, 1, f.bufA, f.bufB);
-    for (int i = threadIdx.x; i < p.enc.sizes[p.enc.n_layers]; i += blockDim.x) s_emb[fi + i] = o[i];
+    cluster.sync();  // every CTA's barriers are initialised before the first push
+    last = cluster_mlp<T>(cluster, f, p.enc, f.bars1, 1, f.buf(0), 1, 0, ph);
+    for (int i = threadIdx.x; i < p.enc.sizes[p.enc.n_layers]; i += blockDim.x) s_emb[fi + i] = f.buf(last)[i];
   } else {
     for (int i = threadIdx.x; i < p.emb_dim; i += blockDim.x) s_emb[i] = p.enc_in[i];
+    cluster.sync();
   }
   for (int i = threadIdx.x; i < HD; i += blockDim.x) s_vals[i] = p.start[i];
   for (int i = threadIdx.x; i < p.state_dim; i += blockDim.x) s_state[i] = p.state[i];
@@ -384,17 +447,20 @@ __global__ void __launch_bounds__(kThreads, 1) tiny_full_round_kernel(const Full
   const int n_in = p.has_field ? p.field.sizes[0] : 0;
   for (int step = 0; step < p.N; ++step) {
     const T tau = (T)((double)step / (double)p.N);
+    const int pin = (last + 1) % 3;  // no push targets it before every CTA finished layer 0
     for (int i = threadIdx.x; i < n_in; i += blockDim.x) {
       T v;
       if (i < HD) v = s_vals[i];
       else if (i == HD) v = tau;
       else if (i < HD + 1 + p.emb_dim) v = s_emb[i - HD - 1];
       else v = s_state[i - HD - 1 - p.emb_dim];
-      f.bufA[i] = v;
+      f.buf(pin)[i] = v;
     }
     __syncthreads();
-    cluster.sync();
-    const T* out = cluster_mlp<T>(cluster, p.field, f.arena, f.bars0, 1, f.bufA, f.bufB);
+    // layer 0 pushes into the third buffer: neither the one a lagging CTA may
+    // still read (the previous output) nor the packed input
+    last = cluster_mlp<T>(cluster, f, p.field, f.bars0, 1, f.buf(pin), (last + 2) % 3, pin, ph);
+    const T* out = f.buf(last);
     const T omt = sub_rn(T(1), tau);
     const T n = (T)p.N;
     for (int i = threadIdx.x; i < HD; i += blockDim.x) {
@@ -452,11 +518,13 @@ __global__ void __launch_bounds__(kThreads, 1) tiny_field_eval_kernel(const Eval
     else if (i == p.HD) v = p.taus[r];
     else if (i < p.HD + 1 + p.emb_dim) v = p.emb[i - p.HD - 1];
     else v = p.state[i - p.HD - 1 - p.emb_dim];
-    f.bufA[idx] = v;
+    f.buf(0)[idx] = v;
   }
   __syncthreads();
-  cluster.sync();
-  const T* out = cluster_mlp<T>(cluster, p.field, f.arena, f.bars0, p.R, f.bufA, f.bufB);
+  cluster.sync();  // every CTA's barriers are initialised before the first push
+  uint32_t ph = 0;
+  const T* out = f.buf(cluster_mlp<T>(cluster, f, p.field, f.bars0, p.R, f.buf(0), 1, 0, ph));
+  cluster.sync();  // no CTA exits while its pushes to peers may be in flight
   if (cluster.block_rank() != 0) return;
   __shared__ int s_bad[kMaxRows];
   if (threadIdx.x < kMaxRows) s_bad[threadIdx.x] = 0;
@@ -490,10 +558,12 @@ __global__ void __launch_bounds__(kThreads, 1) tiny_mlp_forward_kernel(const Fwd
   const Frame<T> f = frame<T>(smem_raw, p.buf_elems, p.extra_elems);
   prologue<T>(cluster, f, p.net, nullptr);
   const int n_in = p.net.sizes[0], n_out = p.net.sizes[p.net.n_layers];
-  for (int i = threadIdx.x; i < p.R * n_in; i += blockDim.x) f.bufA[i] = p.x[i];
+  for (int i = threadIdx.x; i < p.R * n_in; i += blockDim.x) f.buf(0)[i] = p.x[i];
   __syncthreads();
-  cluster.sync();
-  const T* o = cluster_mlp<T>(cluster, p.net, f.arena, f.bars0, p.R, f.bufA, f.bufB);
+  cluster.sync();  // every CTA's barriers are initialised before the first push
+  uint32_t ph = 0;
+  const T* o = f.buf(cluster_mlp<T>(cluster, f, p.net, f.bars0, p.R, f.buf(0), 1, 0, ph));
+  cluster.sync();  // no CTA exits while its pushes to peers may be in flight
   if (cluster.block_rank() == 0)
     for (int i = threadIdx.x; i < p.R * n_out; i += blockDim.x) p.out[i] = o[i];
 }
@@ -524,13 +594,6 @@ template <typename T>
 size_t plan_arena(DevMlp<T>* first, DevMlp<T>* second, size_t fixed, int csize) {
   size_t off = 0;  // elements
   DevMlp<T>* order[2] = {first, second};
-  for (DevMlp<T>* m : order) {  // biases first: always resident
-    if (!m) continue;
-    for (int l = 0; l < m->n_layers; ++l) {
-      m->boff[l] = (int)off;
-      off += ((m->sizes[l + 1] + csize - 1) / csize + 15) & ~15;
-    }
-  }
   for (DevMlp<T>* m : order) {
     if (!m) continue;
     for (int l = 0; l < m->n_layers; ++l) {
@@ -799,6 +862,17 @@ extern "C" int sf_tiny_flash_round(int precision, const sf_mlp_t* draft_net, con
   return SF_DISPATCH(precision, sf::flash_round_impl, draft_net, draft_in, field_net, emb, emb_dim,
                      state, state_dim, eps, horizon, dim, continuous_dims, cfg, out,
                      (cudaStream_t)stream);
+}
+
+// trace of the next tiny flash rounds (rank 0 stamps): on != 0 enables, out
+// (32 u64) receives the stamps of the last round
+extern "C" int sf_tiny_trace(int on, unsigned long long* out) {
+  SF_CHECK_CUDA(cudaMemcpyToSymbol(sf::g_tiny_trace_on, &on, sizeof(int)));
+  if (out) {
+    SF_CHECK_CUDA(cudaDeviceSynchronize());
+    SF_CHECK_CUDA(cudaMemcpyFromSymbol(out, sf::g_tiny_trace, 32 * sizeof(unsigned long long)));
+  }
+  return SF_OK;
 }
 
 extern "C" int sf_tiny_full_round(int precision, const sf_mlp_t* encoder, const void* enc_in,

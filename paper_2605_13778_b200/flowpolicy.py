@@ -104,23 +104,23 @@ class ContextEncoder:
 
 
 def _run_full(encoder_net, enc_in, emb_dim, field_net, state, start, horizon, dim, n):
-    """One ``sf_tiny_full_round`` launch; returns (chunk, emb, status) on host."""
-    lib = _capi.lib()
-    dev = _device.device()
-    d_in = _device.to_dev(enc_in)
-    d_state = _device.to_dev(state if np.size(state) else np.zeros(1))
-    d_start = _device.to_dev(start)
-    chunk = torch.empty(horizon * dim, dtype=d_start.dtype, device=dev)
-    emb = torch.empty(max(emb_dim, 1), dtype=d_start.dtype, device=dev)
-    status = torch.full((2,), -1, dtype=torch.int32, device=dev)
+    """One ``sf_tiny_full_round`` launch; returns (chunk, emb, status) on host.
+    Inputs go up in one pinned copy, chunk + embedding + status come back in
+    one copy (``_device.Staging``)."""
+    enc_in = np.asarray(enc_in, dtype=np.float64).ravel()
+    st_in = np.asarray(state, dtype=np.float64).ravel()
+    start = np.asarray(start, dtype=np.float64).ravel()
+    hd = horizon * dim
+    ne = max(emb_dim, 1)
+    stg = _device.Staging.get("full", enc_in.size + max(st_in.size, 1) + start.size, hd + ne, 2)
+    p_in, p_state, p_start = stg.upload([enc_in, st_in if st_in.size else np.zeros(1), start])
     enc_desc = encoder_net.device().desc if encoder_net is not None else None
     field_desc = field_net.device().desc if field_net is not None else None
-    _capi.check(lib.sf_tiny_full_round(
-        _device.code(), enc_desc, d_in.data_ptr(), emb_dim, field_desc, d_state.data_ptr(),
-        int(np.size(state)), d_start.data_ptr(), horizon, dim, n, chunk.data_ptr(),
-        emb.data_ptr(), status.data_ptr(), _device.stream_ptr()), "full round")
-    st = status.cpu().numpy()
-    return (_device.to_host(chunk).reshape(horizon, dim), _device.to_host(emb)[:emb_dim], st)
+    _capi.check(_capi.lib().sf_tiny_full_round(
+        _device.code(), enc_desc, p_in, emb_dim, field_desc, p_state, int(st_in.size), p_start, horizon,
+        dim, n, stg.out_ptr(0), stg.out_ptr(hd), stg.word_ptr(0), _device.stream_ptr()), "full round")
+    vals, st = stg.download(hd + ne, 2)
+    return vals[:hd].reshape(horizon, dim), vals[hd:hd + emb_dim], st
 
 
 def encode_context(encoder: ContextEncoder, obs: Observation, round_index: int = 0,
