@@ -119,6 +119,7 @@ class Staging:
         self.h_words_np = ob[self.words_off:].view(np.int32)
         self.d_in_ptr, self.h_in_ptr = self.d_in.data_ptr(), self.h_in.data_ptr()
         self.d_out_ptr, self.h_out_ptr = self.d_out.data_ptr(), self.h_out.data_ptr()
+        self.extra: dict = {}  # per-shape ctypes argument structs built once by callers
 
     @classmethod
     def get(cls, key, n_in, n_out, n_words) -> "Staging":

@@ -67,8 +67,24 @@ class VerifierReport:
     planned: int | None = None   # runtime.py:310, :319-320
 
 
+_cfg_cache: dict = {}
+
+
 def make_cfg(cfg: VerifierConfig, current_sign: float, phase_fallback: bool = True,
              prefix_cap: bool = True, replan_size: int = 12) -> "_capi.SfVerifyCfg":
+    """C-ABI verifier config; memoised (configs are frozen, and building the
+    ctypes struct costs several us on a ~0.1 ms round)."""
+    key = (cfg, float(current_sign), bool(phase_fallback), bool(prefix_cap), int(replan_size))
+    c = _cfg_cache.get(key)
+    if c is None:
+        if len(_cfg_cache) > 256:
+            _cfg_cache.clear()
+        c = _cfg_cache[key] = _make_cfg(cfg, current_sign, phase_fallback, prefix_cap, replan_size)
+    return c
+
+
+def _make_cfg(cfg: VerifierConfig, current_sign: float, phase_fallback: bool, prefix_cap: bool,
+              replan_size: int) -> "_capi.SfVerifyCfg":
     c = _capi.SfVerifyCfg()
     c.k = len(cfg.timesteps)
     for i, t in enumerate(cfg.timesteps):
@@ -195,8 +211,11 @@ def tiny_flash_round(field: VelocityField, draft_net, draft_in, cache: Condition
     n_words = _capi.SF_RESULT_WORDS + k
     stg = _device.Staging.get("flash", din.size + eps.size + emb.size + st.size + 3, n_out, n_words)
     p_draft, p_eps, p_emb, p_state = stg.upload([din, eps, emb, st])
-    out = _capi.SfVerifyOut(stg.out_ptr(0), stg.out_ptr(h * d), stg.out_ptr(h * d + k * h * d),
-                            stg.word_ptr(_capi.SF_RESULT_WORDS), stg.word_ptr(0))
+    out = stg.extra.get("vout")
+    if out is None:
+        out = stg.extra["vout"] = _capi.SfVerifyOut(
+            stg.out_ptr(0), stg.out_ptr(h * d), stg.out_ptr(h * d + k * h * d),
+            stg.word_ptr(_capi.SF_RESULT_WORDS), stg.word_ptr(0))
     c = make_cfg(cfg, current_sign, phase_fallback, prefix_cap, replan_size)
     _capi.check(_capi.lib().sf_tiny_flash_round(
         _device.code(), draft_net.device().desc if draft_net is not None else None, p_draft,
