@@ -122,8 +122,8 @@ class Staging:
         self.extra: dict = {}  # per-shape ctypes argument structs built once by callers
 
     @classmethod
-    def get(cls, key, n_in, n_out, n_words) -> "Staging":
-        dt = tdtype()
+    def get(cls, key, n_in, n_out, n_words, dtype: torch.dtype | None = None) -> "Staging":
+        dt = dtype or tdtype()
         k = (key, n_in, n_out, n_words, dt, torch._C._cuda_getDevice())
         st = cls._cache.get(k)
         if st is None:

@@ -388,41 +388,61 @@ class ActionExpert:
         return self.velocity_batch(x, [tau], st)[0, 0].double().cpu().numpy()
 
     def device_verify(self, draft, cache, state, cfg, eps, current_sign, noise_seed):
-        from .verifier import VerifierReport
+        """The reference-facing plugin call (verifier.verify on this field):
+        numpy in, numpy out. Inputs go up in ONE pinned copy, recon /
+        distances / branch prefixes / result words come back in ONE copy
+        (``_device.Staging``), around one ``sf_ae_verify`` graph launch."""
+        from .verifier import VerifierReport, make_cfg
 
         if self._env_of(cache) != 0:
             raise ValueError("single-env verify uses prefix env 0")
-        dev = _device.device()
-        d = torch.as_tensor(np.asarray(draft.values, np.float32)).to(dev)[None]
-        e = torch.as_tensor(np.asarray(eps, np.float32)).to(dev)[None]
-        st = torch.as_tensor(np.asarray(state, np.float32)).to(dev).reshape(1, -1)
-        recon, dist, branch, result = self.verify_batch(cfg, d, e, st, current_sign=current_sign)
-        res = result[0].cpu().numpy()
+        H, D = self.horizon, self.dim
+        K = len(cfg.timesteps)
+        vals = np.asarray(draft.values, np.float64)
+        st_in = np.asarray(state, np.float64).ravel()
+        stg = _device.Staging.get("ae_verify", 2 * H * D + st_in.size, K * H * D + K * H,
+                                  K + _capi.SF_RESULT_WORDS, torch.float32)
+        p_d, p_e, p_s = stg.upload([vals, np.asarray(eps, np.float64), st_in])
+        out = stg.extra.get(("vout", K))
+        if out is None:
+            out = stg.extra[("vout", K)] = _capi.SfVerifyOut(
+                None, stg.out_ptr(0), stg.out_ptr(K * H * D), stg.word_ptr(_capi.SF_RESULT_WORDS),
+                stg.word_ptr(0))
+        c = make_cfg(cfg, current_sign)
+        _capi.check(_capi.lib().sf_ae_verify(self._h, 1, ctypes.byref(c), p_d, p_e, p_s, None,
+                                             ctypes.byref(out), self.flags, _device.stream_ptr()), "ae verify")
+        v, words = stg.download(K * H * D + K * H, K + _capi.SF_RESULT_WORDS)
+        res = words[:_capi.SF_RESULT_WORDS]
         if int(res[_capi.RES_NONFINITE]) >= 0:
             raise FloatingPointError(
                 f"velocity produced non-finite values at tau={cfg.timesteps[int(res[_capi.RES_NONFINITE])]}")
         return VerifierReport(
-            reconstructed=recon[0].double().cpu().numpy(), distances=dist[0].double().cpu().numpy(),
-            branch_prefixes=tuple(int(x) for x in branch[0].cpu()),
+            reconstructed=v[:K * H * D].reshape(K, H, D), distances=v[K * H * D:].reshape(K, H),
+            branch_prefixes=tuple(int(x) for x in words[_capi.SF_RESULT_WORDS:]),
             prefix=int(res[_capi.RES_PREFIX]), gripper_switch_detected=bool(res[_capi.RES_SWITCH]),
             shared_noise_seed=noise_seed, decision=_capi.PATH_CODES[int(res[_capi.RES_PATH])],
             planned=int(res[_capi.RES_PLANNED]))
 
     def device_denoise(self, cache, state, start, n) -> np.ndarray:
+        """integrate_flow on this field (plugin call): one pinned upload of the
+        start noise + state, one ``sf_ae_denoise`` launch, one readback of the
+        chunk and the status words."""
         if self._env_of(cache) != 0:
             raise ValueError("single-env denoise uses prefix env 0")
         self.eval_count += n
-        dev = _device.device()
-        a0 = torch.as_tensor(np.asarray(start, np.float32)).to(dev)[None]
-        st = torch.as_tensor(np.asarray(state, np.float32)).to(dev).reshape(1, -1)
-        chunk, status = self.denoise_batch(a0, st, n)
-        sv = status[0].cpu().numpy()
+        H, D = self.horizon, self.dim
+        st_in = np.asarray(state, np.float64).ravel()
+        stg = _device.Staging.get("ae_denoise", H * D + st_in.size, H * D, 2, torch.float32)
+        p_a, p_s = stg.upload([np.asarray(start, np.float64), st_in])
+        _capi.check(_capi.lib().sf_ae_denoise(self._h, 1, n, p_a, p_s, stg.out_ptr(0), stg.word_ptr(0),
+                                              self.flags, _device.stream_ptr()), "ae denoise")
+        chunk, sv = stg.download(H * D, 2)
         if sv[0] >= 0:
             step = int(sv[0])
             if sv[1]:
                 raise FloatingPointError(f"velocity produced non-finite values at tau={step / n}")
             raise FloatingPointError(f"denoising diverged at step {step} (tau={step / n})")
-        return chunk[0].double().cpu().numpy()
+        return chunk.reshape(H, D)
 
 
 class BatchedReplanner:
