@@ -628,6 +628,21 @@ def run_ours(args, rank, world, local):
     if world == 1 and not args.no_latency:
         line.update(latency_b1(ae, vcfg, obs, eps_v, state, signs, hbm_peak, peak_kind, dev))
         line["latency_tiny"] = latency_tiny()
+        # speculative attempt vs batch size: tensor utilisation at batch >= 64
+        # (north star: >= 50 % of bf16 peak), same graph entry point
+        sweep = []
+        for b in (1, 8, 64, 128, 256):
+            if b > E:
+                break
+            ob = ae.flash_batch(vcfg, obs[:b], eps_v[:b], state[:b], signs[:b])
+            for _ in range(3):
+                ae.flash_batch(vcfg, obs[:b], eps_v[:b], state[:b], signs[:b], outputs=ob)
+            t = p50_ms(lambda: ae.flash_batch(vcfg, obs[:b], eps_v[:b], state[:b], signs[:b], outputs=ob),
+                       20 if b >= 64 else 50)
+            tf = b * flash_env / (t / 1e3) / 1e12
+            sweep.append({"envs": b, "ms": t, "attempts_per_s": b / (t / 1e3), "tflops": tf,
+                          "frac_of_sustained_bf16": tf / tc_sust})
+        line["flash_batch_sweep"] = sweep
 
     # ---------------- CPU baseline (rank 0, N=1 only, bounded sample)
     if world == 1 and not args.no_cpu_baseline and rank == 0:
