@@ -75,7 +75,8 @@ def stream_ptr() -> int:
 
 def to_dev(a, dtype: torch.dtype | None = None) -> torch.Tensor:
     """numpy/array-like -> contiguous device tensor in the current precision."""
-    t = torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=np.float64)))
+    # a writable copy: reference arrays are often read-only (ActionChunk freezes its values)
+    t = torch.as_tensor(np.array(a, dtype=np.float64, order="C"))
     return t.to(device=device(), dtype=dtype or tdtype(), non_blocking=False).contiguous()
 
 
