@@ -594,27 +594,29 @@ __device__ __forceinline__ void epilogue_red(const Smem& sm, uint32_t tmem, int 
   }
 }
 
-// ---- tile epilogues of the last-arriving split CTA (units of 8 outputs)
+// ---- residual tile epilogue (units of 8 outputs)
 
-// residual tile f (O / DN): xb = bf16(x) and the rows' partial sums of squares
-// over the tile's 128 features -> ssq_out (the next RMSNorm)
-__device__ __forceinline__ void tile_epi_resid(const Params& p, int wt, int f, float* ssq_out) {
-  for (int base = 0; base < kTok * 16; base += kWorkers) {
-    const int idx = base + wt, t = idx >> 4, u = idx & 15;  // 16 lanes per row
-    float v[8];
-    float sq = 0.f;
-    if (t < p.T) {
-      const float* src = p.x + (size_t)t * kW + f * 128 + u * 8;
-      const float4 a = ldcg4(src), b = ldcg4(src + 4);
-      v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+// rows [r0, r0 + nr) of residual tile f (nr * 16 <= kWorkers): the share of
+// one split CTA once every split of the tile has reduced into L2
+__device__ __forceinline__ void tile_epi_resid_rows(const Params& p, int wt, int f, int r0, int nr,
+                                                    float* ssq_out) {
+  if (wt >= nr * 16) return;
+  const int t = r0 + (wt >> 4), u = wt & 15;  // 16 lanes per row (half a warp)
+  float v[8];
+  float sq = 0.f;
+  if (t < p.T) {
+    const float* src = p.x + (size_t)t * kW + f * 128 + u * 8;
+    const float4 a = ldcg4(src), b = ldcg4(src + 4);
+    v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) sq = fmaf(v[k], v[k], sq);
-      __stcg(reinterpret_cast<uint4*>(p.xb + (size_t)t * kW + f * 128 + u * 8), pack8(v));
-    }
-#pragma unroll
-    for (int off = 8; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
-    if (u == 0 && t < p.T) atomicAdd(ssq_out + t, sq);
+    for (int k = 0; k < 8; ++k) sq = fmaf(v[k], v[k], sq);
+    __stcg(reinterpret_cast<uint4*>(p.xb + (size_t)t * kW + f * 128 + u * 8), pack8(v));
   }
+  // the 16 lanes of the row are one half-warp: all of them reach the shuffles
+  const unsigned hm = (wt & 16) ? 0xffff0000u : 0x0000ffffu;
+#pragma unroll
+  for (int off = 8; off > 0; off >>= 1) sq += __shfl_xor_sync(hm, sq, off);
+  if (u == 0 && t < p.T) atomicAdd(ssq_out + t, sq);
 }
 
 // ---- M = 64 accumulators (QKV, gate/up: whole K in one CTA, no split):
@@ -1046,18 +1048,29 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         epilogue_red(sm, tmem, warp, lane, dst, ld, gm.tile * 128, nrows, nfeat);
         sm100::tc_fence_before();
         if (r.kind != K_HEAD) {
-          // the last of the tile's split CTAs finishes the tile from the L2 sums
+          // all split CTAs of the tile finish it together from the L2 sums,
+          // 1/S of its rows each, once the last split arrived (a single
+          // last-arriver converting the whole tile held the O / down stages
+          // ~2 us longer, profiles/r2 engine traces)
           workers_bar();
+          const int S = splits_of(r.kind);
           if (wt == 0) {
-            const int S = splits_of(r.kind);
-            const unsigned old = atom_add_acq_rel(p.cnt + r.kind * 64 + gm.tile, 1u);
-            *sm.flag = ((old + 1) % S) == 0;
+            unsigned* cp = p.cnt + r.kind * 64 + gm.tile;
+            const unsigned target = (atom_add_acq_rel(cp, 1u) / S + 1) * S;
+            if (ld_acquire(cp) < target) {
+              const long long t0 = clock64();
+              while (ld_acquire(cp) < target) {
+                if (clock64() - t0 > (1ll << 33)) {
+                  printf("sf b1 engine: tile counter timeout (block %d stage %d)\n", blockIdx.x, st);
+                  __trap();
+                }
+              }
+            }
           }
           workers_bar();
-          if (*sm.flag) {
-            if (r.kind == K_O) tile_epi_resid(p, wt, gm.tile, p.ssq2 + r.l * kTok);
-            else tile_epi_resid(p, wt, gm.tile, p.ssq1 + (r.l + 1) * kTok);  // DN
-          }
+          const int rows = kTok / S, r0 = (t / 8) * rows;  // task t = split * 8 + tile
+          tile_epi_resid_rows(p, wt, gm.tile, r0, rows, r.kind == K_O ? p.ssq2 + r.l * kTok
+                                                                      : p.ssq1 + (r.l + 1) * kTok);
         }
         }
       }
