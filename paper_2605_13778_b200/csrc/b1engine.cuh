@@ -52,7 +52,7 @@ constexpr int kSlots = 4;
 constexpr uint32_t kSlotBytes = 32768;  // one ring item: 2 k-blocks of 128 weight rows, or a K / V^T key block
 constexpr uint32_t kRingBytes = kSlots * kSlotBytes;
 constexpr uint32_t kBBytes = 65536;     // GEMM B operand (<= 8 k-blocks of 64 tokens) | attention Q | epilogue staging
-constexpr uint32_t kCtlBytes = 8192;
+constexpr uint32_t kCtlBytes = 8192 + 16384;  // barriers + scratch | the QKV tile's RoPE slice (16 KB)
 constexpr uint32_t kSmemBytes = 1024 + kRingBytes + kBBytes + kCtlBytes;
 // TMEM columns: GEMM accumulator | S (2 buffers) | O | P (2 buffers, bf16 pairs)
 constexpr uint32_t kAccCol = 0, kSCol = 64, kOCol = 192, kPCol = 448;
@@ -283,6 +283,7 @@ struct Smem {
   float* xm;          // [2 parity][2 half][128] softmax pair exchange
   float* wts;         // [64][kAttSplits] split-KV merge weights
   float* rs;          // [64] RMS row scales of the stage
+  float2* rope;       // [64 tokens][32 pairs] RoPE (cos, sin) of the QKV tile, staged during the MMAs
 };
 
 __device__ __forceinline__ Smem carve(uint8_t* base) {
@@ -311,6 +312,7 @@ __device__ __forceinline__ Smem carve(uint8_t* base) {
   s.xm = f;            // 512 floats
   s.wts = f + 512;     // 64 * kAttSplits
   s.rs = f + 512 + 64 * kAttSplits;
+  s.rope = reinterpret_cast<float2*>(c + 8192);
   return s;
 }
 
@@ -647,12 +649,9 @@ __device__ __forceinline__ void epi64_qkv(const Params& p, const Smem& sm, uint3
     bf16* stg = reinterpret_cast<bf16*>(sm.B);  // [64 tokens][64]: dims i0 + [0, 32) | 128 + i0 + [0, 32)
 #pragma unroll
     for (int j0 = 0; j0 < 32; j0 += 16) {
-      float2 cs[16];  // all table loads in flight before the shared stores
+      float2 cs[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int tok = half * 32 + j0 + k;
-        cs[k] = tok < p.T ? __ldg(p.rope + (size_t)(p.P + tok) * 128 + i) : make_float2(1.f, 0.f);
-      }
+      for (int k = 0; k < 16; ++k) cs[k] = sm.rope[(half * 32 + j0 + k) * 32 + (fl >> 1)];
       float yv[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
@@ -799,6 +798,15 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
         if (wt < kTok) {
           const float* ssq = (r.kind == K_QKV ? p.ssq1 : p.ssq2) + r.l * kTok;
           sm.rs[wt] = wt < p.T ? rsqrtf(__ldcg(ssq + wt) * p.inv_width + p.eps) : 0.f;
+        }
+        if (r.kind == K_QKV && t < 36) {
+          // the tile's 32 RoPE pairs for every token, staged while the MMAs
+          // run (the epilogue's L2 table loads were on the critical path)
+          const int i_base = ((t * 64) & 255) >> 1;
+          for (int e = wt; e < kTok * 32; e += kWorkers) {
+            const int tok = e >> 5, j = e & 31;
+            sm.rope[e] = tok < p.T ? __ldg(p.rope + (size_t)(p.P + tok) * 128 + i_base + j) : make_float2(1.f, 0.f);
+          }
         }
       }
       if (r.kind == K_E) {
