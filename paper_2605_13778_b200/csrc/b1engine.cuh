@@ -812,13 +812,33 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
       if (r.kind == K_E) {
         // ---- Euler update of the previous step (flowpolicy.py:289-291) + embedding
         const int i = r.step;
+        // this CTA's embedding rows (features 8c .. 8c + 7: action / state
+        // weights, biases, time embedding) and the state go to SMEM first, in
+        // parallel with the Euler update's loads: the embedding's dependent
+        // global-load chains held the stage ~5 us
+        float* e_aw = reinterpret_cast<float*>(sm.rope);  // [8][D] | [8][S] | a_b[8] | s_b[8] | temb[8] | state[S]
+        float* e_sw = e_aw + 8 * p.D;
+        float* e_ab = e_sw + 8 * p.S;
+        float* e_sb = e_ab + 8;
+        float* e_te = e_sb + 8;
+        float* e_st = e_te + 8;
+        if (i < p.n_steps && c < kW / 8) {
+          for (int e = wt; e < 8 * p.D; e += kWorkers) e_aw[e] = __ldg(p.a_w + (size_t)c * 8 * p.D + e);
+          for (int e = wt; e < 8 * p.S; e += kWorkers) e_sw[e] = __ldg(p.s_w + (size_t)c * 8 * p.S + e);
+          if (wt < 8) {
+            e_ab[wt] = __ldg(p.a_b + c * 8 + wt);
+            e_sb[wt] = __ldg(p.s_b + c * 8 + wt);
+            e_te[wt] = __ldg(p.temb + (size_t)i * kW + c * 8 + wt);
+          }
+          if (wt < p.S) e_st[wt] = __ldg(p.state + wt);
+        }
         if (i > 0) {
           const float* Aprev = p.A + ((i - 1) & 1) * HD_;
           const float* ssqf = p.ssq1 + (size_t)p.L * kTok;
-          for (int e0 = wt; e0 < HD_; e0 += 4 * kWorkers) {
-            float hv[4], ap[4], rf[4];
+          for (int e0 = wt; e0 < HD_; e0 += 8 * kWorkers) {  // one round of loads (H * D <= 2048)
+            float hv[8], ap[8], rf[8];
 #pragma unroll
-            for (int z = 0; z < 4; ++z) {
+            for (int z = 0; z < 8; ++z) {
               const int e = e0 + z * kWorkers;
               if (e < HD_) {
                 hv[z] = __ldcg(p.acc_head + e);
@@ -827,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
               }
             }
 #pragma unroll
-            for (int z = 0; z < 4; ++z) {
+            for (int z = 0; z < 8; ++z) {
               const int e = e0 + z * kWorkers;
               if (e >= HD_) continue;
               const int d = e % p.D;
@@ -854,24 +874,23 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(const __grid_consta
           if (c < kW / 8) {
             // features n = 8c + (wt & 7), tokens wt >> 3 and +32 (embed_kernel's
             // FMA order); x fp32 + its bf16 copy + the first RMSNorm's sums
-            const int n = c * 8 + (wt & 7);
-            const float temb = __ldg(p.temb + (size_t)i * kW + n);
+            const int n = c * 8 + (wt & 7), nl = wt & 7;
+            const float temb = e_te[nl];
             for (int tk0 = 0; tk0 < 64; tk0 += 32) {
               const int tk = tk0 + (wt >> 3);
               float v = 0.f;
               if (tk == 0) {
-                v = __ldg(p.s_b + n);
-                for (int cc = 0; cc < p.S; ++cc) v = fmaf(__ldg(p.s_w + (size_t)n * p.S + cc), __ldg(p.state + cc), v);
+                v = e_sb[nl];
+                for (int cc = 0; cc < p.S; ++cc) v = fmaf(e_sw[nl * p.S + cc], e_st[cc], v);
               } else if (tk < p.T) {
-                v = __ldg(p.a_b + n);
+                v = e_ab[nl];
                 const float* arow = A_new + (tk - 1) * p.D;
-                const float4* w4 = reinterpret_cast<const float4*>(p.a_w + (size_t)n * p.D);
+                const float* wrow = e_aw + nl * p.D;
                 for (int c4 = 0; c4 < p.D / 4; ++c4) {
-                  const float4 w = __ldg(w4 + c4);
-                  v = fmaf(w.x, arow[4 * c4], v);
-                  v = fmaf(w.y, arow[4 * c4 + 1], v);
-                  v = fmaf(w.z, arow[4 * c4 + 2], v);
-                  v = fmaf(w.w, arow[4 * c4 + 3], v);
+                  v = fmaf(wrow[4 * c4], arow[4 * c4], v);
+                  v = fmaf(wrow[4 * c4 + 1], arow[4 * c4 + 1], v);
+                  v = fmaf(wrow[4 * c4 + 2], arow[4 * c4 + 2], v);
+                  v = fmaf(wrow[4 * c4 + 3], arow[4 * c4 + 3], v);
                 }
                 v = v + temb;
               }

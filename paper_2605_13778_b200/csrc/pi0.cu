@@ -1563,6 +1563,7 @@ static bool b1_supported(const Handle& h) {
   if (getenv("SF_NO_B1ENGINE")) return false;
   if (c.width != b1::kW || c.q_heads != b1::kHeads || c.head_dim != b1::kHD || c.mlp != b1::kMlp) return false;
   if (c.horizon + 1 > b1::kTok || c.action_dim % 4 != 0 || c.action_dim > 32 || c.layers > b1::kMaxL) return false;
+  if (c.state_dim > 256) return false;  // the E stage stages 8 state-weight rows + the state in 16 KB
   if (!h.k_img || c.prefix_len < 64) return false;
   static int nsm = -1;
   if (nsm < 0) {
