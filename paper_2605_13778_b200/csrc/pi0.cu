@@ -362,8 +362,58 @@ struct StatusParams {
 };
 
 // dst[0 .. n) = v (the per-env gripper sign when the caller passes one sign)
-__global__ void fill_f32_kernel(float* dst, int n, float v) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = v;
+// Several small device copies / fills of 32-bit words in ONE launch (copy j
+// = blockIdx.y; src == nullptr fills with fill[j]): the per-call staging of a
+// speculative round was 4 input + 5 output cudaMemcpyAsync nodes at ~2 us of
+// GPU time each around the graph.
+struct CopyList {
+  static constexpr int kMax = 10;
+  const void* src[kMax];
+  void* dst[kMax];
+  long long n[kMax];  // 32-bit words
+  float fill[kMax];
+  int count;
+};
+
+__global__ void copy_list_kernel(const CopyList cl) {
+  const int j = blockIdx.y;
+  const uint32_t* src = static_cast<const uint32_t*>(cl.src[j]);
+  uint32_t* dst = static_cast<uint32_t*>(cl.dst[j]);
+  const long long n = cl.n[j];
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, nt = (long long)gridDim.x * blockDim.x;
+  if (!src) {
+    const uint32_t v = __float_as_uint(cl.fill[j]);
+    for (long long i = tid; i < n; i += nt) dst[i] = v;
+    return;
+  }
+  long long done = 0;
+  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    const long long n4 = n >> 2;
+    for (long long i = tid; i < n4; i += nt)
+      reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+    done = n4 << 2;
+  }
+  for (long long i = done + tid; i < n; i += nt) dst[i] = __ldg(src + i);
+}
+
+static void copy_list_add(CopyList& cl, void* dst, const void* src, long long words, float fill = 0.f) {
+  cl.dst[cl.count] = dst;
+  cl.src[cl.count] = src;
+  cl.n[cl.count] = words;
+  cl.fill[cl.count] = fill;
+  ++cl.count;
+}
+
+static int copy_list_launch(const CopyList& cl, cudaStream_t s) {
+  if (cl.count == 0) return SF_OK;
+  long long mx = 1;
+  for (int j = 0; j < cl.count; ++j) mx = cl.n[j] > mx ? cl.n[j] : mx;
+  const long long blocks = (mx / 4 + 255) / 256;
+  dim3 grid((unsigned)(blocks < 1 ? 1 : (blocks > 296 ? 296 : blocks)), (unsigned)cl.count);
+  copy_list_kernel<<<grid, 256, 0, s>>>(cl);
+  SF_CHECK_CUDA(cudaGetLastError());
+  sf::count_launch();
+  return SF_OK;
 }
 
 __global__ void status_init_kernel(const StatusParams p) {
@@ -1832,21 +1882,17 @@ static int verify_common(Handle* h, int n_envs, const sf_verify_cfg_t* cfg, cons
   if ((rc = ensure_temb(*h, cfg, s))) return rc;
   const sf_ae_config_t& c = h->cfg;
   const size_t hd = (size_t)n_envs * c.horizon * c.action_dim;
+  // inputs -> the graph's buffers in one launch (a missing signs vector is
+  // one sign for every env, filled on the stream: no host staging, no sync)
+  CopyList cin{};
   if (with_draft)
-    SF_CHECK_CUDA(cudaMemcpyAsync(b->obs, in, (size_t)n_envs * c.draft_in * 4,
-                                  cudaMemcpyDeviceToDevice, s));
+    copy_list_add(cin, b->obs, in, (long long)n_envs * c.draft_in);
   else
-    SF_CHECK_CUDA(cudaMemcpyAsync(b->draft, in, hd * 4, cudaMemcpyDeviceToDevice, s));
-  SF_CHECK_CUDA(cudaMemcpyAsync(b->eps, eps, hd * 4, cudaMemcpyDeviceToDevice, s));
-  SF_CHECK_CUDA(cudaMemcpyAsync(b->state, state, (size_t)n_envs * c.state_dim * 4,
-                                cudaMemcpyDeviceToDevice, s));
-  if (signs) {
-    SF_CHECK_CUDA(cudaMemcpyAsync(b->signs, signs, n_envs * 4, cudaMemcpyDeviceToDevice, s));
-  } else {  // one sign for every env: filled on the stream (no host staging, no sync)
-    fill_f32_kernel<<<(n_envs + 255) / 256, 256, 0, s>>>(b->signs, n_envs, (float)cfg->current_sign);
-    SF_CHECK_CUDA(cudaGetLastError());
-    sf::count_launch();
-  }
+    copy_list_add(cin, b->draft, in, (long long)hd);
+  copy_list_add(cin, b->eps, eps, (long long)hd);
+  copy_list_add(cin, b->state, state, (long long)n_envs * c.state_dim);
+  copy_list_add(cin, b->signs, signs, n_envs, (float)cfg->current_sign);
+  if ((rc = copy_list_launch(cin, s))) return rc;
   const bool pdl = (flags & SF_AE_PDL) != 0;
   if (flags & SF_AE_GRAPH) {
     const int key = cfg_key(cfg) ^ (pdl ? 0x5bd1e995 : 0) ^ (with_draft ? 0x2f3a7c11 : 0);
@@ -1863,18 +1909,13 @@ static int verify_common(Handle* h, int n_envs, const sf_verify_cfg_t* cfg, cons
     if ((rc = enqueue_verify(*h, *b, cfg, s, pdl, with_draft))) return rc;
   }
   const size_t khd = hd * cfg->k;
-  if (out->draft)
-    SF_CHECK_CUDA(cudaMemcpyAsync(out->draft, b->draft, hd * 4, cudaMemcpyDeviceToDevice, s));
-  if (out->reconstructed)
-    SF_CHECK_CUDA(cudaMemcpyAsync(out->reconstructed, b->recon, khd * 4, cudaMemcpyDeviceToDevice, s));
-  if (out->distances)
-    SF_CHECK_CUDA(cudaMemcpyAsync(out->distances, b->dist, (size_t)n_envs * cfg->k * c.horizon * 4,
-                                  cudaMemcpyDeviceToDevice, s));
-  SF_CHECK_CUDA(cudaMemcpyAsync(out->branch_prefixes, b->branch, (size_t)n_envs * cfg->k * 4,
-                                cudaMemcpyDeviceToDevice, s));
-  SF_CHECK_CUDA(cudaMemcpyAsync(out->result, b->result, (size_t)n_envs * SF_RESULT_WORDS * 4,
-                                cudaMemcpyDeviceToDevice, s));
-  return SF_OK;
+  CopyList co{};
+  if (out->draft) copy_list_add(co, out->draft, b->draft, (long long)hd);
+  if (out->reconstructed) copy_list_add(co, out->reconstructed, b->recon, (long long)khd);
+  if (out->distances) copy_list_add(co, out->distances, b->dist, (long long)n_envs * cfg->k * c.horizon);
+  copy_list_add(co, out->branch_prefixes, b->branch, (long long)n_envs * cfg->k);
+  copy_list_add(co, out->result, b->result, (long long)n_envs * SF_RESULT_WORDS);
+  return copy_list_launch(co, s);
 }
 
 extern "C" int sf_ae_verify(void* handle, int n_envs, const sf_verify_cfg_t* cfg, const float* draft,
@@ -1999,11 +2040,11 @@ extern "C" int sf_ae_denoise_envs(void* handle, int n_envs, const int* env_map, 
   const size_t hd = (size_t)n_envs * c.horizon * c.action_dim;
   // batch env e attends to pool slot env_map[e] (fallback envs compacted by
   // sf_replan_update); identity when no map is given
-  SF_CHECK_CUDA(cudaMemcpyAsync(b->env_map, env_map ? env_map : b->env_ident, sizeof(int) * n_envs,
-                                cudaMemcpyDeviceToDevice, s));
-  SF_CHECK_CUDA(cudaMemcpyAsync(b->draft, start, hd * 4, cudaMemcpyDeviceToDevice, s));
-  SF_CHECK_CUDA(cudaMemcpyAsync(b->state, state, (size_t)n_envs * c.state_dim * 4,
-                                cudaMemcpyDeviceToDevice, s));
+  CopyList cin{};
+  copy_list_add(cin, b->env_map, env_map ? env_map : b->env_ident, n_envs);
+  copy_list_add(cin, b->draft, start, (long long)hd);
+  copy_list_add(cin, b->state, state, (long long)n_envs * c.state_dim);
+  if ((rc = copy_list_launch(cin, s))) return rc;
   const bool pdl = (flags & SF_AE_PDL) != 0;
   if (flags & SF_AE_GRAPH) {
     const int key = 0x40000000 | (num_steps << 1) | (pdl ? 1 : 0);
@@ -2019,9 +2060,10 @@ extern "C" int sf_ae_denoise_envs(void* handle, int n_envs, const int* env_map, 
   } else {
     if ((rc = enqueue_denoise(*h, *b, num_steps, s, pdl))) return rc;
   }
-  SF_CHECK_CUDA(cudaMemcpyAsync(chunk_out, b->draft, hd * 4, cudaMemcpyDeviceToDevice, s));
-  SF_CHECK_CUDA(cudaMemcpyAsync(status, b->status, (size_t)n_envs * 8, cudaMemcpyDeviceToDevice, s));
-  return SF_OK;
+  CopyList co{};
+  copy_list_add(co, chunk_out, b->draft, (long long)hd);
+  copy_list_add(co, status, b->status, 2LL * n_envs);
+  return copy_list_launch(co, s);
 }
 
 namespace {
@@ -2224,31 +2266,26 @@ extern "C" int sf_ae_replan_round(void* handle, int n_envs, const sf_verify_cfg_
   Replan& R = *it->second;
   Buffers& bf = *R.bf;
   const size_t hd = (size_t)n_envs * c.horizon * c.action_dim;
-  SF_CHECK_CUDA(cudaMemcpyAsync(bf.obs, obs, (size_t)n_envs * c.draft_in * 4, cudaMemcpyDeviceToDevice, s));
-  SF_CHECK_CUDA(cudaMemcpyAsync(bf.eps, eps_verify, hd * 4, cudaMemcpyDeviceToDevice, s));
-  SF_CHECK_CUDA(cudaMemcpyAsync(R.eps_d, eps_denoise, hd * 4, cudaMemcpyDeviceToDevice, s));
-  SF_CHECK_CUDA(cudaMemcpyAsync(bf.state, state, (size_t)n_envs * c.state_dim * 4, cudaMemcpyDeviceToDevice, s));
-  SF_CHECK_CUDA(cudaMemcpyAsync(bf.signs, signs, (size_t)n_envs * 4, cudaMemcpyDeviceToDevice, s));
+  CopyList cin{};
+  copy_list_add(cin, bf.obs, obs, (long long)n_envs * c.draft_in);
+  copy_list_add(cin, bf.eps, eps_verify, (long long)hd);
+  copy_list_add(cin, R.eps_d, eps_denoise, (long long)hd);
+  copy_list_add(cin, bf.state, state, (long long)n_envs * c.state_dim);
+  copy_list_add(cin, bf.signs, signs, n_envs);
+  if ((rc = copy_list_launch(cin, s))) return rc;
   SF_CHECK_CUDA(cudaGraphLaunch(R.exec, s));
   sf::count_launch(R.fixed_kernels);
-  SF_CHECK_CUDA(cudaMemcpyAsync(out->chunk, R.chunk, hd * 4, cudaMemcpyDeviceToDevice, s));
-  if (out->chunk_raw && policy->std_mean)
-    SF_CHECK_CUDA(cudaMemcpyAsync(out->chunk_raw, R.chunk_raw, hd * 4, cudaMemcpyDeviceToDevice, s));
-  SF_CHECK_CUDA(cudaMemcpyAsync(out->path, R.path, (size_t)n_envs * 4, cudaMemcpyDeviceToDevice, s));
-  SF_CHECK_CUDA(cudaMemcpyAsync(out->planned, R.planned, (size_t)n_envs * 4, cudaMemcpyDeviceToDevice, s));
-  if (out->switch_in_executed)
-    SF_CHECK_CUDA(cudaMemcpyAsync(out->switch_in_executed, R.sie, (size_t)n_envs * 4, cudaMemcpyDeviceToDevice, s));
-  if (out->nonfinite)
-    SF_CHECK_CUDA(cudaMemcpyAsync(out->nonfinite, R.bad, (size_t)n_envs * 4, cudaMemcpyDeviceToDevice, s));
-  if (out->branch_prefixes)
-    SF_CHECK_CUDA(cudaMemcpyAsync(out->branch_prefixes, bf.branch, (size_t)n_envs * cfg->k * 4,
-                                  cudaMemcpyDeviceToDevice, s));
-  if (out->result)
-    SF_CHECK_CUDA(cudaMemcpyAsync(out->result, bf.result, (size_t)n_envs * SF_RESULT_WORDS * 4,
-                                  cudaMemcpyDeviceToDevice, s));
-  if (out->n_fallback)
-    SF_CHECK_CUDA(cudaMemcpyAsync(out->n_fallback, R.fb_count, 4, cudaMemcpyDeviceToDevice, s));
-  return SF_OK;
+  CopyList co{};
+  copy_list_add(co, out->chunk, R.chunk, (long long)hd);
+  if (out->chunk_raw && policy->std_mean) copy_list_add(co, out->chunk_raw, R.chunk_raw, (long long)hd);
+  copy_list_add(co, out->path, R.path, n_envs);
+  copy_list_add(co, out->planned, R.planned, n_envs);
+  if (out->switch_in_executed) copy_list_add(co, out->switch_in_executed, R.sie, n_envs);
+  if (out->nonfinite) copy_list_add(co, out->nonfinite, R.bad, n_envs);
+  if (out->branch_prefixes) copy_list_add(co, out->branch_prefixes, bf.branch, (long long)n_envs * cfg->k);
+  if (out->result) copy_list_add(co, out->result, bf.result, (long long)n_envs * SF_RESULT_WORDS);
+  if (out->n_fallback) copy_list_add(co, out->n_fallback, R.fb_count, 1);
+  return copy_list_launch(co, s);
 }
 
 extern "C" int sf_ae_velocity(void* handle, int n_envs, int rows, const float* x, const double* taus,
