@@ -465,11 +465,18 @@ def run_ours(args, rank, world, local):
     rp = BatchedReplanner(ae, E, vcfg, replan_size=REPLAN, periodic_refresh=PF)
     paths_acc = torch.zeros(5, dtype=torch.int64, device=dev)
     fb_rounds = torch.zeros(1, dtype=torch.int64, device=dev)
+    fl_rounds = torch.zeros(2, dtype=torch.int64, device=dev)  # rounds with an attempt / with a compacted one
+    fl_max_sub = []  # largest flash bucket below E (host value of the built graph)
 
     def round_step():
         _, path, _, _, _ = rp.round(obs, eps_v, eps_d, state, signs)
+        if not fl_max_sub:
+            fl_max_sub.append(rp.kernel_counts()[3])
         paths_acc.add_(torch.bincount(path.long(), minlength=5)[:5])
         fb_rounds.add_((rp.n_fallback > 0).long())
+        n_att = (path <= 2).sum()
+        fl_rounds[0].add_((n_att > 0).long())
+        fl_rounds[1].add_(((n_att > 0) & (n_att <= fl_max_sub[0])).long())
 
     # ---------------- warm-up: round 0 is a full round for every env (no context
     # yet); later rounds settle into the flash / periodic / fallback mix
@@ -479,6 +486,7 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     paths_acc.zero_()
     fb_rounds.zero_()
+    fl_rounds.zero_()
 
     # ---------------- timed region: replanning rounds (device time, max over ranks)
     if world > 1:
@@ -492,9 +500,12 @@ def run_ours(args, rank, world, local):
             round_step()
         b.record()
         b.synchronize()
-    # the Euler bucket body of the graph SWITCH runs only when selected: its
-    # kernels are added per round that ran the full path (device counter)
-    launches = _capi.launch_count() - launches0 + int(fb_rounds.item()) * rp.body_kernels
+    # the flash-attempt and Euler bucket bodies of the graph SWITCHes run only
+    # when selected: their kernels are added per round that ran them (device
+    # counters); the host counter holds the fixed kernels + staging launches
+    kc = rp.kernel_counts()
+    fl = fl_rounds.tolist()
+    launches = (_capi.launch_count() - launches0 + int(fb_rounds.item()) * kc[2] + fl[0] * kc[1] + fl[1] * 2)
     ms = max_over_ranks(a.elapsed_time(b) / args.steps, dev)
     path_counts = gather_counts(paths_acc.clone()).tolist()
     value = args.envs / (ms / 1e3)

@@ -152,8 +152,9 @@ typedef struct {
                                 env's current sign (runtime.py:321-323); 0 otherwise */
   int* nonfinite;            /* [n] 1: the chunk is non-finite (the reference raises
                                 FloatingPointError, flowpolicy.py:290 / verifier.py:89) */
-  int* branch_prefixes;      /* [n][K] of the flash attempt (may be NULL) */
-  int* result;               /* [n][SF_RESULT_WORDS] of the flash attempt (may be NULL) */
+  int* branch_prefixes;      /* [n][K] of the flash attempt, -1 without one (may be NULL) */
+  int* result;               /* [n][SF_RESULT_WORDS] of the flash attempt; words 0..SF_RES_NONFINITE
+                                -1 for envs that made none this round (may be NULL) */
   int* n_fallback;           /* [1] envs that ran the full path (may be NULL) */
 } sf_replan_out_t;
 
@@ -164,6 +165,13 @@ int sf_ae_replan_round(void* handle, int n_envs, const sf_verify_cfg_t* cfg,
                        const sf_replan_policy_t* policy, const float* obs, const float* eps_verify,
                        const float* eps_denoise, const float* state, const float* signs, int* fsr,
                        int* has_cache, const sf_replan_out_t* out, int flags, void* stream);
+
+/* Kernel counts of the last sf_ae_replan_round graph (launch accounting; the
+ * SWITCH bodies run only when selected on the device): out4 = {kernels of a
+ * round with neither an attempt nor the full path, kernels of the flash
+ * attempt's verify (+2 gather / scatter when the attempting envs fit a bucket
+ * <= out4[3]), kernels of an Euler bucket body, largest flash bucket below n}. */
+int sf_ae_replan_kernels(void* handle, int* out4);
 
 /* Field protocol: velocities for n_envs x rows states x [..][rows][H][D] at
  * taus[rows] (HOST). */

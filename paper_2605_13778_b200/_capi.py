@@ -119,6 +119,7 @@ SIGNATURES = {
     "sf_ae_velocity": (_I, [_P, _I, _I, _P, _P, _P, _P, _P]),
     "sf_ae_replan_round": (_I, [_P, _I, ctypes.POINTER(SfVerifyCfg), ctypes.POINTER(SfReplanPolicy), _P, _P,
                                 _P, _P, _P, _P, _P, ctypes.POINTER(SfReplanOut), _I, _P]),
+    "sf_ae_replan_kernels": (_I, [_P, _P]),
     "sf_fill_hash_uniform": (_I, [_P, _I, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64,
                                   ctypes.c_double, _P]),
     # include/specflow_b200_internal.h (kernel unit-test hooks)

@@ -491,6 +491,143 @@ __global__ void __launch_bounds__(1024) replan_select_kernel(const ReplanSelectP
   }
 }
 
+struct FlashSelectParams {
+  int n;
+  const int* fsr;
+  const int* has_cache;
+  int mode_flash, pf;
+  int* use;       // [n] 1 = the env makes a flash attempt this round
+  int* fl_idx;    // [n] attempting envs in env order
+  int* fl_count;  // [1]
+  int n_buckets;
+  int bucket[kMaxBuckets];
+  cudaGraphConditionalHandle cond;
+};
+
+// Which envs make a flash attempt this round (runtime.py:242-253: a cached
+// context and no forced periodic refresh), compacted in env order; the SWITCH
+// value is the smallest pre-captured flash bucket holding them (n_buckets =
+// none: a round of full rounds only runs no speculative attempt at all).
+__global__ void __launch_bounds__(1024) flash_select_kernel(const FlashSelectParams p) {
+  __shared__ int warp_tot[32];
+  __shared__ int base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) base = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < p.n; c0 += blockDim.x) {
+    const int e = c0 + tid;
+    int u = 0;
+    if (e < p.n) {
+      const bool forced = p.pf > 0 && p.fsr[e] >= p.pf;
+      u = p.mode_flash && p.has_cache[e] && !forced;
+      p.use[e] = u;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, u);
+    if (lane == 0) warp_tot[warp] = __popc(m);
+    __syncthreads();
+    if (warp == 0) {
+      int v = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+      }
+      warp_tot[lane] = v;
+    }
+    __syncthreads();
+    if (u) p.fl_idx[base + (warp ? warp_tot[warp - 1] : 0) + __popc(m & ((1u << lane) - 1u))] = e;
+    __syncthreads();
+    if (tid == 0) base += warp_tot[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    *p.fl_count = base;
+    unsigned sel = (unsigned)p.n_buckets;
+    for (int i = 0; i < p.n_buckets && base > 0; ++i)
+      if (base <= p.bucket[i]) {
+        sel = (unsigned)i;
+        break;
+      }
+    cudaGraphSetConditional(p.cond, sel);
+  }
+}
+
+// flash bucket row j <- attempting env fl_idx[j] (rows past the count repeat
+// the first one; their results are dropped): observation, verify noise,
+// state, sign and the env's prefix-KV slot
+struct FlashGatherParams {
+  const int* fl_idx;
+  const int* fl_count;
+  int Bk, F, HD, S;
+  const float *obs, *eps, *state, *signs;
+  float *obs_o, *eps_o, *state_o, *signs_o;
+  int* env_map;
+};
+
+__global__ void flash_gather_kernel(const FlashGatherParams p) {
+  const int cnt = *p.fl_count;
+  const int per = p.F + p.HD + p.S + 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.Bk * per; i += gridDim.x * blockDim.x) {
+    const int j = i / per;
+    int c = i - j * per;
+    const int e = p.fl_idx[j < cnt ? j : 0];
+    if (c < p.F) {
+      p.obs_o[(size_t)j * p.F + c] = p.obs[(size_t)e * p.F + c];
+    } else if ((c -= p.F) < p.HD) {
+      p.eps_o[(size_t)j * p.HD + c] = p.eps[(size_t)e * p.HD + c];
+    } else if ((c -= p.HD) < p.S) {
+      p.state_o[(size_t)j * p.S + c] = p.state[(size_t)e * p.S + c];
+    } else {
+      p.signs_o[j] = p.signs[e];
+      p.env_map[j] = e;
+    }
+  }
+}
+
+// attempt results back to their envs: result words, branch prefixes, draft
+struct FlashScatterParams {
+  const int* fl_idx;
+  const int* fl_count;
+  int K, HD;
+  const int *result, *branch;
+  const float* draft;
+  int *result_o, *branch_o;
+  float* draft_o;
+};
+
+__global__ void flash_scatter_kernel(const FlashScatterParams p) {
+  const int cnt = *p.fl_count;
+  const int per = SF_RESULT_WORDS + p.K + p.HD;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt * per; i += gridDim.x * blockDim.x) {
+    const int j = i / per;
+    int c = i - j * per;
+    const int e = p.fl_idx[j];
+    if (c < SF_RESULT_WORDS) {
+      p.result_o[e * SF_RESULT_WORDS + c] = p.result[j * SF_RESULT_WORDS + c];
+    } else if ((c -= SF_RESULT_WORDS) < p.K) {
+      p.branch_o[e * p.K + c] = p.branch[j * p.K + c];
+    } else {
+      c -= p.K;
+      p.draft_o[(size_t)e * p.HD + c] = p.draft[(size_t)j * p.HD + c];
+    }
+  }
+}
+
+// envs without an attempt this round: result words 0..SF_RES_NONFINITE and branch prefixes -1
+// (the reference's RoundRecord has no prefix / branch prefixes for them)
+__global__ void flash_mark_kernel(const int* __restrict__ use, int n, int K, int* __restrict__ result,
+                                  int* __restrict__ branch) {
+  const int per = SF_RESULT_WORDS + K;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n * per; i += gridDim.x * blockDim.x) {
+    const int e = i / per, c = i - e * per;
+    if (use[e]) continue;
+    if (c < SF_RESULT_WORDS) {
+      if (c <= SF_RES_NONFINITE) result[e * SF_RESULT_WORDS + c] = -1;  // reserved words untouched
+    } else {
+      branch[e * K + (c - SF_RESULT_WORDS)] = -1;
+    }
+  }
+}
+
 // chunk <- draft for every env (accepted envs execute it); clear the flags
 __global__ void chunk_init_kernel(const float* __restrict__ draft, float* __restrict__ chunk,
                                   int* __restrict__ bad, int n, int hd) {
@@ -641,6 +778,7 @@ struct Buffers {
 };
 
 struct Handle {
+  int replan_kernels[4] = {0, 0, 0, 0};  // last replanning round: fixed, flash verify, Euler body, max sub-n flash bucket
   sf_ae_config_t cfg{};
   sf_ae_weights_t w{};
   const bf16* k_prefix = nullptr;   // [L][E][P][256]
@@ -680,12 +818,18 @@ struct Replan {
   float* stdv = nullptr;             // [D]
   int *path = nullptr, *planned = nullptr, *sie = nullptr, *bad = nullptr;
   int *fb_idx = nullptr, *fb_count = nullptr;
+  std::vector<int> fbuckets;         // flash-attempt bucket sizes (the last one = n runs on bf)
+  std::vector<Buffers*> fbb;         // verify buffers per flash bucket (nullptr for n: bf)
+  int *use = nullptr, *fl_idx = nullptr, *fl_count = nullptr;
   cudaGraphExec_t exec = nullptr;
-  int fixed_kernels = 0;             // kernels of a round without the full path
+  int fixed_kernels = 0;             // kernels of a round with neither an attempt nor the full path
+  int flash_body_kernels = 0;        // kernels of a compacted flash-attempt body (the n-env body: 2 fewer)
+  int euler_body_kernels = 0;        // kernels of an Euler bucket body
   ~Replan() {
     if (exec) cudaGraphExecDestroy(exec);
     for (void* q : {(void*)eps_d, (void*)chunk, (void*)chunk_raw, (void*)mean, (void*)stdv, (void*)path,
-                    (void*)planned, (void*)sie, (void*)bad, (void*)fb_idx, (void*)fb_count})
+                    (void*)planned, (void*)sie, (void*)bad, (void*)fb_idx, (void*)fb_count, (void*)use,
+                    (void*)fl_idx, (void*)fl_count})
       if (q) cudaFree(q);
   }
 };
@@ -2077,6 +2221,51 @@ std::vector<int> replan_buckets(int n) {
   return b;
 }
 
+// flash-attempt buckets: powers of two up to 32, then multiples of 32, capped
+// at n (the attempt costs ~4x an Euler step per env: finer steps)
+std::vector<int> flash_buckets(int n) {
+  std::vector<int> b;
+  for (int v = 1; v < 32 && v < n; v *= 2) b.push_back(v);
+  for (int v = 32; v < n; v += 32) b.push_back(v);
+  b.push_back(n);
+  return b;
+}
+
+// conditional handle of a SWITCH over `nb` bodies in the graph being captured on cs
+int make_switch_handle(cudaStream_t cs, int nb, cudaGraphConditionalHandle* cond) {
+  cudaStreamCaptureStatus st;
+  cudaGraph_t cg = nullptr;
+  if (cudaStreamGetCaptureInfo(cs, &st, nullptr, &cg, nullptr, nullptr) != cudaSuccess || !cg) return SF_ECUDA;
+  if (cudaGraphConditionalHandleCreate(cond, cg, (unsigned)nb, cudaGraphCondAssignDefault) != cudaSuccess) {
+    sf::set_error("cudaGraphConditionalHandleCreate failed");
+    return SF_ECUDA;
+  }
+  return SF_OK;
+}
+
+// the SWITCH node at the capture position of cs (its bodies: cp->conditional.phGraph_out)
+int add_switch_node(cudaStream_t cs, cudaGraphConditionalHandle cond, int nb, cudaGraphNodeParams* cp) {
+  cudaStreamCaptureStatus st;
+  cudaGraph_t cg = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  if (cudaStreamGetCaptureInfo(cs, &st, nullptr, &cg, &deps, &ndeps) != cudaSuccess) return SF_ECUDA;
+  memset(cp, 0, sizeof(*cp));
+  cp->type = cudaGraphNodeTypeConditional;
+  cp->conditional.handle = cond;
+  cp->conditional.type = cudaGraphCondTypeSwitch;
+  cp->conditional.size = (unsigned)nb;
+  cudaGraphNode_t node;
+  const cudaError_t ce = cudaGraphAddNode(&node, cg, deps, ndeps, cp);
+  if (ce != cudaSuccess) {
+    sf::set_error("conditional SWITCH node: %s", cudaGetErrorString(ce));
+    return SF_ECUDA;
+  }
+  if (cudaStreamUpdateCaptureDependencies(cs, &node, 1, cudaStreamSetCaptureDependencies) != cudaSuccess)
+    return SF_ECUDA;
+  return SF_OK;
+}
+
 int build_replan(Handle& h, Replan& R, int n, const sf_verify_cfg_t* cfg, const sf_replan_policy_t* pol,
                  const float* signs_unused, int* fsr, int* has_cache, bool pdl, bool fp32) {
   (void)signs_unused;
@@ -2096,11 +2285,19 @@ int build_replan(Handle& h, Replan& R, int n, const sf_verify_cfg_t* cfg, const 
     if (!b) return rc;
     R.bb.push_back(b);
   }
+  R.fbuckets = pol->mode_flash ? flash_buckets(n) : std::vector<int>{};
+  SF_REQUIRE((int)R.fbuckets.size() <= kMaxBuckets, "too many flash buckets");
+  for (int bk : R.fbuckets) {
+    Buffers* b = bk == n ? nullptr : get_buffers(h, bk, cfg->k, f32mode, &rc);
+    if (bk != n && !b) return rc;
+    R.fbb.push_back(b);
+  }
   if ((rc = dalloc(&R.eps_d, (size_t)n * hd)) || (rc = dalloc(&R.chunk, (size_t)n * hd)) ||
       (rc = dalloc(&R.chunk_raw, (size_t)n * hd)) || (rc = dalloc(&R.mean, (size_t)c.action_dim)) ||
       (rc = dalloc(&R.stdv, (size_t)c.action_dim)) || (rc = dalloc(&R.path, n)) ||
       (rc = dalloc(&R.planned, n)) || (rc = dalloc(&R.sie, n)) || (rc = dalloc(&R.bad, n)) ||
-      (rc = dalloc(&R.fb_idx, n)) || (rc = dalloc(&R.fb_count, 1)))
+      (rc = dalloc(&R.fb_idx, n)) || (rc = dalloc(&R.fb_count, 1)) || (rc = dalloc(&R.use, n)) ||
+      (rc = dalloc(&R.fl_idx, n)) || (rc = dalloc(&R.fl_count, 1)))
     return rc;
   if (pol->std_mean) {
     SF_CHECK_CUDA(cudaMemcpy(R.mean, pol->std_mean, sizeof(float) * c.action_dim, cudaMemcpyDeviceToDevice));
@@ -2112,6 +2309,7 @@ int build_replan(Handle& h, Replan& R, int n, const sf_verify_cfg_t* cfg, const 
   cudaStream_t cs = h.capture_stream;
   Buffers& bf = *R.bf;
   const int64_t before = sf_launch_count(0);
+  int64_t bodies = 0;  // kernels captured into SWITCH bodies (they run only when selected)
   cudaGraph_t g = nullptr;
   SF_CHECK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   auto fail = [&](int code) {
@@ -2121,19 +2319,82 @@ int build_replan(Handle& h, Replan& R, int n, const sf_verify_cfg_t* cfg, const 
     sf::count_launch(-(int)(sf_launch_count(0) - before));
     return code;
   };
-  // 1. the speculative attempt for every env (draft MLP -> verify -> gate -> decision)
-  if ((rc = enqueue_verify(h, bf, cfg, cs, pdl, true))) return fail(rc);
-  // 2. bookkeeping + compaction + bucket select (sets the SWITCH value)
-  cudaStreamCaptureStatus st;
-  cudaGraph_t cg = nullptr;
-  if (cudaStreamGetCaptureInfo(cs, &st, nullptr, &cg, nullptr, nullptr) != cudaSuccess || !cg)
-    return fail(SF_ECUDA);
-  cudaGraphConditionalHandle cond;
-  if (cudaGraphConditionalHandleCreate(&cond, cg, (unsigned)R.buckets.size(), cudaGraphCondAssignDefault) !=
-      cudaSuccess) {
-    sf::set_error("cudaGraphConditionalHandleCreate failed");
-    return fail(SF_ECUDA);
+  auto begin_body = [&](cudaGraph_t body_graph, size_t i) {
+    if (cudaStreamBeginCaptureToGraph(h.body_stream, body_graph, nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      sf::set_error("body capture %zu failed", i);
+      return SF_ECUDA;
+    }
+    return SF_OK;
+  };
+  auto end_body = [&](int brc, size_t i) {
+    cudaGraph_t body = nullptr;
+    const cudaError_t be = cudaStreamEndCapture(h.body_stream, &body);
+    if (brc) return brc;
+    if (be != cudaSuccess) {
+      sf::set_error("body capture %zu: %s", i, cudaGetErrorString(be));
+      return SF_ECUDA;
+    }
+    return SF_OK;
+  };
+  // 1. the speculative attempt of the envs that make one this round (a cached
+  //    context, no forced periodic refresh: runtime.py:242-253), compacted into
+  //    the smallest flash bucket (draft MLP -> verify -> gate -> decision); the
+  //    results go back to the envs' rows of bf
+  if (pol->mode_flash) {
+    cudaGraphConditionalHandle fcond;
+    if ((rc = make_switch_handle(cs, (int)R.fbuckets.size(), &fcond))) return fail(rc);
+    FlashSelectParams fs{};
+    fs.n = n;
+    fs.fsr = fsr;
+    fs.has_cache = has_cache;
+    fs.mode_flash = pol->mode_flash;
+    fs.pf = pol->periodic_refresh;
+    fs.use = R.use;
+    fs.fl_idx = R.fl_idx;
+    fs.fl_count = R.fl_count;
+    fs.n_buckets = (int)R.fbuckets.size();
+    for (int i = 0; i < fs.n_buckets; ++i) fs.bucket[i] = R.fbuckets[i];
+    fs.cond = fcond;
+    flash_select_kernel<<<1, 1024, 0, cs>>>(fs);
+    sf::count_launch(1);
+    cudaGraphNodeParams fcp{};
+    if ((rc = add_switch_node(cs, fcond, (int)R.fbuckets.size(), &fcp))) return fail(rc);
+    for (size_t i = 0; i < R.fbuckets.size(); ++i) {
+      if ((rc = begin_body(fcp.conditional.phGraph_out[i], i))) return fail(rc);
+      cudaStream_t bs = h.body_stream;
+      const int64_t k0 = sf_launch_count(0);
+      int brc;
+      if (!R.fbb[i]) {
+        brc = enqueue_verify(h, bf, cfg, bs, pdl, true);  // every env attempts: in place
+      } else {
+        Buffers& b = *R.fbb[i];
+        const int bk = R.fbuckets[i];
+        FlashGatherParams gp{R.fl_idx, R.fl_count, bk, c.draft_in, hd, c.state_dim, bf.obs, bf.eps, bf.state,
+                             bf.signs, b.obs, b.eps, b.state, b.signs, b.env_map};
+        const int per = c.draft_in + hd + c.state_dim + 1;
+        const int gblocks = (bk * per + 255) / 256 < 1184 ? (bk * per + 255) / 256 : 1184;
+        flash_gather_kernel<<<gblocks, 256, 0, bs>>>(gp);
+        sf::count_launch(1);
+        brc = enqueue_verify(h, b, cfg, bs, pdl, true);
+        FlashScatterParams sp{R.fl_idx, R.fl_count, cfg->k, hd, b.result, b.branch, b.draft,
+                              bf.result, bf.branch, bf.draft};
+        const int sper = SF_RESULT_WORDS + cfg->k + hd;
+        const int sblocks = (bk * sper + 255) / 256 < 1184 ? (bk * sper + 255) / 256 : 1184;
+        flash_scatter_kernel<<<sblocks, 256, 0, bs>>>(sp);
+        sf::count_launch(1);
+        R.flash_body_kernels = (int)(sf_launch_count(0) - k0);
+      }
+      bodies += sf_launch_count(0) - k0;
+      if ((rc = end_body(brc, i))) return fail(rc);
+    }
+    flash_mark_kernel<<<(n * (SF_RESULT_WORDS + cfg->k) + 255) / 256, 256, 0, cs>>>(R.use, n, cfg->k, bf.result,
+                                                                                 bf.branch);
+    sf::count_launch(1);
   }
+  // 2. bookkeeping + compaction + bucket select (sets the Euler SWITCH value)
+  cudaGraphConditionalHandle cond;
+  if ((rc = make_switch_handle(cs, (int)R.buckets.size(), &cond))) return fail(rc);
   ReplanSelectParams sp{};
   sp.n = n;
   sp.result = bf.result;
@@ -2154,32 +2415,14 @@ int build_replan(Handle& h, Replan& R, int n, const sf_verify_cfg_t* cfg, const 
       bf.draft, R.chunk, R.bad, n, hd);
   sf::count_launch(2);
   // 3. SWITCH over the Euler buckets
-  const cudaGraphNode_t* deps = nullptr;
-  size_t ndeps = 0;
-  if (cudaStreamGetCaptureInfo(cs, &st, nullptr, &cg, &deps, &ndeps) != cudaSuccess) return fail(SF_ECUDA);
   cudaGraphNodeParams cp{};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = cond;
-  cp.conditional.type = cudaGraphCondTypeSwitch;
-  cp.conditional.size = (unsigned)R.buckets.size();
-  cudaGraphNode_t cnode;
-  cudaError_t ce = cudaGraphAddNode(&cnode, cg, deps, ndeps, &cp);
-  if (ce != cudaSuccess) {
-    sf::set_error("conditional SWITCH node: %s", cudaGetErrorString(ce));
-    return fail(SF_ECUDA);
-  }
-  if (cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies) != cudaSuccess)
-    return fail(SF_ECUDA);
-  const int64_t body0 = sf_launch_count(0);
+  if ((rc = add_switch_node(cs, cond, (int)R.buckets.size(), &cp))) return fail(rc);
   for (size_t i = 0; i < R.buckets.size(); ++i) {
     Buffers& b = *R.bb[i];
     const int bk = R.buckets[i];
     cudaStream_t bs = h.body_stream;
-    if (cudaStreamBeginCaptureToGraph(bs, cp.conditional.phGraph_out[i], nullptr, nullptr, 0,
-                                      cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
-      sf::set_error("body capture %zu failed", i);
-      return fail(SF_ECUDA);
-    }
+    if ((rc = begin_body(cp.conditional.phGraph_out[i], i))) return fail(rc);
+    const int64_t k0 = sf_launch_count(0);
     const int per = hd + c.state_dim;
     const int gblocks = (bk * per + 255) / 256 < 1184 ? (bk * per + 255) / 256 : 1184;
     bucket_gather_kernel<<<gblocks, 256, 0, bs>>>(R.fb_idx, R.fb_count, bk, hd, c.state_dim, R.eps_d, bf.state,
@@ -2187,24 +2430,19 @@ int build_replan(Handle& h, Replan& R, int n, const sf_verify_cfg_t* cfg, const 
     int brc = enqueue_denoise(h, b, pol->num_steps, bs, pdl);
     const int sblocks = (bk * hd + 255) / 256 < 1184 ? (bk * hd + 255) / 256 : 1184;
     bucket_scatter_kernel<<<sblocks, 256, 0, bs>>>(R.fb_idx, R.fb_count, hd, b.draft, b.status, R.chunk, R.bad);
-    cudaGraph_t body = nullptr;
-    cudaError_t be = cudaStreamEndCapture(bs, &body);
-    if (brc) return fail(brc);
-    if (be != cudaSuccess) {
-      sf::set_error("body capture %zu: %s", i, cudaGetErrorString(be));
-      return fail(SF_ECUDA);
-    }
+    sf::count_launch(2);
+    R.euler_body_kernels = (int)(sf_launch_count(0) - k0);
+    bodies += sf_launch_count(0) - k0;
+    if ((rc = end_body(brc, i))) return fail(rc);
   }
-  // body kernels run only when their bucket is selected: not counted here
-  sf::count_launch(-(int)(sf_launch_count(0) - body0));
   // 4. non-finite flags, switch_in_executed, destandardize
   ReplanFinalParams fp{n, c.horizon, c.action_dim, R.path, R.planned, bf.result, bf.signs, R.chunk, R.bad,
                        R.sie, pol->std_mean ? R.chunk_raw : nullptr, R.mean, R.stdv};
   replan_finalize_kernel<<<(n * 32 + 255) / 256, 256, 0, cs>>>(fp);
   sf::count_launch(1);
-  ce = cudaStreamEndCapture(cs, &g);
-  R.fixed_kernels = (int)(sf_launch_count(0) - before);
-  sf::count_launch(-R.fixed_kernels);
+  cudaError_t ce = cudaStreamEndCapture(cs, &g);
+  R.fixed_kernels = (int)(sf_launch_count(0) - before - bodies);
+  sf::count_launch(-(int)(sf_launch_count(0) - before));  // launched per replay, counted there
   if (ce != cudaSuccess) {
     sf::set_error("replan capture: %s", cudaGetErrorString(ce));
     if (g) cudaGraphDestroy(g);
@@ -2275,6 +2513,10 @@ extern "C" int sf_ae_replan_round(void* handle, int n_envs, const sf_verify_cfg_
   if ((rc = copy_list_launch(cin, s))) return rc;
   SF_CHECK_CUDA(cudaGraphLaunch(R.exec, s));
   sf::count_launch(R.fixed_kernels);
+  h->replan_kernels[0] = R.fixed_kernels;
+  h->replan_kernels[1] = R.flash_body_kernels ? R.flash_body_kernels - 2 : 0;
+  h->replan_kernels[2] = R.euler_body_kernels;
+  h->replan_kernels[3] = R.fbuckets.size() > 1 ? R.fbuckets[R.fbuckets.size() - 2] : 0;
   CopyList co{};
   copy_list_add(co, out->chunk, R.chunk, (long long)hd);
   if (out->chunk_raw && policy->std_mean) copy_list_add(co, out->chunk_raw, R.chunk_raw, (long long)hd);
@@ -2286,6 +2528,13 @@ extern "C" int sf_ae_replan_round(void* handle, int n_envs, const sf_verify_cfg_
   if (out->result) copy_list_add(co, out->result, bf.result, (long long)n_envs * SF_RESULT_WORDS);
   if (out->n_fallback) copy_list_add(co, out->n_fallback, R.fb_count, 1);
   return copy_list_launch(co, s);
+}
+
+extern "C" int sf_ae_replan_kernels(void* handle, int* out4) {
+  auto* h = static_cast<Handle*>(handle);
+  SF_REQUIRE(h && out4, "null argument");
+  for (int i = 0; i < 4; ++i) out4[i] = h->replan_kernels[i];
+  return SF_OK;
 }
 
 extern "C" int sf_ae_velocity(void* handle, int n_envs, int rows, const float* x, const double* taus,

@@ -461,10 +461,18 @@ class BatchedReplanner:
     (runtime.py:321-323) and destandardizes the chunk when a Standardizer is
     given (actions.py:139-144, runtime.py:325).
 
+    The speculative attempt itself runs only for the envs that make one this
+    round (a cached context and no forced periodic refresh, runtime.py:242-253):
+    they are compacted on the device into the smallest pre-captured flash
+    bucket (powers of two up to 32, then multiples of 32) by a second SWITCH,
+    and a round of full rounds only runs no attempt at all.
+
     ``round`` returns device tensors (chunk [B, H, D] standardized, path codes
     ``_capi.SF_PATH_*``, planned, branch prefixes [B, K], flash result words
-    [B, 8]); ``chunk_raw``, ``switch_in_executed``, ``nonfinite`` and
-    ``n_fallback`` are attributes updated by the same launch."""
+    [B, 8]; branch prefixes and result words 0-4 are -1 for envs without an
+    attempt this round); ``chunk_raw``,
+    ``switch_in_executed``, ``nonfinite`` and ``n_fallback`` are attributes
+    updated by the same launch."""
 
     def __init__(self, ae: ActionExpert, n_envs: int, vcfg, replan_size: int = 12,
                  periodic_refresh: int = 2, phase_fallback: bool = True, prefix_cap: bool = True,
@@ -513,6 +521,16 @@ class BatchedReplanner:
         # [embed, layers x (qkv, attention, o, gate/up, down), head, update], scatter)
         L = ae.cfg.layers
         self.body_kernels = 3 + num_steps * ((9 * L + 2) + 2 if ae.precision == "fp32" else 3 + 5 * L)
+
+    def kernel_counts(self):
+        """(fixed, flash verify, Euler body, largest flash bucket below n) of
+        the last round's graph: a round launches `fixed` kernels, plus the
+        flash verify's (+2 gather / scatter when the attempting envs fit a
+        bucket <= the last value) when any env attempted, plus the Euler
+        body's when any env ran the full path."""
+        out = (ctypes.c_int * 4)()
+        _capi.check(_capi.lib().sf_ae_replan_kernels(self.ae._h, out), "replan kernels")
+        return tuple(out)
 
     def round(self, obs: torch.Tensor, eps_verify: torch.Tensor, eps_denoise: torch.Tensor,
               state: torch.Tensor, signs: torch.Tensor, stream=None):
