@@ -616,6 +616,7 @@ def run_ours(args, rank, world, local):
         "e2e": {"value": args.envs / (e2e_ms / 1e3), "unit": "rounds/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "BatchedReplanner.round"},
         "gpu_launches": int(launches),
+        "device_mem_gb": round((lambda fr: (fr[1] - fr[0]) / 1e9)(torch.cuda.mem_get_info(dev)), 1),
         "clocks": clk.summary(),
     }
     # deciding-distance quantile of delta over the same-sign envs (sanity of DELTA_CFG4)
