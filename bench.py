@@ -711,13 +711,22 @@ def latency_b1(ae, vcfg, obs, eps_v, state, signs, hbm_peak, peak_kind, dev):
     plug_f = host_p50_ms(lambda: integrate_flow(ae, cache, st, DenoiseConfig(10), rng), 10)
     bytes_ver = cfg.weight_bytes_streamed() + cfg.kv_bytes()
     gbs = bytes_ver / (ver / 1e3) / 1e9
+    traffic = None  # DRAM bytes of one speculative round, summed over its kernels (ncu launch list)
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("verify_b1", {}).get("dram_bytes")
+        except Exception:
+            traffic = None
     return {
         "latency_b1": {"spec_round_p50_ms": spec, "verify_p50_ms": ver, "full_round_p50_ms": full,
                        "plugin_verify_p50_ms": plug_v, "plugin_integrate_flow_p50_ms": plug_f,
                        "config": "cfg3: batch 1, K=4, H=50, D=32, P=800, 10-step Euler; plugin = "
                                  "verifier.verify / flowpolicy.integrate_flow with numpy in/out"},
         "roofline_b1": {"bound": "hbm", "kernel": "whole verify graph (batch 1)", "achieved": gbs,
-                        "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak, "traffic": None,
+                        "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak, "traffic": traffic,
+                        "traffic_source": "profiles/ncu_summary.json verify_b1 (spec round incl. draft; "
+                                          "ncu launch list, cold caches per kernel)",
                         "algorithmic_bytes": bytes_ver, "peak_kind": f"{peak_kind} hbm copy"},
     }
 
