@@ -361,7 +361,6 @@ struct StatusParams {
   int B;
 };
 
-// dst[0 .. n) = v (the per-env gripper sign when the caller passes one sign)
 // Several small device copies / fills of 32-bit words in ONE launch (copy j
 // = blockIdx.y; src == nullptr fills with fill[j]): the per-call staging of a
 // speculative round was 4 input + 5 output cudaMemcpyAsync nodes at ~2 us of
