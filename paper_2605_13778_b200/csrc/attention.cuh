@@ -83,7 +83,16 @@ struct Params {
   const uint8_t* k_img;
   const uint8_t* v_img;
   int img_blocks;      // key blocks per env image
+  // optional live env count on the device (compacted bucket bodies of the
+  // replanning graph): envs past it are not visited (batched kernels; null: n_envs)
+  const int* envs_dev;
 };
+
+__device__ __forceinline__ int live_envs(const Params& p) {
+  if (!p.envs_dev) return p.n_envs;
+  const int n = __ldg(p.envs_dev);
+  return n < p.n_envs ? n : p.n_envs;
+}
 
 #ifdef SF_TRACE
 #define ATT_STAMP(i)                                                     \
@@ -669,7 +678,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0 && smem + kPersistSmemUsed > smem_raw + kPersistSmemBytes) __trap();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles = p.tiles;
+  const int n_tiles = p.envs_dev ? live_envs(p) * p.tiles_env : p.tiles;
   // tile -> first token, env, first suffix key block (sb) and the number of key
   // blocks the tile visits: the prefix blocks plus the suffix blocks covering
   // the segments of its 16 tokens (p.n_blocks is the bound over all tiles)
@@ -1183,7 +1192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool leader = rank == 0;
   const int tiles_env = p.tiles_env;
   const int pairs_env = (tiles_env + 1) / 2;
-  const int n_pairs = p.n_envs * pairs_env;
+  const int n_pairs = live_envs(p) * pairs_env;
   const int cl = blockIdx.x >> 1, n_cl = gridDim.x >> 1;
   const int my_pairs = cl < n_pairs ? (n_pairs - 1 - cl) / n_cl + 1 : 0;
   // pair tile -> env, this CTA's first token, validity, first suffix key block

@@ -693,6 +693,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ------------------------------------------------------ batched: persistent
 
+// tiles a batched kernel visits: all, or the row tiles holding the live rows
+// (*rows_dev * rows_mul, written before this kernel by the replanning graph)
+__device__ __forceinline__ int live_tiles(const Params& p, int tile_rows, int tiles_b) {
+  if (!p.rows_dev) return p.total_tiles;
+  int r = __ldg(p.rows_dev) * p.rows_mul;
+  r = r < p.rows_a ? r : p.rows_a;
+  return ((r + tile_rows - 1) / tile_rows) * tiles_b;
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_persistent_kernel(const __grid_constant__ CUtensorMap tma_a,
@@ -721,6 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *T.tmem_slot;
+  const int live = live_tiles(p, BM, p.tiles_b);
 
   if (warp == 0) {
     if (sm100::elect_one()) {
@@ -730,7 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_x = sm100::policy_evict_first();  // activations: read by tiles_b CTAs at once
       int kiter = 0;
       bool first = true;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      for (int t = blockIdx.x; t < live; t += gridDim.x) {
         const int ta = t / p.tiles_b, tb = t % p.tiles_b;
         produce_tile(ring, &tma_b, &tma_a, kAStageBytes, 0, tb * p.bn, ta * BM, 0, p.num_kb, kiter,
                      first, pol_w, pol_x);
@@ -741,7 +751,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (sm100::elect_one()) {
       const uint32_t idesc = sm100::make_idesc_bf16(BM, p.bn);
       int kiter = 0, it = 0;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
+      for (int t = blockIdx.x; t < live; t += gridDim.x, ++it) {
         const int a = it & 1;
         if (it >= 2) sm100::mbar_wait(&T.tmem_empty[a], ((it >> 1) & 1) ^ 1);
         sm100::tc_fence_after();
@@ -758,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::pdl_wait();
     if (threadIdx.x == 64) sm100::pdl_launch_dependents();
     int it = 0;
-    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
+    for (int t = blockIdx.x; t < live; t += gridDim.x, ++it) {
       const int ta = t / p.tiles_b, tb = t % p.tiles_b;
       const int a = it & 1;
       const int m = ta * BM + lane_row;
@@ -907,6 +917,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster.sync();  // barriers of both CTAs initialised, TMEM allocated in both
   sm100::tc_fence_after();
   const uint32_t tmem = *T.tmem_slot;
+  const int live = live_tiles(p, 256, tiles_n);
 
   if (warp == 0) {
     if (sm100::elect_one()) {
@@ -920,7 +931,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_x = sm100::policy_evict_last();
       int kiter = 0;
       bool first = true;
-      for (int t = pair; t < p.total_tiles; t += n_pairs) {
+      for (int t = pair; t < live; t += n_pairs) {
         const int tm = t / tiles_n, tn = t % tiles_n;
         const int a_row = tm * 256 + rank * BM, b_row = tn * 256 + rank * BM;
         for (int i = 0; i < p.num_kb; ++i, ++kiter) {
@@ -940,7 +951,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (leader && sm100::elect_one()) {
       const uint32_t idesc = sm100::make_idesc_bf16(256, 256);
       int kiter = 0, it = 0;
-      for (int t = pair; t < p.total_tiles; t += n_pairs, ++it) {
+      for (int t = pair; t < live; t += n_pairs, ++it) {
         const int a = it & 1;
         if (it >= 2) sm100::mbar_wait(&T.tmem_empty[a], ((it >> 1) & 1) ^ 1);
         sm100::tc_fence_after();
@@ -969,7 +980,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::pdl_wait();
     if (threadIdx.x == 64) sm100::pdl_launch_dependents();
     int it = 0;
-    for (int t = pair; t < p.total_tiles; t += n_pairs, ++it) {
+    for (int t = pair; t < live; t += n_pairs, ++it) {
       const int tm = t / tiles_n, tn = t % tiles_n;
       const int a = it & 1;
       const int m = tm * 256 + rank * BM + lane_row;

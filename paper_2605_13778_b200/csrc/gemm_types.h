@@ -66,6 +66,11 @@ struct Params {
   uint32_t smem_stage_region;  // bytes reserved for the TMA ring (>= split-K staging)
   unsigned long long* dbg;     // optional %globaltimer stamps of CTA (0,0,0) (null: off)
   float* ws;                   // split-K partials [split][tile][chunk][4][128][4] (swap, S > 1)
+  // optional live row count on the device (compacted bucket bodies of the
+  // replanning graph): rows = min(rows_a, *rows_dev * rows_mul); row tiles
+  // past it are not visited (batched kernels only; null: rows_a)
+  const int* rows_dev;
+  int rows_mul;
   EpiArgs e;
 };
 

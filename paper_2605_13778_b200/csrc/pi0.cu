@@ -2326,6 +2326,16 @@ int build_replan(Handle& h, Replan& R, int n, const sf_verify_cfg_t* cfg, const 
     }
     return SF_OK;
   };
+  // a bucket body's GEMMs / attention visit only the live rows / envs (the
+  // compacted count on the device), not the bucket's padding; set for the
+  // capture only (the Buffers are shared with the plain entry points)
+  auto set_live = [&](Buffers& b, const int* cnt) {
+    for (auto& op : b.ops) {
+      op.p.rows_dev = cnt;
+      op.p.rows_mul = b.env_rows;
+    }
+    b.ap.envs_dev = cnt;
+  };
   auto end_body = [&](int brc, size_t i) {
     cudaGraph_t body = nullptr;
     const cudaError_t be = cudaStreamEndCapture(h.body_stream, &body);
@@ -2375,7 +2385,9 @@ int build_replan(Handle& h, Replan& R, int n, const sf_verify_cfg_t* cfg, const 
         const int gblocks = (bk * per + 255) / 256 < 1184 ? (bk * per + 255) / 256 : 1184;
         flash_gather_kernel<<<gblocks, 256, 0, bs>>>(gp);
         sf::count_launch(1);
+        set_live(b, R.fl_count);
         brc = enqueue_verify(h, b, cfg, bs, pdl, true);
+        set_live(b, nullptr);
         FlashScatterParams sp{R.fl_idx, R.fl_count, cfg->k, hd, b.result, b.branch, b.draft,
                               bf.result, bf.branch, bf.draft};
         const int sper = SF_RESULT_WORDS + cfg->k + hd;
@@ -2426,7 +2438,9 @@ int build_replan(Handle& h, Replan& R, int n, const sf_verify_cfg_t* cfg, const 
     const int gblocks = (bk * per + 255) / 256 < 1184 ? (bk * per + 255) / 256 : 1184;
     bucket_gather_kernel<<<gblocks, 256, 0, bs>>>(R.fb_idx, R.fb_count, bk, hd, c.state_dim, R.eps_d, bf.state,
                                                   b.draft, b.state, b.env_map);
+    set_live(b, R.fb_count);
     int brc = enqueue_denoise(h, b, pol->num_steps, bs, pdl);
+    set_live(b, nullptr);
     const int sblocks = (bk * hd + 255) / 256 < 1184 ? (bk * hd + 255) / 256 : 1184;
     bucket_scatter_kernel<<<sblocks, 256, 0, bs>>>(R.fb_idx, R.fb_count, hd, b.draft, b.status, R.chunk, R.bad);
     sf::count_launch(2);
